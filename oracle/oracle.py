@@ -1,0 +1,117 @@
+"""ctypes wrapper around oracle.c -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this module.  It never imports the CUDA package and
+the CUDA package never imports it.  See oracle.c for what is computed and the
+PAPER.md passages it follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+EINVAL, EDISCONNECTED, ELIMIT, ENOMEM = -1, -2, -3, -4
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", _LIB, _SRC])
+    return _LIB
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        lib.oracle_graph_build.restype = P
+        lib.oracle_graph_build.argtypes = [ctypes.c_uint32, ctypes.c_uint64, P, P, P, P, ctypes.c_int]
+        lib.oracle_graph_free.argtypes = [P]
+        lib.oracle_graph_arcs.restype = ctypes.c_uint64
+        lib.oracle_graph_arcs.argtypes = [P]
+        lib.oracle_match.restype = ctypes.c_int64
+        lib.oracle_match.argtypes = [P, ctypes.c_uint32, P, P, ctypes.c_uint32, P, P, P, P,
+                                     ctypes.c_uint64, ctypes.c_uint64]
+        _lib = lib
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class OracleGraph:
+    """The oracle's own adjacency, built from the raw edge list (never a CSR
+    produced by the CUDA path)."""
+
+    def __init__(self, g):
+        lib = _load()
+        self._keep = [np.ascontiguousarray(g.src, np.uint32), np.ascontiguousarray(g.dst, np.uint32),
+                      None if g.elab is None else np.ascontiguousarray(g.elab, np.uint16),
+                      None if g.vlab is None else np.ascontiguousarray(g.vlab, np.uint16)]
+        s, d, el, vl = self._keep
+        self.n = int(g.n)
+        self._h = lib.oracle_graph_build(self.n, s.shape[0], _ptr(s), _ptr(d), _ptr(el), _ptr(vl),
+                                         1 if g.undirected else 0)
+        if not self._h:
+            raise ValueError("oracle_graph_build rejected the input")
+        self._keep = None
+
+    @property
+    def arcs(self) -> int:
+        return int(_load().oracle_graph_arcs(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.oracle_graph_free(self._h)
+            self._h = None
+
+
+def _qarrays(q):
+    vl = np.array(q.vlabels, np.int32)
+    bd = np.array(q.bound, np.int64)
+    e = np.array(q.edges, np.int32).reshape(-1, 3)
+    return vl, bd, np.ascontiguousarray(e[:, 0]), np.ascontiguousarray(e[:, 1]), np.ascontiguousarray(e[:, 2])
+
+
+def count(og: OracleGraph, q, limit: int = 0) -> int:
+    """#Emb(Q, G); raises on error, returns -3 (ELIMIT) when count > limit > 0."""
+    vl, bd, a, b, lab = _qarrays(q)
+    r = _load().oracle_match(og._h, q.k, _ptr(vl), _ptr(bd), a.shape[0], _ptr(a), _ptr(b), _ptr(lab),
+                             None, 0, limit)
+    if r < 0 and r != ELIMIT:
+        raise ValueError(f"oracle error {r}")
+    return int(r)
+
+
+def match(og: OracleGraph, q, limit: int = 0) -> np.ndarray:
+    """All embeddings as a lexicographically sorted (R, k) uint32 array."""
+    c = count(og, q, limit)
+    if c == ELIMIT:
+        raise OverflowError("more than %d embeddings" % limit)
+    rows = np.zeros((max(c, 1), q.k), np.uint32)
+    vl, bd, a, b, lab = _qarrays(q)
+    r = _load().oracle_match(og._h, q.k, _ptr(vl), _ptr(bd), a.shape[0], _ptr(a), _ptr(b), _ptr(lab),
+                             _ptr(rows), c, 0)
+    assert r == c
+    rows = rows[:c]
+    return sort_rows(rows)
+
+
+def sort_rows(rows: np.ndarray) -> np.ndarray:
+    """Lexicographic row sort (plain numpy; used to compare sets of rows)."""
+    rows = np.ascontiguousarray(rows)
+    if rows.shape[0] == 0:
+        return rows
+    order = np.lexsort(rows.T[::-1])
+    return rows[order]
