@@ -1,0 +1,198 @@
+/*
+ * gpsense.h -- C-ABI boundary of the B200-native GpSense subgraph-matching hot path.
+ *
+ * Problem (PAPER.md §"Subgraph Similarity Search"): "Given a large data
+ * graph G and a query graph Q, we find all matches of Q in G"; a match is the
+ * injective, edge- and label-preserving map of Def. 2.  The calls
+ * below follow Alg. 1 FilteringAndJoining: inputs q and g, output
+ * "all matches of q in g", "a set of subgraph isomorphisms".
+ * Generalisations (directed labelled arcs, '*' wildcards, bound "concept"
+ * vertices P:592, non-induced, injective) are the readings R1-R9 in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *   - Every function returns gps_status (0 = GPS_OK, < 0 = error) except
+ *     gps_last_error / gps_result_free.  On error a thread-local message is
+ *     available from gps_last_error(); output arguments are left untouched
+ *     unless stated.
+ *   - Input arrays are BORROWED for the duration of the call and copied; the
+ *     caller keeps ownership.  Pointers are HOST pointers unless a flag says
+ *     otherwise.
+ *   - A gps_ctx is bound to one CUDA device and one stream; it is not
+ *     thread-safe.  A gps_graph is immutable after load and may be used by any
+ *     ctx on the same device.
+ *   - There is NO CPU fallback: every step of filtering and joining runs in the
+ *     library's sm_100a kernels; the only host work is validation, the query
+ *     plan ("the only step that runs on the CPU") and the join-order
+ *     choice.  Without a usable CUDA device gps_create fails with
+ *     GPS_ECUDA.
+ */
+#ifndef GPSENSE_H
+#define GPSENSE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GPS_API __attribute__((visibility("default")))
+#else
+#define GPS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GPS_OK = 0,
+    GPS_EINVAL = -1,         /* malformed argument (see each call) */
+    GPS_EDISCONNECTED = -2,  /* query skeleton not connected */
+    GPS_ENOMEM = -3,         /* device or host allocation failed */
+    GPS_ECUDA = -4,          /* CUDA runtime / launch failure */
+    GPS_ENCCL = -5,          /* reserved: collective failure */
+    GPS_EOVERFLOW = -6,      /* result does not fit the caller's buffer / 32-bit tables */
+    GPS_EUNSUPPORTED = -7    /* graph beyond the packed-arc layout (n << b >= 2^32, m >= 2^32) */
+} gps_status;
+
+#define GPS_ANY (-1)         /* wildcard vertex / edge label ('*'; variable edge P:594) */
+#define GPS_FREE (-1)        /* unbound query vertex (variable node P:592) */
+#define GPS_MAX_QV 32        /* max query vertices */
+#define GPS_MAX_QE 64        /* max query arcs */
+
+/* gps_csr_desc.flags */
+#define GPS_DIRECTED 0u
+#define GPS_UNDIRECTED 1u    /* each listed arc is an unordered edge: the library symmetrises it */
+
+typedef struct gps_ctx gps_ctx;
+typedef struct gps_graph gps_graph;
+typedef struct gps_result gps_result;
+
+typedef struct {
+    int device;              /* CUDA ordinal */
+    void* stream;            /* cudaStream_t to run on (e.g. torch.cuda.current_stream().cuda_stream);
+                                NULL = the library creates its own non-blocking stream */
+    void* nccl_comm;         /* reserved (row-sharded join); must be NULL */
+    int rank, world;         /* reserved; world <= 1 */
+} gps_ctx_opts;
+
+/* Data graph as CSR ("nodes array ... edges array ... two additional
+ * arrays ... labels of nodes and edges").  Rows need not be sorted; duplicate
+ * (src, dst, label) arcs are collapsed (set semantics, reading R5).
+ *   offsets        [n_vertices+1] u64, offsets[0] = 0, non-decreasing, offsets[n] = n_arcs
+ *   targets        [n_arcs] u32 < n_vertices
+ *   edge_labels    [n_arcs] u16 or NULL (all 0)
+ *   vertex_labels  [n_vertices] u16 or NULL (all 0; commonsense graphs "contain no node labels")
+ * Errors: GPS_EINVAL (bad offsets / target >= n / n = 0), GPS_EUNSUPPORTED
+ * ((n-1) << b >= 2^32 with b = bits of the largest edge label, or >= 2^32 stored arcs). */
+typedef struct {
+    uint32_t n_vertices;
+    uint64_t n_arcs;
+    const uint64_t* offsets;
+    const uint32_t* targets;
+    const uint16_t* edge_labels;
+    const uint16_t* vertex_labels;
+    uint32_t flags;
+} gps_csr_desc;
+
+/* One query arc src -> dst with an edge label or GPS_ANY.  No self-loops. */
+typedef struct { int32_t src, dst, label; } gps_qedge;
+
+/* Query graph (P:580-594 concept / variable nodes, labelled / variable edges).
+ *   vertex_labels [n_vertices] label or GPS_ANY (NULL = all GPS_ANY)
+ *   bound         [n_vertices] data id or GPS_FREE (NULL = all free)
+ *   edges         [n_edges]
+ * Errors: GPS_EINVAL (k = 0, k > 32, e > 64, endpoint >= k, self-loop,
+ * bound id >= n), GPS_EDISCONNECTED (k > 1 and skeleton not connected). */
+typedef struct {
+    uint32_t n_vertices, n_edges;
+    const int32_t* vertex_labels;
+    const int64_t* bound;
+    const gps_qedge* edges;
+} gps_query;
+
+/* Knobs of the method (NULL = defaults from gps_default_opts). */
+typedef struct {
+    uint32_t refine_rounds;      /* refinement rounds after initialisation; default 1 */
+    int32_t reverse_refine;      /* refine in reversed visit order; default 1 */
+    uint32_t lowconn_threshold;  /* query degree <= this is "low connectivity"; default 1 */
+    int32_t result_on_device;    /* gps_match: 1 = rows stay in device memory (default), 0 = host copy */
+} gps_match_opts;
+
+GPS_API gps_status gps_default_opts(gps_match_opts* opts);
+
+GPS_API gps_status gps_create(const gps_ctx_opts* opts, gps_ctx** out);
+/* Frees the ctx and the device memory of any gps_result it still owns. */
+GPS_API gps_status gps_destroy(gps_ctx* ctx);
+
+/* a0: copies the CSR to the device, sorts + de-duplicates
+ * every row, builds the incoming CSR ("both incoming and outgoing graph
+ * representations") and the vertex-label histogram freq(label). */
+GPS_API gps_status gps_load_data_graph(gps_ctx* ctx, const gps_csr_desc* desc, gps_graph** out);
+GPS_API gps_status gps_free_graph(gps_graph* g);
+/* n, stored arcs (after de-duplication / symmetrisation), #vertex labels, edge-label bits. */
+GPS_API gps_status gps_graph_info(const gps_graph* g, uint32_t* n, uint64_t* arcs, uint32_t* n_vlabels,
+                          uint32_t* elabel_bits);
+
+/* Alg. 1 end to end: plan (host) -> filter (check, collect, explore, refine)
+ * -> collect edge candidates -> combine.  *out receives all embeddings as
+ * row-major uint32 rows x k, column j = image of query vertex j, rows in an
+ * unspecified but deterministic order (reading R25).  Empty result is GPS_OK
+ * with rows = 0. */
+GPS_API gps_status gps_match(gps_ctx* ctx, const gps_graph* g, const gps_query* q,
+                     const gps_match_opts* opts, gps_result** out);
+/* Same, writing rows into a caller-owned HOST buffer of cap_rows x k uint32
+ * (pinned memory recommended).  *rows = #embeddings; GPS_EOVERFLOW (with *rows
+ * set) if it exceeds cap_rows (nothing written then). */
+GPS_API gps_status gps_match_host(gps_ctx* ctx, const gps_graph* g, const gps_query* q,
+                          const gps_match_opts* opts, uint32_t* host_out, uint64_t cap_rows,
+                          uint64_t* rows);
+/* #embeddings; the last join level is counted, never written. */
+GPS_API gps_status gps_count(gps_ctx* ctx, const gps_graph* g, const gps_query* q,
+                     const gps_match_opts* opts, uint64_t* count);
+
+/* rows, cols (= k), data (device or host pointer, owned by the result), on_device. */
+GPS_API gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols,
+                           const uint32_t** data, int* on_device);
+GPS_API void gps_result_free(gps_result* r);
+
+GPS_API const char* gps_last_error(void);
+
+/* ---- introspection (tests, bench) ------------------------------------- */
+
+/* Kernel classes for stats / profiling. */
+enum {
+    GPS_K_CHECK = 0, GPS_K_COLLECT, GPS_K_EXPLORE, GPS_K_BITAND, GPS_K_EC_COUNT, GPS_K_EC_WRITE,
+    GPS_K_SCAN, GPS_K_JOIN_LEN, GPS_K_JOIN_COUNT, GPS_K_JOIN_WRITE, GPS_K_LOAD, GPS_K_NCLASSES
+};
+
+typedef struct {
+    uint64_t queries;                      /* gps_match / gps_count calls completed */
+    uint64_t embeddings;                   /* rows produced / counted */
+    uint64_t launches;                     /* kernels launched by this ctx */
+    uint64_t host_syncs;                   /* stream synchronisations */
+    uint64_t k_launches[GPS_K_NCLASSES];   /* per kernel class */
+    double k_bytes[GPS_K_NCLASSES];        /* algorithmic bytes */
+    double k_ms[GPS_K_NCLASSES];           /* CUDA-event time, only for profiled classes */
+    uint64_t k_timed[GPS_K_NCLASSES];      /* launches that were event-timed */
+} gps_stats;
+
+GPS_API gps_status gps_get_stats(gps_ctx* ctx, gps_stats* out);   /* synchronises the ctx stream */
+GPS_API gps_status gps_reset_stats(gps_ctx* ctx);
+/* Event-time every launch of the classes in class_mask (bit i = class i) on the ctx stream. */
+GPS_API gps_status gps_set_profiling(gps_ctx* ctx, uint32_t class_mask);
+
+/* Query plan: visit order O (order_out[k], *n_order entries),
+ * ranking f(u) = deg(u) / freq(u.label) as unreduced (deg, freq) pairs
+ * (rank_out[2k]). */
+GPS_API gps_status gps_debug_plan(gps_ctx* ctx, const gps_graph* g, const gps_query* q,
+                          const gps_match_opts* opts, int32_t* order_out, uint32_t* n_order,
+                          uint64_t* rank_out);
+/* Candidate bitmaps c_set (Alg. 2) after stage 0 = kernel_check, 1 = initialisation
+ * (explore over T), 2 = refinement.  bitmaps_out: k x ceil(n/32) uint32 host
+ * words, bit v of row u = "v is a candidate of u". */
+GPS_API gps_status gps_debug_candidates(gps_ctx* ctx, const gps_graph* g, const gps_query* q,
+                                const gps_match_opts* opts, int stage, uint32_t* bitmaps_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPSENSE_H */

@@ -1,0 +1,190 @@
+// internal.cuh -- shared declarations of libgpsense (CUDA path).  Never included by oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gpsense.h"
+
+namespace gps {
+
+constexpr int kWarp = 32;
+constexpr uint32_t kFull = 0xffffffffu;
+
+// ---- errors ---------------------------------------------------------------
+struct Error {
+    gps_status status;
+    std::string msg;
+};
+void set_last_error(const std::string& m);
+[[noreturn]] void fail(gps_status s, const std::string& m);
+void check_cuda(cudaError_t e, const char* what, const char* file, int line);
+#define GPS_CK(x) ::gps::check_cuda((x), #x, __FILE__, __LINE__)
+
+// ---- device views (POD, passed by value to kernels) ----------------------
+// Packed arc word: (dst << lbits) | elabel; rows sorted
+// ascending by the word = by (dst, label), de-duplicated.
+struct DevGraph {
+    uint32_t n;       // #vertices
+    uint32_t nw;      // ceil(n / 32) bitmap words actually used
+    uint32_t nws;     // bitmap row stride in words (nw rounded up to 64)
+    uint32_t lbits;   // bits of the edge label in an arc word
+    uint32_t lmask;   // (1 << lbits) - 1
+    const uint32_t* off_out;  // [n+1]
+    const uint32_t* arc_out;  // [m]
+    const uint32_t* off_in;   // [n+1]
+    const uint32_t* arc_in;   // [m]
+    const uint16_t* vlab;     // [n]
+};
+
+__device__ __forceinline__ bool bit_test(const uint32_t* __restrict__ B, uint32_t v) {
+    return (__ldg(B + (v >> 5)) >> (v & 31)) & 1u;
+}
+// Rank of v among the set bits of bitmap B (v must be set): rp = per-word exclusive prefix.
+__device__ __forceinline__ uint32_t bit_rank(const uint32_t* __restrict__ B, const uint32_t* __restrict__ rp,
+                                             uint32_t v) {
+    uint32_t w = v >> 5;
+    return __ldg(rp + w) + __popc(__ldg(B + w) & ((1u << (v & 31)) - 1u));
+}
+__device__ __forceinline__ bool lab_ok(uint32_t arc, uint32_t lmask, int32_t lab) {
+    return lab < 0 || (arc & lmask) == (uint32_t)lab;
+}
+
+// ---- context ----------------------------------------------------------------
+struct PendingTiming {
+    int cls;
+    cudaEvent_t e0, e1;
+};
+
+}  // namespace gps
+
+struct gps_ctx {
+    int device = 0;
+    int nsm = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint32_t prof_mask = 0;
+    gps_stats stats{};
+    std::vector<gps::PendingTiming> pending;
+    std::vector<cudaEvent_t> event_pool;
+    unsigned long long* d_bytes = nullptr;   // [GPS_K_NCLASSES] device-accumulated algorithmic bytes
+    uint64_t* d_info = nullptr;              // small device scratch (counts, totals)
+    uint64_t* h_info = nullptr;              // pinned mirror
+    unsigned int* d_done = nullptr;          // last-block counters
+    std::vector<gps_result*> results;        // live device results (freed at destroy)
+};
+
+struct gps_graph {
+    int device = 0;
+    gps::DevGraph d{};
+    uint64_t m = 0;              // stored arcs (per direction)
+    bool undirected = false;
+    uint32_t n_vlabels = 1;
+    std::vector<uint64_t> lab_hist;   // freq(label)
+    void* mem[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+struct gps_result {
+    uint64_t rows = 0;
+    uint32_t cols = 0;
+    uint32_t* data = nullptr;
+    int on_device = 0;
+    gps_ctx* ctx = nullptr;
+};
+
+namespace gps {
+
+// ---- launch helper: stats, optional CUDA-event timing --------------------
+cudaEvent_t ctx_event(gps_ctx* c);
+void ctx_harvest(gps_ctx* c);          // after a stream sync: fold finished event pairs into stats
+void ctx_sync(gps_ctx* c);             // stream sync + harvest
+
+template <typename Kernel, typename... Args>
+inline void launch(gps_ctx* c, int cls, dim3 grid, dim3 block, size_t smem, Kernel k, Args... args) {
+    if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
+    bool timed = (c->prof_mask >> cls) & 1u;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) {
+        e0 = ctx_event(c);
+        e1 = ctx_event(c);
+        GPS_CK(cudaEventRecord(e0, c->stream));
+    }
+    k<<<grid, block, smem, c->stream>>>(args...);
+    GPS_CK(cudaGetLastError());
+    if (timed) {
+        GPS_CK(cudaEventRecord(e1, c->stream));
+        c->pending.push_back({cls, e0, e1});
+    }
+    c->stats.launches++;
+    c->stats.k_launches[cls]++;
+}
+
+// ---- stream-ordered device memory -----------------------------------------
+void* dmalloc(gps_ctx* c, size_t bytes);
+void dfree(gps_ctx* c, void* p);
+template <typename T>
+T* dalloc(gps_ctx* c, size_t count) {
+    return static_cast<T*>(dmalloc(c, count * sizeof(T) + 16));
+}
+struct DevPtr {  // RAII stream-ordered buffer
+    gps_ctx* c = nullptr;
+    void* p = nullptr;
+    DevPtr() = default;
+    DevPtr(gps_ctx* ctx, size_t bytes) : c(ctx), p(dmalloc(ctx, bytes)) {}
+    DevPtr(const DevPtr&) = delete;
+    DevPtr& operator=(const DevPtr&) = delete;
+    DevPtr(DevPtr&& o) noexcept : c(o.c), p(o.p) { o.p = nullptr; }
+    DevPtr& operator=(DevPtr&& o) noexcept {
+        reset();
+        c = o.c;
+        p = o.p;
+        o.p = nullptr;
+        return *this;
+    }
+    ~DevPtr() { reset(); }
+    void reset() {
+        if (p) dfree(c, p);
+        p = nullptr;
+    }
+    void* release() {
+        void* q = p;
+        p = nullptr;
+        return q;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// ---- primitives (scan.cu, sort.cu) ------------------------------------------
+// Exclusive scan of nseg independent arrays: out[s][0..n[s]] (n[s]+1 entries,
+// out[s][n[s]] = total).  TI/TO in {u32->u32, u32->u64, u64->u64}.
+constexpr int kMaxScanSeg = 64;
+template <typename TI, typename TO>
+struct ScanBatch {
+    int nseg;
+    const TI* in[kMaxScanSeg];
+    TO* out[kMaxScanSeg];
+    uint64_t n[kMaxScanSeg];
+};
+template <typename TI, typename TO>
+void scan_exclusive(gps_ctx* c, const ScanBatch<TI, TO>& b);
+template <typename TI, typename TO>
+inline void scan_exclusive1(gps_ctx* c, const TI* in, TO* out, uint64_t n) {
+    ScanBatch<TI, TO> b{};
+    b.nseg = 1;
+    b.in[0] = in;
+    b.out[0] = out;
+    b.n[0] = n;
+    scan_exclusive(c, b);
+}
+// LSD radix sort of u64 keys on bits [0, nbits); result in *keys (ping-pong with tmp).
+void radix_sort_u64(gps_ctx* c, uint64_t* keys, uint64_t* tmp, uint64_t n, int nbits);
+
+// ---- graph load (load.cu) ---------------------------------------------------
+void load_graph(gps_ctx* c, const gps_csr_desc* desc, gps_graph* g);
+void free_graph_mem(gps_graph* g);
+
+}  // namespace gps

@@ -1,0 +1,111 @@
+// kernels.cuh -- argument blocks and host launchers of the per-query kernels
+// (filter.cu, join.cu).  Row numbers refer to SURVEY.md §8(a).
+#pragma once
+#include "internal.cuh"
+
+namespace gps {
+
+// ---- a2 kernel_check (Def. 3; Alg. 2 line 7 P:723) -------------------
+struct QDesc {
+    int k;
+    int32_t lab[GPS_MAX_QV];     // vertex label or -1
+    int64_t bound[GPS_MAX_QV];   // bound data id or -1
+    uint32_t qout[GPS_MAX_QV];   // required out-degree
+    uint32_t qin[GPS_MAX_QV];    // required in-degree
+};
+void run_check(gps_ctx* c, const DevGraph& g, const QDesc& q, uint32_t* B);
+
+// ---- a3 kernel_collect ----------------------------------
+// For each listed query vertex u: c_array[u] (sorted candidate ids), rank
+// prefix rp[u][w] (exclusive popcount prefix per bitmap word, rp[u][nw] = |C(u)|)
+// and cnt[u] = |C(u)|.
+struct CollectArgs {
+    int nu;
+    const uint32_t* B[GPS_MAX_QV];
+    uint32_t* rp[GPS_MAX_QV];
+    uint32_t* carr[GPS_MAX_QV];
+    uint32_t* cnt[GPS_MAX_QV];
+};
+void run_collect(gps_ctx* c, const DevGraph& g, const CollectArgs& a);
+
+// ---- a4/a5 kernel_explore (Alg. 2 lines 14-22) ---------
+// Constraint of a candidate u' of u for one query arc between u and v:
+// adj_dir(u') must hold some v' != u' with a fitting label and v' in B[v].
+struct Cons {
+    const uint32_t* Bv;   // bitmap of the neighbour v
+    uint32_t* X;          // propagation scratch for v (nullptr = prune only)
+    int32_t lab;          // edge label or -1
+    int dir;              // 0: arc u -> v (out-adjacency of u'), 1: arc v -> u (in-adjacency)
+};
+struct ExploreArgs {
+    int nc;
+    Cons c[GPS_MAX_QE];
+    const uint32_t* cands;  // c_array[u]
+    const uint32_t* cnt;    // device |C(u)|
+    uint32_t* Bu;           // bitmap of u (pruned bits cleared)
+};
+void run_explore(gps_ctx* c, const DevGraph& g, const ExploreArgs& a, uint32_t max_cands);
+
+// B[v] &= X_1 & X_2 & ... (each listed scratch), then the scratch is zeroed.
+struct AndArgs {
+    int nt;
+    uint32_t* B[GPS_MAX_QE];
+    int xbeg[GPS_MAX_QE + 1];
+    uint32_t* X[GPS_MAX_QE];
+};
+void run_bitand(gps_ctx* c, const DevGraph& g, const AndArgs& a);
+
+// ---- a6 collect_edge_candidates, two-step -----------------------
+struct ECArc {
+    const uint32_t* keys;   // c_array of the key endpoint p
+    uint32_t nkeys;         // |C(p)|
+    int dir;                // 0: values are out-neighbours of the key, 1: in-neighbours
+    int32_t lab;
+    const uint32_t* Bq;     // bitmap of the value endpoint q
+    uint32_t* cnt;          // [nkeys] count pass output
+    const uint32_t* off;    // [nkeys+1] exclusive scan of cnt (write pass)
+    uint32_t* val;          // [total] write pass output
+};
+struct ECArgs {
+    int na;
+    ECArc a[GPS_MAX_QE];
+};
+void run_ec(gps_ctx* c, const DevGraph& g, const ECArgs& a, bool write, uint32_t max_keys);
+
+// ---- a8 join step: count -> scan -> write ----------------
+struct CloseChk {          // fused closing arc p -> q: value(q) must be in EC(p->q)[value(p)]
+    int key_new;           // key endpoint is the vertex added by this step
+    uint32_t key_col;      // else its column in the input table
+    int tgt_new;
+    uint32_t tgt_col;
+    const uint32_t* Bk;    // bitmap + rank prefix of the key endpoint
+    const uint32_t* rpk;
+    const uint32_t* off;   // EC offsets / values of the closing arc
+    const uint32_t* val;
+};
+struct StepArgs {
+    const uint32_t* M;     // input table, row-major R x w
+    uint32_t w;
+    uint64_t R;
+    uint32_t x_col;        // column of the visited endpoint (EC key)
+    const uint32_t* Bx;
+    const uint32_t* rpx;
+    const uint32_t* ec_off;
+    const uint32_t* ec_val;
+    int nclose;
+    CloseChk cl[GPS_MAX_QE];
+    const uint32_t* s0;    // [R] segment start of each row in ec_val
+    const uint64_t* poff;  // [R+1] exclusive scan of segment lengths (pair space)
+    uint64_t* blk;         // [G+1] per-block valid counts -> exclusive offsets
+    uint64_t* info;        // [0] = #pairs P, [1] = #output rows
+    unsigned int* done;    // last-block counter (self-resetting)
+    uint32_t* out;         // output table
+    uint32_t wout;         // output width (w + 1)
+    int final_;            // write in query-vertex order via perm
+    uint8_t perm[GPS_MAX_QV + 1];
+};
+void run_join_len(gps_ctx* c, const StepArgs& s, uint32_t* len);
+void run_join_count(gps_ctx* c, const StepArgs& s, uint32_t G);
+void run_join_write(gps_ctx* c, const StepArgs& s, uint32_t G);
+
+}  // namespace gps

@@ -1,0 +1,320 @@
+"""Thin ctypes binding of include/gpsense.h (argument marshalling only).
+
+Every step of filtering and joining runs in libgpsense.so's sm_100a kernels; this
+module only converts Python/numpy/torch arguments into the C structs and wraps
+results.  PyTorch is used for device memory views (zero-copy via
+__cuda_array_interface__) and streams.  There is no CPU fallback: if the CUDA
+library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgpsense.so")
+
+GPS_OK, GPS_EINVAL, GPS_EDISCONNECTED, GPS_ENOMEM, GPS_ECUDA, GPS_ENCCL, GPS_EOVERFLOW, GPS_EUNSUPPORTED = (
+    0, -1, -2, -3, -4, -5, -6, -7)
+GPS_ANY = -1
+GPS_FREE = -1
+GPS_DIRECTED, GPS_UNDIRECTED = 0, 1
+KERNEL_CLASSES = ["check", "collect", "explore", "bitand", "ec_count", "ec_write", "scan", "join_len",
+                  "join_count", "join_write", "load"]
+NK = len(KERNEL_CLASSES)
+K = {name: i for i, name in enumerate(KERNEL_CLASSES)}
+
+_STATUS = {GPS_EINVAL: "EINVAL", GPS_EDISCONNECTED: "EDISCONNECTED", GPS_ENOMEM: "ENOMEM",
+           GPS_ECUDA: "ECUDA", GPS_ENCCL: "ENCCL", GPS_EOVERFLOW: "EOVERFLOW",
+           GPS_EUNSUPPORTED: "EUNSUPPORTED"}
+
+
+class GpsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"gps error {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class CtxOpts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p),
+                ("rank", ctypes.c_int), ("world", ctypes.c_int)]
+
+
+class CsrDesc(ctypes.Structure):
+    _fields_ = [("n_vertices", ctypes.c_uint32), ("n_arcs", ctypes.c_uint64),
+                ("offsets", ctypes.c_void_p), ("targets", ctypes.c_void_p),
+                ("edge_labels", ctypes.c_void_p), ("vertex_labels", ctypes.c_void_p),
+                ("flags", ctypes.c_uint32)]
+
+
+class QEdge(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_int32), ("dst", ctypes.c_int32), ("label", ctypes.c_int32)]
+
+
+class QueryDesc(ctypes.Structure):
+    _fields_ = [("n_vertices", ctypes.c_uint32), ("n_edges", ctypes.c_uint32),
+                ("vertex_labels", ctypes.c_void_p), ("bound", ctypes.c_void_p),
+                ("edges", ctypes.c_void_p)]
+
+
+class MatchOpts(ctypes.Structure):
+    _fields_ = [("refine_rounds", ctypes.c_uint32), ("reverse_refine", ctypes.c_int32),
+                ("lowconn_threshold", ctypes.c_uint32), ("result_on_device", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("queries", ctypes.c_uint64), ("embeddings", ctypes.c_uint64),
+                ("launches", ctypes.c_uint64), ("host_syncs", ctypes.c_uint64),
+                ("k_launches", ctypes.c_uint64 * NK), ("k_bytes", ctypes.c_double * NK),
+                ("k_ms", ctypes.c_double * NK), ("k_timed", ctypes.c_uint64 * NK)]
+
+
+def _load_lib():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() (nvcc, sm_100a); "
+                          "there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    S = ctypes.c_int
+    sig = {
+        "gps_default_opts": (S, [P]),
+        "gps_create": (S, [P, P]),
+        "gps_destroy": (S, [P]),
+        "gps_load_data_graph": (S, [P, P, P]),
+        "gps_free_graph": (S, [P]),
+        "gps_graph_info": (S, [P, P, P, P, P]),
+        "gps_match": (S, [P, P, P, P, P]),
+        "gps_match_host": (S, [P, P, P, P, P, ctypes.c_uint64, P]),
+        "gps_count": (S, [P, P, P, P, P]),
+        "gps_result_info": (S, [P, P, P, P, P]),
+        "gps_result_free": (None, [P]),
+        "gps_last_error": (ctypes.c_char_p, []),
+        "gps_get_stats": (S, [P, P]),
+        "gps_reset_stats": (S, [P]),
+        "gps_set_profiling": (S, [P, ctypes.c_uint32]),
+        "gps_debug_plan": (S, [P, P, P, P, P, P, P]),
+        "gps_debug_candidates": (S, [P, P, P, P, S, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load_lib()
+EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_graph", "gps_free_graph",
+            "gps_graph_info", "gps_match", "gps_match_host", "gps_count", "gps_result_info",
+            "gps_result_free", "gps_last_error", "gps_get_stats", "gps_reset_stats",
+            "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates"]
+
+
+def _check(st: int):
+    if st != GPS_OK:
+        raise GpsError(st, (lib.gps_last_error() or b"").decode())
+
+
+def _addr(a) -> Optional[int]:
+    return None if a is None else a.ctypes.data
+
+
+def default_opts(**kw) -> MatchOpts:
+    o = MatchOpts()
+    _check(lib.gps_default_opts(ctypes.byref(o)))
+    for k_, v in kw.items():
+        setattr(o, k_, int(v))
+    return o
+
+
+class _QueryArrays:
+    """Keeps the numpy buffers behind a QueryDesc alive."""
+
+    def __init__(self, q):
+        if isinstance(q, dict):
+            k, vl, bd, edges = q["k"], q["vlabels"], q["bound"], q["edges"]
+        else:
+            k, vl, bd, edges = q.k, q.vlabels, q.bound, q.edges
+        self.vl = np.ascontiguousarray(np.asarray(vl, np.int32).reshape(-1))
+        self.bd = np.ascontiguousarray(np.asarray(bd, np.int64).reshape(-1))
+        e = np.asarray(edges, np.int32).reshape(-1, 3)
+        self.e = np.ascontiguousarray(e)
+        self.k = int(k)
+        self.desc = QueryDesc(self.k, int(self.e.shape[0]), _addr(self.vl), _addr(self.bd),
+                              _addr(self.e) if self.e.shape[0] else None)
+
+
+class _DeviceRows:
+    """Owner of a device gps_result; exposes __cuda_array_interface__ for torch."""
+
+    def __init__(self, res, rows, cols, ptr):
+        self._res = res
+        self.__cuda_array_interface__ = {"shape": (int(rows), int(cols)), "typestr": "<u4",
+                                         "data": (int(ptr), False), "version": 3, "strides": None,
+                                         "stream": None}
+
+    def __del__(self):
+        if self._res:
+            lib.gps_result_free(self._res)
+            self._res = None
+
+
+class Graph:
+    def __init__(self, ctx: "Context", handle):
+        self.ctx = ctx
+        self._h = handle
+        n, m, nvl, lb = ctypes.c_uint32(), ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint32()
+        _check(lib.gps_graph_info(handle, ctypes.byref(n), ctypes.byref(m), ctypes.byref(nvl), ctypes.byref(lb)))
+        self.n, self.arcs, self.n_vlabels, self.elabel_bits = n.value, m.value, nvl.value, lb.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h:
+            lib.gps_free_graph(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Context:
+    """One gps_ctx: a device and a stream (default: a library-owned stream)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        o = CtxOpts(device, None, None, 0, 1)
+        if stream is not None:
+            o.stream = int(getattr(stream, "cuda_stream", stream))
+        h = ctypes.c_void_p()
+        _check(lib.gps_create(ctypes.byref(o), ctypes.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if self._h:
+            lib.gps_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- graph ----
+    def load_graph_csr(self, n, offsets, targets, edge_labels=None, vertex_labels=None,
+                       undirected=False) -> Graph:
+        off = np.ascontiguousarray(offsets, np.uint64)
+        tgt = np.ascontiguousarray(targets, np.uint32)
+        el = None if edge_labels is None else np.ascontiguousarray(edge_labels, np.uint16)
+        vl = None if vertex_labels is None else np.ascontiguousarray(vertex_labels, np.uint16)
+        d = CsrDesc(int(n), int(tgt.shape[0]), _addr(off), _addr(tgt), _addr(el), _addr(vl),
+                    GPS_UNDIRECTED if undirected else GPS_DIRECTED)
+        h = ctypes.c_void_p()
+        _check(lib.gps_load_data_graph(self._h, ctypes.byref(d), ctypes.byref(h)))
+        return Graph(self, h)
+
+    def load_graph(self, g) -> Graph:
+        """From a synth.DataGraph-like object (n, to_csr(), vlab, undirected)."""
+        off, tgt, el = g.to_csr()
+        return self.load_graph_csr(g.n, off, tgt, el, g.vlab, g.undirected)
+
+    # ---- queries ----
+    def match(self, graph: Graph, q, opts: Optional[MatchOpts] = None, device: bool = True):
+        """All embeddings: torch uint32 (rows, k) CUDA tensor (device=True) or numpy array."""
+        qa = _QueryArrays(q)
+        o = opts if opts is not None else default_opts()
+        o = MatchOpts(o.refine_rounds, o.reverse_refine, o.lowconn_threshold, 1 if device else 0)
+        res = ctypes.c_void_p()
+        _check(lib.gps_match(self._h, graph.handle, ctypes.byref(qa.desc), ctypes.byref(o), ctypes.byref(res)))
+        rows, cols, ptr, ondev = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_void_p(), ctypes.c_int()
+        _check(lib.gps_result_info(res, ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(ptr),
+                                   ctypes.byref(ondev)))
+        if device:
+            import torch
+            holder = _DeviceRows(res, rows.value, cols.value, ptr.value)
+            if rows.value == 0:
+                del holder
+                return torch.empty((0, cols.value), dtype=torch.uint32, device=f"cuda:{self.device}")
+            return torch.as_tensor(holder, device=f"cuda:{self.device}")
+        try:
+            n = rows.value * cols.value
+            if n == 0:
+                return np.zeros((0, cols.value), np.uint32)
+            buf = (ctypes.c_uint32 * n).from_address(ptr.value)
+            return np.frombuffer(buf, dtype=np.uint32).reshape(rows.value, cols.value).copy()
+        finally:
+            lib.gps_result_free(res)
+
+    def match_host(self, graph: Graph, q, out=None, opts: Optional[MatchOpts] = None):
+        """Rows into a caller-owned host buffer (numpy uint32 or pinned torch tensor).
+
+        Returns the (rows, k) view of `out`; raises GpsError(EOVERFLOW) if it is too small.
+        """
+        qa = _QueryArrays(q)
+        if out is None:
+            out = np.zeros((1 << 16, qa.k), np.uint32)
+        if hasattr(out, "data_ptr"):
+            ptr, cap = out.data_ptr(), out.numel() // qa.k
+        else:
+            ptr, cap = out.ctypes.data, out.size // qa.k
+        rows = ctypes.c_uint64()
+        o = opts if opts is not None else default_opts()
+        _check(lib.gps_match_host(self._h, graph.handle, ctypes.byref(qa.desc), ctypes.byref(o),
+                                  ctypes.c_void_p(ptr), cap, ctypes.byref(rows)))
+        flat = out.reshape(-1) if not hasattr(out, "data_ptr") else out.view(-1)
+        return flat[: rows.value * qa.k].reshape(rows.value, qa.k)
+
+    def count(self, graph: Graph, q, opts: Optional[MatchOpts] = None) -> int:
+        qa = _QueryArrays(q)
+        c = ctypes.c_uint64()
+        _check(lib.gps_count(self._h, graph.handle, ctypes.byref(qa.desc),
+                             ctypes.byref(opts) if opts is not None else None, ctypes.byref(c)))
+        return int(c.value)
+
+    # ---- introspection ----
+    def plan(self, graph: Graph, q, opts: Optional[MatchOpts] = None):
+        qa = _QueryArrays(q)
+        order = np.zeros(32, np.int32)
+        n = ctypes.c_uint32()
+        rank = np.zeros(64, np.uint64)
+        _check(lib.gps_debug_plan(self._h, graph.handle, ctypes.byref(qa.desc),
+                                  ctypes.byref(opts) if opts is not None else None,
+                                  ctypes.c_void_p(order.ctypes.data), ctypes.byref(n),
+                                  ctypes.c_void_p(rank.ctypes.data)))
+        return order[: n.value].tolist(), [(int(rank[2 * u]), int(rank[2 * u + 1])) for u in range(qa.k)]
+
+    def candidates(self, graph: Graph, q, stage: int, opts: Optional[MatchOpts] = None) -> np.ndarray:
+        """Candidate bitmaps after stage 0/1/2 as a (k, n) bool array."""
+        qa = _QueryArrays(q)
+        nw = (graph.n + 31) // 32
+        buf = np.zeros((qa.k, nw), np.uint32)
+        _check(lib.gps_debug_candidates(self._h, graph.handle, ctypes.byref(qa.desc),
+                                        ctypes.byref(opts) if opts is not None else None, int(stage),
+                                        ctypes.c_void_p(buf.ctypes.data)))
+        bits = np.unpackbits(buf.view(np.uint8).reshape(qa.k, -1), axis=1, bitorder="little")
+        return bits[:, : graph.n].astype(bool)
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib.gps_get_stats(self._h, ctypes.byref(s)))
+        return {"queries": s.queries, "embeddings": s.embeddings, "launches": s.launches,
+                "host_syncs": s.host_syncs,
+                "kernels": {name: {"launches": s.k_launches[i], "bytes": s.k_bytes[i], "ms": s.k_ms[i],
+                                   "timed": s.k_timed[i]} for i, name in enumerate(KERNEL_CLASSES)}}
+
+    def reset_stats(self):
+        _check(lib.gps_reset_stats(self._h))
+
+    def set_profiling(self, classes):
+        mask = 0
+        for c in classes:
+            mask |= 1 << (K[c] if isinstance(c, str) else int(c))
+        _check(lib.gps_set_profiling(self._h, mask))

@@ -1,0 +1,71 @@
+"""Generate the stored benchmark query sets (calls only synth/ and oracle/).
+
+cfg2: 6-vertex BFS *tree* queries from top-decile seeds, max 2 children
+per BFS expansion, vertex labels kept with prob 0.5 (else '*'), edge labels kept;
+accepted iff 10^3 <= #Emb <= 10^6 by the CPU oracle (count with a limit).
+Seeds 2000+i in order; the first 100 accepted are stored with their oracle counts.
+
+Usage: python scripts/gen_queries.py cfg2 [n_queries]
+Writes synth/data/<cfg>_queries.json.  Never touches the CUDA path.
+"""
+import json
+import multiprocessing as mp
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from synth import bfs_query, config_graph  # noqa: E402
+from oracle import oracle  # noqa: E402
+
+RECIPES = {
+    "cfg2": dict(cfg=2, k=6, seed0=2000, induced=False, max_children=2, p_wild_v=0.5,
+                 lo=10**3, hi=10**6),
+}
+
+_G = None
+_OG = None
+
+
+def _init(cfg):
+    global _G, _OG
+    _G = config_graph(cfg)
+    _OG = oracle.OracleGraph(_G)
+
+
+def _try(args):
+    seed, r = args
+    q = bfs_query(_G, r["k"], seed, induced=r["induced"], max_children=r["max_children"],
+                  p_wild_v=r["p_wild_v"])
+    t = time.time()
+    c = oracle.count(_OG, q, limit=r["hi"])
+    return seed, q.to_json(), c, time.time() - t
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+    want = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+    r = RECIPES[name]
+    out = []
+    seed = r["seed0"]
+    with mp.Pool(min(8, os.cpu_count() or 1), initializer=_init, initargs=(r["cfg"],)) as pool:
+        while len(out) < want:
+            batch = [(s, r) for s in range(seed, seed + 32)]
+            seed += 32
+            for s, qj, c, dt in pool.map(_try, batch):
+                if r["lo"] <= c <= r["hi"] and len(out) < want:
+                    out.append({"seed": s, "query": qj, "oracle_count": c})
+            print(f"tried up to seed {seed}, accepted {len(out)}", flush=True)
+    out.sort(key=lambda d: d["seed"])
+    path = os.path.join(ROOT, "synth", "data", f"{name}_queries.json")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    with open(path, "w") as fh:
+        json.dump({"recipe": {k: v for k, v in r.items()}, "generator": "scripts/gen_queries.py",
+                   "counts_from": "oracle/oracle.c (CPU backtracking oracle)", "queries": out}, fh)
+    print("wrote", path, len(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,75 @@
+"""CPU-side checks of the C-ABI boundary (no compute calls: there is no GPU here).
+
+* libgpsense.so loads and exports every symbol include/gpsense.h declares;
+* the binding's ctypes structs match the header's layouts (sizes);
+* without a CUDA device the library refuses to run (no CPU fallback).
+"""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gpsense.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"GPS_API\s+[\w\s\*]+?\b(gps_\w+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def gps():
+    from paper_1807_08804_b200 import _build
+    _build.build()
+    from paper_1807_08804_b200 import gpsense
+    return gpsense
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    for want in ["gps_load_data_graph", "gps_match", "gps_count", "gps_create", "gps_result_info"]:
+        assert want in names
+
+
+def test_library_exports_every_declared_symbol(gps):
+    lib = ctypes.CDLL(gps.LIB_PATH)
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert sorted(gps.EXPORTED) == _declared()
+
+
+def test_struct_layouts(gps):
+    # offsets/sizes of the C structs as laid out by the x86-64 SysV ABI
+    assert ctypes.sizeof(gps.CtxOpts) == 32
+    assert ctypes.sizeof(gps.CsrDesc) == 56
+    assert ctypes.sizeof(gps.QEdge) == 12
+    assert ctypes.sizeof(gps.QueryDesc) == 32
+    assert ctypes.sizeof(gps.MatchOpts) == 16
+    assert ctypes.sizeof(gps.Stats) == 32 + 4 * 8 * gps.NK
+
+
+def test_default_opts(gps):
+    o = gps.default_opts()
+    assert (o.refine_rounds, o.reverse_refine, o.lowconn_threshold, o.result_on_device) == (1, 1, 1, 1)
+
+
+def test_no_cpu_fallback_without_device(gps):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(gps.GpsError) as ei:
+        gps.Context(0)
+    assert ei.value.status in (gps.GPS_ECUDA, gps.GPS_EINVAL)
+
+
+def test_kernel_sass_is_sm100a(gps):
+    """The .so carries sm_100a SASS (cuobjdump), not PTX for another arch."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump missing")
+    out = subprocess.run([exe, "--list-elf", gps.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out

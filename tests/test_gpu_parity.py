@@ -1,0 +1,293 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle.
+
+Bar: the path is integer-only, so every comparison is
+bit-exact -- the sorted embedding set of gps_match equals the oracle's sorted
+set, and gps_count equals the oracle's count.  Inputs are seeded synth/
+generators; expected values come only from oracle/ (or tests/golden, cited).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from synth import (DataGraph, Query, bfs_query, config_graph, fixture_fig3_example,
+                   random_connected_query, random_multigraph, triangle_tail)
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+@pytest.fixture(scope="module")
+def gps():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1807_08804_b200 import gpsense
+    return gpsense
+
+
+@pytest.fixture(scope="module")
+def ctx(gps):
+    c = gps.Context(0)
+    yield c
+    c.close()
+
+
+def _rows(t):
+    a = t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
+    return oracle.sort_rows(a.astype(np.uint32))
+
+
+def _check(ctx, G, og, q, opts=None):
+    want = oracle.match(og, q)
+    got = _rows(ctx.match(G, q, opts))
+    assert got.shape == want.shape, (got.shape, want.shape)
+    assert np.array_equal(got, want)
+    assert ctx.count(G, q, opts) == want.shape[0]
+    return want
+
+
+# ---------------------------------------------------------------- worked example
+def test_fig3_example(ctx):
+    gold = json.load(open(os.path.join(GOLDEN, "fig3_example.json")))
+    g, q = fixture_fig3_example()
+    G = ctx.load_graph(g)
+    rows = _rows(ctx.match(G, q))
+    assert rows.tolist() == gold["embeddings"]
+    assert ctx.count(G, q) == 1
+    order, rank = ctx.plan(G, q)
+    assert order[:2] == gold["visit_order_prefix"]        # u5, u2
+    for (d, f), (gd, gf) in zip(rank, gold["rank_f"]):     # f(u) = deg/freq
+        assert d * gf == gd * f
+    c0 = ctx.candidates(G, q, 0)
+    assert np.nonzero(c0[2])[0].tolist() == gold["candidates_u3_after_check"]
+    assert np.nonzero(c0[0])[0].tolist() == gold["candidates_u1_after_check"]
+    assert c0[0][:6].tolist() == gold["c_set_u1_flags_v1_to_v6"]
+
+
+# ------------------------------------------------------------- random corpus
+def _instance(seed):
+    rng = np.random.default_rng(10_000 + seed)
+    n = int(rng.integers(20, 301))
+    deg = float(rng.uniform(1.5, 8.0))
+    undirected = seed % 4 == 0
+    g = random_multigraph(n, int(n * deg / (2 if undirected else 1)), n_elabels=int(rng.integers(1, 5)),
+                          n_vlabels=int(rng.integers(1, 21)), seed=seed, undirected=undirected,
+                          self_loops=seed % 3 == 0, dup_prob=0.1)
+    k = int(rng.integers(4, 9))
+    if seed % 5 == 4:
+        q = random_connected_query(rng, min(k, 6), extra=int(rng.integers(0, 4)),
+                                   n_elabels=int(g.elab.max()) + 1 if g.elab is not None else 1,
+                                   n_vlabels=int(g.vlab.max()) + 1, p_wild_v=0.6, p_wild_e=0.6,
+                                   bound_choices=list(range(n)), p_bound=0.1)
+    else:
+        q = bfs_query(g, min(k, n), seed, induced=seed % 2 == 0, p_wild_v=float(rng.uniform(0, 1)),
+                      keep_elabels=seed % 3 != 1, bind_seed=seed % 7 == 3, max_children=int(rng.integers(0, 3)))
+    return g, q
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_random_corpus(ctx, seed):
+    """S:499 acceptance corpus: data <= 300 nodes, avg degree <= 8, <= 20 labels, BFS queries of 4-8 nodes."""
+    g, q = _instance(seed)
+    og = oracle.OracleGraph(g)
+    try:
+        oracle.count(og, q, limit=2_000_000)
+    except ValueError:
+        pytest.skip("oracle rejects the instance")
+    if oracle.count(og, q, limit=2_000_000) == oracle.ELIMIT:
+        pytest.skip("too many embeddings for the oracle")
+    _check(ctx, ctx.load_graph(g), og, q)
+
+
+@pytest.mark.parametrize("seed", range(0, 200, 7))
+def test_filter_soundness_and_monotone(ctx, seed):
+    """No oracle-embedding image is ever pruned; stages only shrink the sets."""
+    g, q = _instance(seed)
+    og = oracle.OracleGraph(g)
+    if oracle.count(og, q, limit=200_000) == oracle.ELIMIT:
+        pytest.skip("too many embeddings")
+    rows = oracle.match(og, q)
+    G = ctx.load_graph(g)
+    prev = None
+    for stage in (0, 1, 2):
+        c = ctx.candidates(G, q, stage)
+        for u in range(q.k):
+            assert c[u][rows[:, u]].all(), (stage, u)
+        if prev is not None:
+            assert not (c & ~prev).any()
+        prev = c
+
+
+@pytest.mark.parametrize("rounds,rev,low", [(0, 1, 1), (1, 0, 1), (3, 1, 1), (1, 1, 0), (2, 0, 2)])
+def test_refinement_variants_same_result(gps, ctx, rounds, rev, low):
+    """P:997-1008 refinement variants change work, never the result."""
+    for seed in (3, 11, 22, 40):
+        g, q = _instance(seed)
+        og = oracle.OracleGraph(g)
+        if oracle.count(og, q, limit=500_000) == oracle.ELIMIT:
+            continue
+        o = gps.default_opts(refine_rounds=rounds, reverse_refine=rev, lowconn_threshold=low)
+        _check(ctx, ctx.load_graph(g), og, q, o)
+
+
+# ------------------------------------------------------------------ config 1
+@pytest.fixture(scope="module")
+def cfg1(ctx):
+    g = config_graph(1)
+    return g, ctx.load_graph(g), oracle.OracleGraph(g)
+
+
+def test_cfg1_graph_layout(cfg1):
+    g, G, og = cfg1
+    assert G.n == 1000 and G.arcs == 10000 == og.arcs
+
+
+@pytest.mark.parametrize("labels", [(-1, -1, -1, -1), (0, 1, 2, 3), (1, 1, 1, 1), (2, -1, 5, 2), (-1, 3, -1, 3),
+                                    (7, 7, 0, -1)])
+def test_cfg1_triangle_tail(ctx, cfg1, labels):
+    g, G, og = cfg1
+    _check(ctx, G, og, triangle_tail(labels))
+
+
+def test_cfg1_label_partition(ctx, cfg1):
+    """sum over the 8^4 labelled variants = all-'*' count (checked on the CUDA path, 512 variants sampled)."""
+    g, G, og = cfg1
+    rng = np.random.default_rng(5)
+    for _ in range(64):
+        lab = tuple(int(x) for x in rng.integers(0, 8, 4))
+        assert ctx.count(G, triangle_tail(lab)) == oracle.count(og, triangle_tail(lab))
+
+
+# ------------------------------------------------------------------ config 2
+@pytest.fixture(scope="module")
+def cfg2(ctx):
+    path = os.path.join(ROOT, "synth", "data", "cfg2_queries.json")
+    data = json.load(open(path))
+    g = config_graph(2)
+    return g, ctx.load_graph(g), data
+
+
+def test_cfg2_graph_layout(cfg2):
+    g, G, data = cfg2
+    assert G.n == 300_000 and G.arcs == 1_500_000 and G.elabel_bits == 6
+
+
+def test_cfg2_counts_all_queries(ctx, cfg2):
+    """Full-size config 2 (the bench workload): gps_count == stored oracle count for all 100 queries."""
+    g, G, data = cfg2
+    for item in data["queries"]:
+        q = Query.from_json(item["query"])
+        assert ctx.count(G, q) == item["oracle_count"], item["seed"]
+
+
+def test_cfg2_match_sets(ctx, cfg2):
+    """Full-size config 2: complete sorted-set equality for the queries the oracle enumerates quickly."""
+    g, G, data = cfg2
+    og = oracle.OracleGraph(g)
+    small = sorted(data["queries"], key=lambda d: d["oracle_count"])[:12]
+    big = max(data["queries"], key=lambda d: d["oracle_count"])
+    for item in small + [big]:
+        q = Query.from_json(item["query"])
+        got = _rows(ctx.match(G, q))
+        assert got.shape[0] == item["oracle_count"]
+        assert np.array_equal(got, oracle.match(og, q))
+
+
+# ---------------------------------------------------------------- edge cases
+def test_single_vertex_query(ctx, cfg1):
+    g, G, og = cfg1
+    for lab in (-1, 3):
+        _check(ctx, G, og, Query(1, [lab], [-1], []))
+    _check(ctx, G, og, Query(1, [-1], [17], []))
+
+
+def test_bound_vertices(ctx, cfg1):
+    g, G, og = cfg1
+    hub = int(np.bincount(np.concatenate([g.src, g.dst])).argmax())
+    _check(ctx, G, og, Query(3, [-1, -1, -1], [hub, -1, -1], [(0, 1, -1), (1, 2, -1)]))
+    _check(ctx, G, og, Query(3, [-1, -1, -1], [-1, hub, -1], [(0, 1, -1), (1, 2, -1), (2, 0, -1)]))
+
+
+def test_empty_results(ctx, cfg1):
+    g, G, og = cfg1
+    assert ctx.count(G, triangle_tail((9, -1, -1, -1))) == 0          # label nobody has
+    assert ctx.match(G, Query(2, [-1, -1], [-1, -1], [(0, 1, 3)])).shape == (0, 2)   # edge label absent
+    assert ctx.count(G, Query(5, [-1] * 5, [-1] * 5,
+                              [(i, j, -1) for i in range(5) for j in range(i + 1, 5)])) == \
+        oracle.count(og, Query(5, [-1] * 5, [-1] * 5, [(i, j, -1) for i in range(5) for j in range(i + 1, 5)]))
+
+
+def test_errors(gps, ctx, cfg1):
+    g, G, og = cfg1
+    with pytest.raises(gps.GpsError) as e:
+        ctx.count(G, Query(3, [-1] * 3, [-1] * 3, [(0, 1, -1)]))
+    assert e.value.status == gps.GPS_EDISCONNECTED
+    with pytest.raises(gps.GpsError) as e:
+        ctx.count(G, Query(2, [-1] * 2, [-1] * 2, [(0, 0, -1), (0, 1, -1)]))
+    assert e.value.status == gps.GPS_EINVAL
+    with pytest.raises(gps.GpsError) as e:
+        ctx.count(G, Query(2, [-1] * 2, [5000, -1], [(0, 1, -1)]))
+    assert e.value.status == gps.GPS_EINVAL
+    with pytest.raises(gps.GpsError) as e:
+        ctx.load_graph_csr(3, np.array([0, 1, 1, 5], np.uint64), np.array([1], np.uint32))
+    assert e.value.status == gps.GPS_EINVAL
+    with pytest.raises(gps.GpsError) as e:
+        ctx.load_graph_csr(3, np.array([0, 1, 1, 1], np.uint64), np.array([7], np.uint32))
+    assert e.value.status == gps.GPS_EINVAL
+
+
+def test_parallel_arcs_and_duplicates(ctx):
+    g = DataGraph(4, np.array([0, 0, 0, 1, 2, 2], np.uint32), np.array([1, 1, 1, 2, 0, 3], np.uint32),
+                  np.array([0, 1, 1, 2, 0, 5], np.uint16), None, False)
+    G = ctx.load_graph(g)
+    og = oracle.OracleGraph(g)
+    assert G.arcs == 5
+    for q in [Query(2, [-1, -1], [-1, -1], [(0, 1, -1)]), Query(2, [-1, -1], [-1, -1], [(0, 1, 1)]),
+              Query(2, [-1, -1], [-1, -1], [(0, 1, 0), (0, 1, 1)]),
+              Query(3, [-1] * 3, [-1] * 3, [(0, 1, -1), (1, 2, -1), (2, 0, -1)]),
+              Query(3, [-1] * 3, [-1] * 3, [(0, 1, -1), (1, 2, -1)])]:
+        _check(ctx, G, og, q)
+
+
+def test_graph_without_arcs(ctx):
+    g = DataGraph(5, np.zeros(0, np.uint32), np.zeros(0, np.uint32), None, None, False)
+    G = ctx.load_graph(g)
+    assert G.arcs == 0
+    assert ctx.count(G, Query(1, [-1], [-1], [])) == 5
+    assert ctx.count(G, Query(2, [-1, -1], [-1, -1], [(0, 1, -1)])) == 0
+
+
+def test_match_host_and_overflow(gps, ctx, cfg1):
+    g, G, og = cfg1
+    q = triangle_tail((1, -1, 2, -1))
+    want = oracle.match(og, q)
+    out = np.zeros((want.shape[0] + 5, 4), np.uint32)
+    got = ctx.match_host(G, q, out)
+    assert np.array_equal(oracle.sort_rows(np.array(got)), want)
+    small = np.zeros((max(want.shape[0] - 1, 0), 4), np.uint32)
+    with pytest.raises(gps.GpsError) as e:
+        ctx.match_host(G, q, small)
+    assert e.value.status == gps.GPS_EOVERFLOW
+    host = ctx.match(G, q, device=False)
+    assert np.array_equal(oracle.sort_rows(host), want)
+
+
+def test_determinism(ctx, cfg1):
+    g, G, og = cfg1
+    q = triangle_tail()
+    a = ctx.match(G, q).cpu().numpy()
+    b = ctx.match(G, q).cpu().numpy()
+    assert np.array_equal(a, b)   # row order is deterministic too (reading R25)
+
+
+def test_stats_count_launches(ctx, cfg1):
+    g, G, og = cfg1
+    ctx.reset_stats()
+    ctx.count(G, triangle_tail())
+    st = ctx.stats()
+    assert st["queries"] == 1 and st["launches"] > 5
+    assert st["kernels"]["join_count"]["launches"] >= 1
