@@ -132,6 +132,12 @@ static int has_arc(const og_graph *g, uint32_t a, uint32_t b, int32_t lab) {
     return 0;
 }
 
+/* Optional bound on search work (candidate tries), for query-acceptance scripts
+ * only: when exceeded the search stops with ORC_ELIMIT.  0 = unlimited (default).
+ * It never changes a completed result. */
+static uint64_t g_work_limit = 0;
+void oracle_set_work_limit(uint64_t tries) { g_work_limit = tries; }
+
 typedef struct { uint32_t other; int out; int32_t lab; } chk_t; /* out: arc u->other, else other->u */
 
 typedef struct {
@@ -146,13 +152,14 @@ typedef struct {
     int nchk[ORC_MAXK];
     uint32_t f[ORC_MAXK];         /* f[u] for query vertex u */
     uint8_t *used;                /* [n] */
-    uint64_t count, limit, cap;
+    uint64_t count, limit, cap, work;
     uint32_t *rows;
     int over;
 } orc_state;
 
 static int try_vertex(orc_state *s, uint32_t i, uint32_t v) {
     uint32_t u = s->pi[i];
+    if (g_work_limit && ++s->work > g_work_limit) { s->over = 1; return 0; }
     if (s->used[v]) return 0;
     if (s->qlab[u] >= 0 && s->g->vlab[v] != s->qlab[u]) return 0;
     if (s->qbound[u] >= 0 && (int64_t)v != s->qbound[u]) return 0;

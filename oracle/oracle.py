@@ -42,6 +42,7 @@ def _load():
         lib.oracle_match.restype = ctypes.c_int64
         lib.oracle_match.argtypes = [P, ctypes.c_uint32, P, P, ctypes.c_uint32, P, P, P, P,
                                      ctypes.c_uint64, ctypes.c_uint64]
+        lib.oracle_set_work_limit.argtypes = [ctypes.c_uint64]
         _lib = lib
     return _lib
 
@@ -82,6 +83,11 @@ def _qarrays(q):
     bd = np.array(q.bound, np.int64)
     e = np.array(q.edges, np.int32).reshape(-1, 3)
     return vl, bd, np.ascontiguousarray(e[:, 0]), np.ascontiguousarray(e[:, 1]), np.ascontiguousarray(e[:, 2])
+
+
+def set_work_limit(tries: int) -> None:
+    """Abort searches after `tries` candidate tests (ELIMIT); 0 = unlimited.  Acceptance scripts only."""
+    _load().oracle_set_work_limit(int(tries))
 
 
 def count(og: OracleGraph, q, limit: int = 0) -> int:

@@ -33,6 +33,7 @@ def _init(cfg):
     global _G, _OG
     _G = config_graph(cfg)
     _OG = oracle.OracleGraph(_G)
+    oracle.set_work_limit(300_000_000)   # give up on searches that would take minutes
 
 
 def _try(args):
