@@ -149,6 +149,20 @@ GPS_API gps_status gps_match_host(gps_ctx* ctx, const gps_graph* g, const gps_qu
 GPS_API gps_status gps_count(gps_ctx* ctx, const gps_graph* g, const gps_query* q,
                      const gps_match_opts* opts, uint64_t* count);
 
+/* Batched execution of nq independent queries (the QA-batch use, BASELINE
+ * configs[4]): the library runs them concurrently on a pool of worker host
+ * threads, each owning a CUDA stream and scratch (set its size with
+ * gps_set_workers; default 8).  results[i] / counts[i] / statuses[i] (statuses
+ * may be NULL) as for the single-query calls; results are owned by the caller
+ * (gps_result_free).  The ctx stream is ordered before / after the batch.
+ * Returns the first failing status (GPS_OK if all succeeded). */
+GPS_API gps_status gps_match_batch(gps_ctx* ctx, const gps_graph* g, const gps_query* queries, uint32_t nq,
+                                   const gps_match_opts* opts, gps_result** results, gps_status* statuses);
+GPS_API gps_status gps_count_batch(gps_ctx* ctx, const gps_graph* g, const gps_query* queries, uint32_t nq,
+                                   const gps_match_opts* opts, uint64_t* counts, gps_status* statuses);
+/* Number of batch workers (1..64; 0 = default 8).  Destroys existing workers (and their results). */
+GPS_API gps_status gps_set_workers(gps_ctx* ctx, uint32_t n);
+
 /* rows, cols (= k), data (device or host pointer, owned by the result), on_device. */
 GPS_API gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols,
                            const uint32_t** data, int* on_device);

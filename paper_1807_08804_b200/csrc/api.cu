@@ -8,9 +8,14 @@
 // Host syncs per query: 1 (candidate counts) + 1 (EC totals -> join order)
 // + 1 per join step (output size, two-step scheme P:809).
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.cuh"
@@ -69,6 +74,27 @@ void dfree(gps_ctx* c, void* p) {
     if (p) (void)cudaFreeAsync(p, c->stream);
 }
 
+LbScratch lb_scratch(gps_ctx* c, uint32_t tiles) {
+    if (tiles == 0) tiles = 1;
+    if (tiles > c->lb_tiles) {
+        uint32_t cap = std::max<uint32_t>(tiles, 2 * c->lb_tiles);
+        cap = std::max<uint32_t>(cap, 256);
+        if (c->lb_status) dfree(c, c->lb_status);
+        c->lb_status = static_cast<uint64_t*>(dmalloc(c, sizeof(uint64_t) * (size_t)cap * kLbSlots));
+        GPS_CK(cudaMemsetAsync(c->lb_status, 0, sizeof(uint64_t) * (size_t)cap * kLbSlots, c->stream));
+        c->lb_tiles = cap;
+    }
+    return LbScratch{c->lb_status, c->lb_ctr, c->lb_tiles};
+}
+uint32_t lb_next_epoch(gps_ctx* c) {
+    c->lb_epoch++;
+    if (c->lb_epoch >= (1u << 20)) {   // wrap: clear stale words so old epochs cannot alias
+        GPS_CK(cudaMemsetAsync(c->lb_status, 0, sizeof(uint64_t) * (size_t)c->lb_tiles * kLbSlots, c->stream));
+        c->lb_epoch = 1;
+    }
+    return c->lb_epoch;
+}
+
 struct DeviceGuard {
     int prev = -1, want;
     explicit DeviceGuard(int d) : want(d) {
@@ -97,19 +123,10 @@ static gps_status guarded(F&& f) {
     }
 }
 
-struct GatherArgs {
-    int n;
-    const uint32_t* p[GPS_MAX_QE];
-};
-__global__ void k_gather(GatherArgs a, uint64_t* out) {
-    int i = threadIdx.x;
-    if (i < a.n) out[i] = *a.p[i];
-}
-
 // ------------------------------------------------------------------ filter
 struct Filtered {
     Plan plan;
-    DevPtr B, X, rp, carr, cnt;
+    DevPtr B, X, rp, carr, cnt, seg, mask;
     uint32_t nws = 0, rps = 0, n = 0;
     uint32_t C[GPS_MAX_QV] = {0};
     uint32_t* Bp(int u) const { return B.as<uint32_t>() + (size_t)u * nws; }
@@ -117,38 +134,56 @@ struct Filtered {
     uint32_t* rpp(int u) const { return rp.as<uint32_t>() + (size_t)u * rps; }
     uint32_t* carrp(int u) const { return carr.as<uint32_t>() + (size_t)u * n; }
     uint32_t* cntp(int u) const { return cnt.as<uint32_t>() + u; }
+    uint32_t* segp(int u, int dir) const { return seg.as<uint32_t>() + (size_t)(2 * u + dir) * (n + 1); }
 };
+
+static void collect_into(CollectArgs& ca, const Filtered& F, int u, bool with_mask) {
+    const int i = ca.nu++;
+    ca.B[i] = F.Bp(u);
+    ca.rp[i] = F.rpp(u);
+    ca.carr[i] = F.carrp(u);
+    ca.cnt[i] = F.cntp(u);
+    ca.seg_out[i] = F.segp(u, 0);
+    ca.seg_in[i] = F.segp(u, 1);
+    ca.mask[i] = with_mask ? F.mask.as<unsigned long long>() : nullptr;
+}
 
 static void filter_step(gps_ctx* c, const gps_graph* g, Filtered& F, const FilterStep& st) {
     const Plan& p = F.plan;
     CollectArgs ca{};
-    ca.nu = 1;
-    ca.B[0] = F.Bp(st.u);
-    ca.rp[0] = F.rpp(st.u);
-    ca.carr[0] = F.carrp(st.u);
-    ca.cnt[0] = F.cntp(st.u);
+    collect_into(ca, F, st.u, true);
     run_collect(c, g->d, ca);
+    // constraints ordered out-arcs first (pair-space layout of k_explore); scratch slot = position
+    std::vector<Constraint> cons;
+    for (const Constraint& cs : st.cons)
+        if (cs.dir == 0) cons.push_back(cs);
+    const int no = (int)cons.size();
+    for (const Constraint& cs : st.cons)
+        if (cs.dir == 1) cons.push_back(cs);
     ExploreArgs ea{};
-    ea.nc = (int)st.cons.size();
-    for (int i = 0; i < ea.nc; i++) {
-        const Constraint& cs = st.cons[i];
-        ea.c[i] = Cons{F.Bp(cs.v), st.propagate ? F.Xp(i) : nullptr, p.arcs[cs.arc].lab, cs.dir};
-    }
+    ea.no = no;
+    ea.ni = (int)cons.size() - no;
+    for (int i = 0; i < (int)cons.size(); i++)
+        ea.c[i] = Cons{F.Bp(cons[i].v), st.propagate ? F.Xp(i) : nullptr, p.arcs[cons[i].arc].lab, cons[i].dir};
     ea.cands = F.carrp(st.u);
     ea.cnt = F.cntp(st.u);
+    ea.seg_out = F.segp(st.u, 0);
+    ea.seg_in = F.segp(st.u, 1);
+    ea.mask = F.mask.as<unsigned long long>();
     ea.Bu = F.Bp(st.u);
-    run_explore(c, g->d, ea, g->d.n);
-    if (st.propagate && ea.nc) {
+    ea.propagate = st.propagate ? 1 : 0;
+    run_explore(c, g->d, ea);
+    if (st.propagate && !cons.empty()) {
         AndArgs aa{};
         std::vector<int> targets;
-        for (const Constraint& cs : st.cons)
+        for (const Constraint& cs : cons)
             if (std::find(targets.begin(), targets.end(), cs.v) == targets.end()) targets.push_back(cs.v);
         int nx = 0;
         for (int t = 0; t < (int)targets.size(); t++) {
             aa.B[t] = F.Bp(targets[t]);
             aa.xbeg[t] = nx;
-            for (int i = 0; i < ea.nc; i++)
-                if (st.cons[i].v == targets[t]) aa.X[nx++] = F.Xp(i);
+            for (int i = 0; i < (int)cons.size(); i++)
+                if (cons[i].v == targets[t]) aa.X[nx++] = F.Xp(i);
         }
         aa.nt = (int)targets.size();
         aa.xbeg[aa.nt] = nx;
@@ -169,6 +204,8 @@ static void run_filter(gps_ctx* c, const gps_graph* g, Filtered& F, int stage) {
     F.rp = DevPtr(c, sizeof(uint32_t) * (size_t)k * F.rps);
     F.carr = DevPtr(c, sizeof(uint32_t) * (size_t)k * F.n);
     F.cnt = DevPtr(c, sizeof(uint32_t) * 64);
+    F.seg = DevPtr(c, sizeof(uint32_t) * (size_t)2 * k * (F.n + 1));
+    F.mask = DevPtr(c, sizeof(unsigned long long) * (size_t)F.n);
     GPS_CK(cudaMemsetAsync(F.X.p, 0, sizeof(uint32_t) * nx * F.nws, c->stream));
     QDesc qd{};
     qd.k = k;
@@ -185,13 +222,7 @@ static void run_filter(gps_ctx* c, const gps_graph* g, Filtered& F, int stage) {
         for (const FilterStep& st : p.refine_steps) filter_step(c, g, F, st);
     if (stage >= 3) {
         CollectArgs ca{};
-        ca.nu = k;
-        for (int u = 0; u < k; u++) {
-            ca.B[u] = F.Bp(u);
-            ca.rp[u] = F.rpp(u);
-            ca.carr[u] = F.carrp(u);
-            ca.cnt[u] = F.cntp(u);
-        }
+        for (int u = 0; u < k; u++) collect_into(ca, F, u, false);
         run_collect(c, g->d, ca);
         GPS_CK(cudaMemcpyAsync(c->h_info, F.cnt.p, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, c->stream));
         ctx_sync(c);
@@ -202,59 +233,80 @@ static void run_filter(gps_ctx* c, const gps_graph* g, Filtered& F, int stage) {
 
 // -------------------------------------------------------------- EC tables
 struct ECTab {
-    DevPtr cnt, off, val;
+    DevPtr cnt, off, val, blk;
     uint64_t total = 0;
     int dir = 0;   // 0: keyed by arc source, 1: keyed by arc target
 };
 
+static uint32_t ec_grid(gps_ctx* c) { return (uint32_t)c->nsm * 4; }
+
+static ECArc ec_arc(gps_ctx* c, const Filtered& F, const QArc& a, ECTab& t) {
+    const int key = t.dir ? a.b : a.a, other = t.dir ? a.a : a.b;
+    ECArc e{};
+    e.keys = F.carrp(key);
+    e.nkeys = F.C[key];
+    e.dir = t.dir;
+    e.lab = a.lab;
+    e.Bq = F.Bp(other);
+    e.seg = F.segp(key, t.dir);
+    e.cnt = t.cnt.as<uint32_t>();
+    e.val = t.val.as<uint32_t>();
+    e.blk = t.blk.as<uint64_t>();
+    return e;
+}
+
+// Pass 1 of the two-step scheme for the listed arcs: per-key counts (scanned into
+// the key offsets) and per-block counts; totals land in c->d_info[2*j+1].
 static void ec_count(gps_ctx* c, const gps_graph* g, const Filtered& F, std::vector<ECTab>& T,
                      const std::vector<int>& arcs, bool need_totals) {
     const Plan& p = F.plan;
+    const uint32_t G = ec_grid(c);
     ECArgs ea{};
     ScanBatch<uint32_t, uint32_t> sb{};
-    uint32_t maxk = 0;
-    for (int i : arcs) {
+    size_t cnt_words = 0;
+    for (int i : arcs) cnt_words += (size_t)F.C[T[i].dir ? p.arcs[i].b : p.arcs[i].a] + 1;
+    DevPtr cnt_all(c, sizeof(uint32_t) * cnt_words);
+    GPS_CK(cudaMemsetAsync(cnt_all.p, 0, sizeof(uint32_t) * cnt_words, c->stream));
+    size_t at = 0;
+    for (int j = 0; j < (int)arcs.size(); j++) {
+        const int i = arcs[j];
         ECTab& t = T[i];
         const QArc& a = p.arcs[i];
-        const int key = t.dir ? a.b : a.a, other = t.dir ? a.a : a.b;
-        const uint32_t nk = F.C[key];
-        t.cnt = DevPtr(c, sizeof(uint32_t) * ((size_t)nk + 1));
+        const uint32_t nk = F.C[t.dir ? a.b : a.a];
         t.off = DevPtr(c, sizeof(uint32_t) * ((size_t)nk + 1));
-        ea.a[ea.na++] = ECArc{F.carrp(key), nk, t.dir, a.lab, F.Bp(other), t.cnt.as<uint32_t>(), nullptr, nullptr};
-        sb.in[sb.nseg] = t.cnt.as<uint32_t>();
+        if (!t.blk.p) t.blk = DevPtr(c, sizeof(uint64_t) * (G + 1));
+        ECArc e = ec_arc(c, F, a, t);
+        e.cnt = cnt_all.as<uint32_t>() + at;
+        e.done = c->d_done + 1 + j;
+        e.info = c->d_info + 2 * j;
+        ea.a[ea.na++] = e;
+        sb.in[sb.nseg] = e.cnt;
         sb.out[sb.nseg] = t.off.as<uint32_t>();
         sb.n[sb.nseg++] = nk;
-        maxk = std::max(maxk, nk);
+        at += (size_t)nk + 1;
     }
-    run_ec(c, g->d, ea, false, maxk);
+    run_ec(c, g->d, ea, false, G);
     scan_exclusive(c, sb);
     if (need_totals) {
-        GatherArgs ga{};
-        for (int i : arcs) {
-            const QArc& a = p.arcs[i];
-            ga.p[ga.n++] = T[i].off.as<uint32_t>() + F.C[T[i].dir ? a.b : a.a];
-        }
-        launch(c, GPS_K_SCAN, dim3(1), dim3(64), 0, k_gather, ga, c->d_info);
-        GPS_CK(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(uint64_t) * ga.n, cudaMemcpyDeviceToHost, c->stream));
+        GPS_CK(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(uint64_t) * 2 * arcs.size(), cudaMemcpyDeviceToHost,
+                               c->stream));
         ctx_sync(c);
-        for (int j = 0; j < (int)arcs.size(); j++) T[arcs[j]].total = c->h_info[j];
+        for (int j = 0; j < (int)arcs.size(); j++) T[arcs[j]].total = c->h_info[2 * j + 1];
     }
 }
 
 static void ec_write(gps_ctx* c, const gps_graph* g, const Filtered& F, std::vector<ECTab>& T) {
     const Plan& p = F.plan;
     ECArgs ea{};
-    uint32_t maxk = 0;
+    double vals = 0;
     for (int i = 0; i < (int)p.arcs.size(); i++) {
         ECTab& t = T[i];
-        const QArc& a = p.arcs[i];
-        const int key = t.dir ? a.b : a.a, other = t.dir ? a.a : a.b;
         t.val = DevPtr(c, sizeof(uint32_t) * (t.total + 1));
-        ea.a[ea.na++] = ECArc{F.carrp(key), F.C[key], t.dir, a.lab, F.Bp(other), nullptr, t.off.as<uint32_t>(),
-                              t.val.as<uint32_t>()};
-        maxk = std::max(maxk, F.C[key]);
+        ea.a[ea.na++] = ec_arc(c, F, p.arcs[i], t);
+        vals += (double)t.total;
     }
-    run_ec(c, g->d, ea, true, maxk);
+    run_ec(c, g->d, ea, true, ec_grid(c));
+    c->stats.k_bytes[GPS_K_EC_WRITE] += 4.0 * vals;
 }
 
 // ------------------------------------------------------------------- query
@@ -344,12 +396,10 @@ static void run_query(gps_ctx* c, const gps_graph* g, const gps_query* q, const 
             cl.val = T[ci].val.as<uint32_t>();
         }
         DevPtr s0(c, sizeof(uint32_t) * (R + 1));
-        DevPtr len(c, sizeof(uint32_t) * (R + 1));
         DevPtr poff(c, sizeof(uint64_t) * (R + 1));
         sa.s0 = s0.as<uint32_t>();
-        run_join_len(c, sa, len.as<uint32_t>());
-        scan_exclusive1<uint32_t, uint64_t>(c, len.as<uint32_t>(), poff.as<uint64_t>(), R);
         sa.poff = poff.as<uint64_t>();
+        run_join_seg(c, sa);
         sa.blk = blk.as<uint64_t>();
         sa.info = c->d_info;
         sa.done = c->d_done;
@@ -383,6 +433,180 @@ static void run_query(gps_ctx* c, const gps_graph* g, const gps_query* q, const 
     out.table = std::move(Mbuf);
 }
 
+
+static void ctx_init(gps_ctx* c, int dev, cudaStream_t stream) {
+    c->device = dev;
+    GPS_CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (stream) {
+        c->stream = stream;
+    } else {
+        GPS_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    cudaMemPool_t pool;
+    GPS_CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = ~0ull;
+    GPS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    GPS_CK(cudaMalloc(&c->d_bytes, sizeof(unsigned long long) * GPS_K_NCLASSES));
+    GPS_CK(cudaMemset(c->d_bytes, 0, sizeof(unsigned long long) * GPS_K_NCLASSES));
+    GPS_CK(cudaMalloc(&c->d_info, sizeof(uint64_t) * 128));
+    GPS_CK(cudaMallocHost(&c->h_info, sizeof(uint64_t) * 128));
+    GPS_CK(cudaMalloc(&c->d_done, sizeof(unsigned int) * (2 + GPS_MAX_QE)));
+    GPS_CK(cudaMemset(c->d_done, 0, sizeof(unsigned int) * (2 + GPS_MAX_QE)));
+    GPS_CK(cudaMalloc(&c->lb_ctr, sizeof(unsigned int) * kLbSlots));
+    GPS_CK(cudaMemset(c->lb_ctr, 0, sizeof(unsigned int) * kLbSlots));
+    GPS_CK(cudaDeviceSynchronize());
+}
+
+static void ctx_release(gps_ctx* c) {
+    cudaStreamSynchronize(c->stream);
+    for (gps_result* r : c->results) {
+        if (r->data && r->on_device) cudaFreeAsync(r->data, c->stream);
+        r->data = nullptr;
+        r->rows = 0;
+        r->ctx = nullptr;
+    }
+    c->results.clear();
+    if (c->lb_status) cudaFreeAsync(c->lb_status, c->stream);
+    c->lb_status = nullptr;
+    cudaStreamSynchronize(c->stream);
+    for (auto& t : c->pending) {
+        c->event_pool.push_back(t.e0);
+        c->event_pool.push_back(t.e1);
+    }
+    c->pending.clear();
+    for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+    c->event_pool.clear();
+    cudaFree(c->d_bytes);
+    cudaFree(c->d_info);
+    cudaFreeHost(c->h_info);
+    cudaFree(c->d_done);
+    cudaFree(c->lb_ctr);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+}
+
+// Persistent host worker pool: run(f) calls f(w) once on every worker and waits.
+struct WorkerPool {
+    std::vector<std::thread> th;
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    std::function<void(int)> job;
+    uint64_t gen = 0;
+    int remaining = 0;
+    bool stop = false;
+    explicit WorkerPool(int n) {
+        for (int w = 0; w < n; w++)
+            th.emplace_back([this, w] {
+                uint64_t seen = 0;
+                for (;;) {
+                    std::function<void(int)> f;
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [&] { return stop || gen != seen; });
+                        if (stop) return;
+                        seen = gen;
+                        f = job;
+                    }
+                    f(w);
+                    {
+                        std::lock_guard<std::mutex> lk(mu);
+                        if (--remaining == 0) done_cv.notify_all();
+                    }
+                }
+            });
+    }
+    void run(std::function<void(int)> f) {
+        std::unique_lock<std::mutex> lk(mu);
+        job = std::move(f);
+        remaining = (int)th.size();
+        gen++;
+        cv.notify_all();
+        done_cv.wait(lk, [&] { return remaining == 0; });
+    }
+    ~WorkerPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : th) t.join();
+    }
+};
+
+static void ensure_workers(gps_ctx* c) {
+    const uint32_t n = c->nworkers_req ? c->nworkers_req : 8;
+    if (c->pool && c->workers.size() == n) return;
+    for (uint32_t w = (uint32_t)c->workers.size(); w < n; w++) {
+        gps_ctx* sc = new gps_ctx();
+        ctx_init(sc, c->device, nullptr);
+        sc->prof_mask = c->prof_mask;
+        c->workers.push_back(sc);
+    }
+    c->pool = new WorkerPool((int)n);
+}
+
+// device rows of one finished query -> gps_result owned by ctx c (worker or main)
+static gps_result* make_result(gps_ctx* c, Filtered& F, QueryOut& qo, bool on_device) {
+    gps_result* r = new gps_result();
+    r->rows = qo.rows;
+    r->cols = (uint32_t)F.plan.k;
+    r->ctx = c;
+    const size_t bytes = sizeof(uint32_t) * qo.rows * r->cols;
+    if (on_device) {
+        r->on_device = 1;
+        if (qo.borrowed) {
+            DevPtr cp(c, bytes);
+            GPS_CK(cudaMemcpyAsync(cp.p, qo.borrowed, bytes, cudaMemcpyDeviceToDevice, c->stream));
+            r->data = static_cast<uint32_t*>(cp.release());
+        } else {
+            r->data = static_cast<uint32_t*>(qo.table.release());
+        }
+        if (!r->data) r->data = static_cast<uint32_t*>(dmalloc(c, 16));
+        c->results.push_back(r);
+    } else {
+        r->on_device = 0;
+        r->data = static_cast<uint32_t*>(std::malloc(bytes ? bytes : 16));
+        if (!r->data) {
+            delete r;
+            fail(GPS_ENOMEM, "host result allocation failed");
+        }
+        const void* src = qo.borrowed ? (const void*)qo.borrowed : qo.table.p;
+        if (bytes) GPS_CK(cudaMemcpyAsync(r->data, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
+    return r;
+}
+
+// Run queries [0, nq) over the worker pool; body(worker ctx, i) per query.
+static gps_status run_batch(gps_ctx* c, uint32_t nq, gps_status* statuses,
+                            const std::function<void(gps_ctx*, uint32_t)>& body) {
+    ensure_workers(c);
+    cudaEvent_t start;
+    GPS_CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    GPS_CK(cudaEventRecord(start, c->stream));
+    std::atomic<uint32_t> next{0};
+    std::vector<cudaEvent_t> fin(c->workers.size(), nullptr);
+    c->pool->run([&](int w) {
+        gps_ctx* sc = c->workers[w];
+        cudaSetDevice(sc->device);
+        cudaStreamWaitEvent(sc->stream, start, 0);
+        for (;;) {
+            const uint32_t i = next.fetch_add(1);
+            if (i >= nq) break;
+            gps_status st = guarded([&] { body(sc, i); });
+            if (statuses) statuses[i] = st;
+        }
+        cudaEventCreateWithFlags(&fin[w], cudaEventDisableTiming);
+        cudaEventRecord(fin[w], sc->stream);
+    });
+    for (cudaEvent_t e : fin)
+        if (e) {
+            cudaStreamWaitEvent(c->stream, e, 0);
+            cudaEventDestroy(e);
+        }
+    cudaEventDestroy(start);
+    return GPS_OK;
+}
+
 }  // namespace gps
 
 using namespace gps;
@@ -410,25 +634,12 @@ gps_status gps_create(const gps_ctx_opts* opts, gps_ctx** out) {
         if (dev < 0 || dev >= ndev) fail(GPS_EINVAL, "bad device ordinal");
         DeviceGuard dg(dev);
         gps_ctx* c = new gps_ctx();
-        c->device = dev;
-        GPS_CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev));
-        if (opts && opts->stream) {
-            c->stream = (cudaStream_t)opts->stream;
-        } else {
-            GPS_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-            c->own_stream = true;
+        try {
+            ctx_init(c, dev, opts ? (cudaStream_t)opts->stream : nullptr);
+        } catch (...) {
+            delete c;
+            throw;
         }
-        cudaMemPool_t pool;
-        GPS_CK(cudaDeviceGetDefaultMemPool(&pool, dev));
-        uint64_t thr = ~0ull;
-        GPS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-        GPS_CK(cudaMalloc(&c->d_bytes, sizeof(unsigned long long) * GPS_K_NCLASSES));
-        GPS_CK(cudaMemset(c->d_bytes, 0, sizeof(unsigned long long) * GPS_K_NCLASSES));
-        GPS_CK(cudaMalloc(&c->d_info, sizeof(uint64_t) * 128));
-        GPS_CK(cudaMallocHost(&c->h_info, sizeof(uint64_t) * 128));
-        GPS_CK(cudaMalloc(&c->d_done, sizeof(unsigned int) * 4));
-        GPS_CK(cudaMemset(c->d_done, 0, sizeof(unsigned int) * 4));
-        GPS_CK(cudaDeviceSynchronize());
         *out = c;
     });
 }
@@ -437,26 +648,36 @@ gps_status gps_destroy(gps_ctx* c) {
     if (!c) return GPS_OK;
     return guarded([&] {
         DeviceGuard dg(c->device);
-        cudaStreamSynchronize(c->stream);
-        for (gps_result* r : c->results) {
-            if (r->data && r->on_device) cudaFreeAsync(r->data, c->stream);
-            r->data = nullptr;
-            r->rows = 0;
-            r->ctx = nullptr;
+        if (c->pool) {
+            delete c->pool;
+            c->pool = nullptr;
         }
-        c->results.clear();
-        cudaStreamSynchronize(c->stream);
-        for (auto& t : c->pending) {
-            c->event_pool.push_back(t.e0);
-            c->event_pool.push_back(t.e1);
+        for (gps_ctx* w : c->workers) {
+            ctx_release(w);
+            delete w;
         }
-        for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
-        cudaFree(c->d_bytes);
-        cudaFree(c->d_info);
-        cudaFreeHost(c->h_info);
-        cudaFree(c->d_done);
-        if (c->own_stream) cudaStreamDestroy(c->stream);
+        c->workers.clear();
+        ctx_release(c);
         delete c;
+    });
+}
+
+gps_status gps_set_workers(gps_ctx* c, uint32_t n) {
+    return guarded([&] {
+        if (!c) fail(GPS_EINVAL, "null ctx");
+        if (n > 64) fail(GPS_EINVAL, "at most 64 workers");
+        if (n == c->nworkers_req) return;
+        DeviceGuard dg(c->device);
+        if (c->pool) {
+            delete c->pool;
+            c->pool = nullptr;
+        }
+        for (gps_ctx* w : c->workers) {
+            ctx_release(w);
+            delete w;
+        }
+        c->workers.clear();
+        c->nworkers_req = n;
     });
 }
 
@@ -512,34 +733,8 @@ gps_status gps_match(gps_ctx* c, const gps_graph* g, const gps_query* q, const g
         QueryOut qo;
         run_query(c, g, q, opts, false, F, qo);
         const gps_match_opts o = resolve_opts(opts);
-        gps_result* r = new gps_result();
-        r->rows = qo.rows;
-        r->cols = (uint32_t)F.plan.k;
-        r->ctx = c;
-        const size_t bytes = sizeof(uint32_t) * qo.rows * r->cols;
-        if (o.result_on_device) {
-            r->on_device = 1;
-            if (qo.borrowed) {
-                DevPtr cp(c, bytes);
-                GPS_CK(cudaMemcpyAsync(cp.p, qo.borrowed, bytes, cudaMemcpyDeviceToDevice, c->stream));
-                r->data = static_cast<uint32_t*>(cp.release());
-            } else {
-                r->data = static_cast<uint32_t*>(qo.table.release());
-            }
-            if (!r->data) r->data = static_cast<uint32_t*>(dmalloc(c, 16));
-            c->results.push_back(r);
-            ctx_sync(c);
-        } else {
-            r->on_device = 0;
-            r->data = static_cast<uint32_t*>(std::malloc(bytes ? bytes : 16));
-            if (!r->data) {
-                delete r;
-                fail(GPS_ENOMEM, "host result allocation failed");
-            }
-            const void* src = qo.borrowed ? (const void*)qo.borrowed : qo.table.p;
-            if (bytes) GPS_CK(cudaMemcpyAsync(r->data, src, bytes, cudaMemcpyDeviceToHost, c->stream));
-            ctx_sync(c);
-        }
+        gps_result* r = make_result(c, F, qo, o.result_on_device != 0);
+        ctx_sync(c);
         c->stats.queries++;
         c->stats.embeddings += qo.rows;
         *out = r;
@@ -586,6 +781,61 @@ gps_status gps_count(gps_ctx* c, const gps_graph* g, const gps_query* q, const g
     });
 }
 
+gps_status gps_match_batch(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t nq,
+                           const gps_match_opts* opts, gps_result** results, gps_status* statuses) {
+    return guarded([&] {
+        if (!c || !g || (nq && (!qs || !results))) fail(GPS_EINVAL, "null argument");
+        if (g->device != c->device) fail(GPS_EINVAL, "graph and ctx on different devices");
+        DeviceGuard dg(c->device);
+        const gps_match_opts o = resolve_opts(opts);
+        for (uint32_t i = 0; i < nq; i++) results[i] = nullptr;
+        std::vector<gps_status> st(nq, GPS_OK);
+        run_batch(c, nq, st.data(), [&](gps_ctx* sc, uint32_t i) {
+            Filtered F;
+            QueryOut qo;
+            run_query(sc, g, &qs[i], &o, false, F, qo);
+            gps_result* r = make_result(sc, F, qo, o.result_on_device != 0);
+            ctx_sync(sc);
+            sc->stats.queries++;
+            sc->stats.embeddings += qo.rows;
+            results[i] = r;
+        });
+        gps_status first = GPS_OK;
+        for (uint32_t i = 0; i < nq; i++) {
+            if (statuses) statuses[i] = st[i];
+            if (st[i] != GPS_OK && first == GPS_OK) first = st[i];
+        }
+        if (first != GPS_OK) fail(first, "some queries of the batch failed (see statuses)");
+    });
+}
+
+gps_status gps_count_batch(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t nq,
+                           const gps_match_opts* opts, uint64_t* counts, gps_status* statuses) {
+    return guarded([&] {
+        if (!c || !g || (nq && (!qs || !counts))) fail(GPS_EINVAL, "null argument");
+        if (g->device != c->device) fail(GPS_EINVAL, "graph and ctx on different devices");
+        DeviceGuard dg(c->device);
+        const gps_match_opts o = resolve_opts(opts);
+        std::vector<gps_status> st(nq, GPS_OK);
+        run_batch(c, nq, st.data(), [&](gps_ctx* sc, uint32_t i) {
+            Filtered F;
+            QueryOut qo;
+            counts[i] = 0;
+            run_query(sc, g, &qs[i], &o, true, F, qo);
+            ctx_sync(sc);
+            sc->stats.queries++;
+            sc->stats.embeddings += qo.rows;
+            counts[i] = qo.rows;
+        });
+        gps_status first = GPS_OK;
+        for (uint32_t i = 0; i < nq; i++) {
+            if (statuses) statuses[i] = st[i];
+            if (st[i] != GPS_OK && first == GPS_OK) first = st[i];
+        }
+        if (first != GPS_OK) fail(first, "some queries of the batch failed (see statuses)");
+    });
+}
+
 gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols, const uint32_t** data,
                            int* on_device) {
     if (!r) return GPS_EINVAL;
@@ -615,11 +865,24 @@ gps_status gps_get_stats(gps_ctx* c, gps_stats* out) {
     return guarded([&] {
         if (!c || !out) fail(GPS_EINVAL, "null ctx/out");
         DeviceGuard dg(c->device);
-        ctx_sync(c);
-        unsigned long long hb[GPS_K_NCLASSES];
-        GPS_CK(cudaMemcpy(hb, c->d_bytes, sizeof(hb), cudaMemcpyDeviceToHost));
-        *out = c->stats;
-        for (int i = 0; i < GPS_K_NCLASSES; i++) out->k_bytes[i] += (double)hb[i];
+        *out = gps_stats{};
+        std::vector<gps_ctx*> all{c};
+        all.insert(all.end(), c->workers.begin(), c->workers.end());
+        for (gps_ctx* x : all) {
+            ctx_sync(x);
+            unsigned long long hb[GPS_K_NCLASSES];
+            GPS_CK(cudaMemcpy(hb, x->d_bytes, sizeof(hb), cudaMemcpyDeviceToHost));
+            out->queries += x->stats.queries;
+            out->embeddings += x->stats.embeddings;
+            out->launches += x->stats.launches;
+            out->host_syncs += x->stats.host_syncs;
+            for (int i = 0; i < GPS_K_NCLASSES; i++) {
+                out->k_launches[i] += x->stats.k_launches[i];
+                out->k_bytes[i] += x->stats.k_bytes[i] + (double)hb[i];
+                out->k_ms[i] += x->stats.k_ms[i];
+                out->k_timed[i] += x->stats.k_timed[i];
+            }
+        }
     });
 }
 
@@ -627,15 +890,20 @@ gps_status gps_reset_stats(gps_ctx* c) {
     return guarded([&] {
         if (!c) fail(GPS_EINVAL, "null ctx");
         DeviceGuard dg(c->device);
-        ctx_sync(c);
-        c->stats = gps_stats{};
-        GPS_CK(cudaMemset(c->d_bytes, 0, sizeof(unsigned long long) * GPS_K_NCLASSES));
+        std::vector<gps_ctx*> all{c};
+        all.insert(all.end(), c->workers.begin(), c->workers.end());
+        for (gps_ctx* x : all) {
+            ctx_sync(x);
+            x->stats = gps_stats{};
+            GPS_CK(cudaMemset(x->d_bytes, 0, sizeof(unsigned long long) * GPS_K_NCLASSES));
+        }
     });
 }
 
 gps_status gps_set_profiling(gps_ctx* c, uint32_t mask) {
     if (!c) return GPS_EINVAL;
     c->prof_mask = mask;
+    for (gps_ctx* w : c->workers) w->prof_mask = mask;
     return GPS_OK;
 }
 

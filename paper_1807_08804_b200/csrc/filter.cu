@@ -1,20 +1,25 @@
 // filter.cu -- filtering phase kernels (PAPER.md §"Filtering Phase").
 //
-//   k_check    a2  kernel_check (Alg. 2 line 7; Def. 3): one streaming
+//   k_check        a2 kernel_check (Alg. 2 line 7; Def. 3): one streaming
 //                  pass over vlab / off_out / off_in tests ALL k query vertices and
 //                  emits one bitmap word per (query vertex, 32 data vertices) with
-//                  __ballot_sync.  HBM bound: (2 + 4 + 4) B per vertex read,
-//                  k/8 B per vertex written.
-//   k_collect  a3  kernel_collect: stream compaction of a
-//                  candidate bitmap into the sorted c_array via popc + block scan,
-//                  also emitting the per-word rank prefix used for O(1) key lookup.
-//   k_explore  a4/a5 kernel_explore (Alg. 2 lines 14-22): one warp per
-//                  candidate u', lanes stride adj(u') (coalesced); prune u'
-//                  if some constraint has no fitting neighbour; else propagate its
-//                  fitting neighbours into per-neighbour scratch bitmaps (atomicOr).
-//   k_bitand   A15 reading: B[v] &= propagated set, scratch reset.
+//                  __ballot_sync.  HBM bound: (2 + 4 + 4) B per vertex read, k/8 B written.
+//   k_collect      a3 kernel_collect: stream compaction of a
+//                  candidate bitmap into the sorted c_array with popc + block scan +
+//                  decoupled look-back (one pass), also emitting the per-word rank
+//                  prefix (O(1) key lookup) and the candidates' degree prefixes (the
+//                  pair spaces of explore and EC).
+//   k_explore<M>   a4/a5 kernel_explore (Alg. 2 lines 14-22) over the PAIR
+//                  space (candidate u', constraint, arc of adj_dir(u')): M=prune marks the
+//                  constraints u' satisfies (Alg. 2 lines 15-18), M=propagate sets the
+//                  fitting neighbours of surviving candidates in per-neighbour scratch
+//                  bitmaps (lines 19-22).  Equal contiguous pair ranges per block replace
+//                  the paper's warp-per-candidate + block-per-hub split.
+//   k_clear        prune candidates that missed a constraint (atomicAnd on B[u]).
+//   k_bitand       reading R15: B[v] &= propagated set, scratch reset.
 #include "kernels.cuh"
-#include "prims.cuh"
+#include "lookback.cuh"
+#include "pairs.cuh"
 
 namespace gps {
 
@@ -43,156 +48,172 @@ __global__ void __launch_bounds__(256) k_check(DevGraph g, QDesc q, uint32_t* __
 }
 
 void run_check(gps_ctx* c, const DevGraph& g, const QDesc& q, uint32_t* B) {
-    uint32_t warps = g.nw;
-    uint32_t blocks = std::min<uint32_t>((warps + 7) / 8, (uint32_t)c->nsm * 8);
+    uint32_t blocks = std::min<uint32_t>((g.nw + 7) / 8, (uint32_t)c->nsm * 8);
     launch(c, GPS_K_CHECK, dim3(blocks), dim3(256), 0, k_check, g, q, B);
     c->stats.k_bytes[GPS_K_CHECK] += (double)g.n * 10.0 + (double)q.k * g.nw * 4.0;
 }
 
 // -------------------------------------------------------------- a3 collect
-constexpr int kColThreads = 256;
-constexpr int kColWords = 8;                       // bitmap words per thread
-constexpr int kColTile = kColThreads * kColWords;  // words per block
+constexpr int kColThreads = 256;   // one bitmap word (32 vertices) per thread
 
-__global__ void __launch_bounds__(kColThreads) k_collect_count(DevGraph g, CollectArgs a, uint32_t* part,
-                                                               uint32_t nblk) {
+__global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, CollectArgs a, LbScratch lb, uint32_t ntiles,
+                                                         uint32_t epoch) {
     const int y = blockIdx.y;
-    const uint32_t* B = a.B[y];
-    const uint32_t base = blockIdx.x * kColTile;
-    uint32_t s = 0;
-#pragma unroll
-    for (int i = 0; i < kColWords; i++) {
-        uint32_t w = base + i * kColThreads + threadIdx.x;
-        if (w < g.nw) s += __popc(B[w]);
-    }
-    s = block_sum(s);
-    if (threadIdx.x == 0) part[y * nblk + blockIdx.x] = s;
-}
-
-__global__ void __launch_bounds__(kColThreads) k_collect_write(DevGraph g, CollectArgs a, const uint32_t* part,
-                                                               uint32_t nblk) {
-    const int y = blockIdx.y;
-    const uint32_t* B = a.B[y];
-    const uint32_t base = blockIdx.x * kColTile;
-    // prefix of the preceding blocks (nblk is small: ceil(n / 65536))
-    uint32_t pre = 0;
-    if (part) {
-        uint32_t s = 0;
-        for (uint32_t j = threadIdx.x; j < blockIdx.x; j += blockDim.x) s += part[y * nblk + j];
-        pre = block_sum(s);
-    }
-    uint32_t wv[kColWords];
-    uint32_t cnt = 0;
-    const uint32_t w0 = base + threadIdx.x * kColWords;
-#pragma unroll
-    for (int i = 0; i < kColWords; i++) {
-        wv[i] = (w0 + i < g.nw) ? B[w0 + i] : 0u;
-        cnt += __popc(wv[i]);
-    }
-    uint32_t tot;
-    uint32_t ex = pre + block_excl_scan(cnt, &tot);
-    uint32_t* rp = a.rp[y];
-    uint32_t* out = a.carr[y];
-#pragma unroll
-    for (int i = 0; i < kColWords; i++) {
-        uint32_t w = w0 + i;
-        if (w < g.nw) {
-            rp[w] = ex;
-            uint32_t bits = wv[i];
-            while (bits) {
-                uint32_t b = __ffs(bits) - 1;
-                out[ex++] = w * 32 + b;
-                bits &= bits - 1;
-            }
+    const uint32_t tile = lb_ticket(lb.ctr + 3 * y, ntiles);
+    const uint32_t w = tile * kColThreads + threadIdx.x;
+    const uint32_t word = w < g.nw ? a.B[y][w] : 0u;
+    uint32_t c = __popc(word), so = 0, si = 0;
+    if (word) {
+        const uint32_t v0 = w * 32;
+        uint32_t bits = word;
+        while (bits) {
+            const uint32_t b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const uint32_t v = v0 + b;
+            so += __ldg(g.off_out + v + 1) - __ldg(g.off_out + v);
+            si += __ldg(g.off_in + v + 1) - __ldg(g.off_in + v);
         }
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-        rp[g.nw] = pre + tot;
-        *a.cnt[y] = pre + tot;
+    uint32_t tc, tso, tsi;
+    const uint32_t ec = block_excl_scan(c, &tc);
+    const uint32_t eso = block_excl_scan(so, &tso);
+    const uint32_t esi = block_excl_scan(si, &tsi);
+    __shared__ uint64_t s_pre[3];
+    if (threadIdx.x < 32) {
+        const size_t base = (size_t)(3 * y) * lb.max_tiles;
+        uint64_t p0 = lb_warp_lookback(lb.status + base, tile, tc, epoch);
+        uint64_t p1 = lb_warp_lookback(lb.status + base + lb.max_tiles, tile, tso, epoch);
+        uint64_t p2 = lb_warp_lookback(lb.status + base + 2 * (size_t)lb.max_tiles, tile, tsi, epoch);
+        if (threadIdx.x == 0) {
+            s_pre[0] = p0;
+            s_pre[1] = p1;
+            s_pre[2] = p2;
+        }
+    }
+    __syncthreads();
+    uint32_t rank = (uint32_t)s_pre[0] + ec;
+    uint32_t ro = (uint32_t)s_pre[1] + eso;
+    uint32_t ri = (uint32_t)s_pre[2] + esi;
+    if (w < g.nw) a.rp[y][w] = rank;
+    uint32_t* carr = a.carr[y];
+    uint32_t* sgo = a.seg_out[y];
+    uint32_t* sgi = a.seg_in[y];
+    unsigned long long* mask = a.mask[y];
+    uint32_t bits = word;
+    while (bits) {
+        const uint32_t b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const uint32_t v = w * 32 + b;
+        carr[rank] = v;
+        sgo[rank] = ro;
+        sgi[rank] = ri;
+        if (mask) mask[rank] = 0ull;
+        ro += __ldg(g.off_out + v + 1) - __ldg(g.off_out + v);
+        ri += __ldg(g.off_in + v + 1) - __ldg(g.off_in + v);
+        rank++;
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        const uint32_t C = (uint32_t)s_pre[0] + tc;
+        a.rp[y][g.nw] = C;
+        *a.cnt[y] = C;
+        sgo[C] = (uint32_t)s_pre[1] + tso;
+        sgi[C] = (uint32_t)s_pre[2] + tsi;
     }
 }
 
-void run_collect(gps_ctx* c, const DevGraph& g, const CollectArgs& a) {
+void run_collect(gps_ctx* c, const DevGraph& g, CollectArgs a) {
     if (a.nu == 0) return;
-    const uint32_t nblk = (g.nw + kColTile - 1) / kColTile;
-    if (nblk <= 1) {
-        launch(c, GPS_K_COLLECT, dim3(1, a.nu), dim3(kColThreads), 0, k_collect_write, g, a,
-               (const uint32_t*)nullptr, 1u);
-    } else {
-        DevPtr part(c, sizeof(uint32_t) * nblk * a.nu);
-        launch(c, GPS_K_COLLECT, dim3(nblk, a.nu), dim3(kColThreads), 0, k_collect_count, g, a, part.as<uint32_t>(),
-               nblk);
-        launch(c, GPS_K_COLLECT, dim3(nblk, a.nu), dim3(kColThreads), 0, k_collect_write, g, a,
-               (const uint32_t*)part.as<uint32_t>(), nblk);
-    }
-    // algorithmic: read the bitmap, write rank prefix + (<= n) ids; ids counted as written on device
+    const uint32_t ntiles = (g.nw + kColThreads - 1) / kColThreads;
+    LbScratch lb = lb_scratch(c, ntiles);
+    launch(c, GPS_K_COLLECT, dim3(ntiles, a.nu), dim3(kColThreads), 0, k_collect, g, a, lb, ntiles,
+           lb_next_epoch(c));
+    // algorithmic: read bitmap + 8 B offsets per vertex window, write rank prefix; ids/segments on the device side
     c->stats.k_bytes[GPS_K_COLLECT] += (double)a.nu * g.nw * 8.0;
 }
 
 // -------------------------------------------------------------- a4 explore
-__global__ void __launch_bounds__(256) k_explore(DevGraph g, ExploreArgs a, unsigned long long* bytes_acc) {
-    const uint32_t lane = lane_id();
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t cnt = *a.cnt;
-    unsigned long long bytes = 0;
-    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < cnt; i += nwarps) {
-        const uint32_t up = a.cands[i];
-        bool alive = true;
-        // prune (Alg. 2 lines 15-18): every constraint needs one fitting neighbour
-        for (int ci = 0; ci < a.nc && alive; ci++) {
-            const Cons cs = a.c[ci];
-            const uint32_t* off = cs.dir ? g.off_in : g.off_out;
-            const uint32_t* arc = cs.dir ? g.arc_in : g.arc_out;
-            const uint32_t s = off[up], e = off[up + 1];
-            bytes += 8 + 4ull * (e - s);
-            bool found = false;
-            for (uint32_t b = s; b < e; b += 32) {
-                const uint32_t j = b + lane;
-                bool ok = false;
-                if (j < e) {
-                    const uint32_t x = __ldg(arc + j);
-                    const uint32_t d = x >> g.lbits;
-                    ok = lab_ok(x, g.lmask, cs.lab) && d != up && bit_test(cs.Bv, d);
-                }
-                if (__any_sync(kFull, ok)) {
-                    found = true;
-                    break;
-                }
+constexpr int kET = 256;
+constexpr int kEI = 4;
+constexpr int kEW = 1024;
+
+template <int MODE>   // 0: prune (mark satisfied constraints), 1: propagate
+__global__ void __launch_bounds__(kET) k_explore(DevGraph g, const __grid_constant__ ExploreArgs a,
+                                                 unsigned long long* bytes_acc) {
+    __shared__ uint64_t s_off[kEW + 1];
+    __shared__ uint64_t s_row;
+    const uint32_t C = *a.cnt;
+    const uint64_t no = (uint64_t)a.no, ni = (uint64_t)a.ni;
+    auto offs = [&](uint64_t i) -> uint64_t {
+        return no * __ldg(a.seg_out + i) + ni * __ldg(a.seg_in + i);
+    };
+    const uint64_t P = offs(C);
+    uint64_t p0, p1;
+    pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
+    const int nc = a.no + a.ni;
+    const unsigned long long full = nc >= 64 ? ~0ull : ((1ull << nc) - 1ull);
+    for_pairs<kET, kEI, kEW>(p0, p1, (uint64_t)C, offs, s_off, &s_row,
+                             [&](bool v, uint64_t p, uint64_t row, uint64_t j) {
+        uint32_t key = 0xffffffffu;
+        unsigned long long bits = 0;
+        bool fits = false;
+        int ci = 0;
+        uint32_t d = 0;
+        if (v) {
+            key = __ldg(a.cands + row);
+            const uint32_t dout = __ldg(a.seg_out + row + 1) - __ldg(a.seg_out + row);
+            const uint32_t din = __ldg(a.seg_in + row + 1) - __ldg(a.seg_in + row);
+            uint32_t arc;
+            if (j < no * dout) {
+                ci = (int)(j / dout);
+                arc = __ldg(g.arc_out + __ldg(g.off_out + key) + (uint32_t)(j % dout));
+            } else {
+                const uint64_t jj = j - no * dout;
+                ci = a.no + (int)(jj / din);
+                arc = __ldg(g.arc_in + __ldg(g.off_in + key) + (uint32_t)(jj % din));
             }
-            alive = found;
+            const Cons& cs = a.c[ci];
+            d = arc >> g.lbits;
+            fits = lab_ok(arc, g.lmask, cs.lab) && d != key && bit_test(cs.Bv, d);
+            if (MODE == 1) fits = fits && __ldg(a.mask + row) == full;
+            bits = fits ? (1ull << ci) : 0ull;
         }
-        if (!alive) {
-            if (lane == 0) atomicAnd(a.Bu + (up >> 5), ~(1u << (up & 31)));
-            continue;
+        if (MODE == 0) {
+            uint32_t peers;
+            const uint32_t leader = warp_group_leader((uint32_t)row ^ (v ? 0u : 0x80000000u), peers);
+            const uint32_t lo = __reduce_or_sync(peers, (uint32_t)bits);
+            const uint32_t hi = __reduce_or_sync(peers, (uint32_t)(bits >> 32));
+            const unsigned long long agg = ((unsigned long long)hi << 32) | lo;
+            if (v && lane_id() == leader && agg && (__ldcg(a.mask + row) & agg) != agg)
+                atomicOr(a.mask + row, agg);
+        } else {
+            if (fits) atomicOr(a.c[ci].X + (d >> 5), 1u << (d & 31));
         }
-        // propagate (Alg. 2 lines 19-22): fitting neighbours become candidates of v
-        for (int ci = 0; ci < a.nc; ci++) {
-            const Cons cs = a.c[ci];
-            if (!cs.X) continue;
-            const uint32_t* off = cs.dir ? g.off_in : g.off_out;
-            const uint32_t* arc = cs.dir ? g.arc_in : g.arc_out;
-            const uint32_t s = off[up], e = off[up + 1];
-            for (uint32_t j = s + lane; j < e; j += 32) {
-                const uint32_t x = __ldg(arc + j);
-                const uint32_t d = x >> g.lbits;
-                if (lab_ok(x, g.lmask, cs.lab) && d != up && bit_test(cs.Bv, d))
-                    atomicOr(cs.X + (d >> 5), 1u << (d & 31));
-            }
-        }
-    }
+    });
     if (bytes_acc) {
-        // one lane per warp accounted the bytes; aggregate per block
-        unsigned long long v = lane == 0 ? bytes : 0ull;
-        v = block_sum(v);
-        if (threadIdx.x == 0 && v) atomicAdd(bytes_acc, v);
+        // algorithmic bytes: 4 per arc examined (the 8 B of row offsets per candidate are read by collect)
+        unsigned long long mine = (p1 - p0) * 4ull;
+        if (threadIdx.x == 0 && mine) atomicAdd(bytes_acc, mine);
     }
 }
 
-void run_explore(gps_ctx* c, const DevGraph& g, const ExploreArgs& a, uint32_t max_cands) {
-    if (max_cands == 0) return;
-    uint32_t warps_needed = max_cands;
-    uint32_t blocks = std::min<uint32_t>((warps_needed + 7) / 8, (uint32_t)c->nsm * 8);
-    launch(c, GPS_K_EXPLORE, dim3(blocks), dim3(256), 0, k_explore, g, a, c->d_bytes + GPS_K_EXPLORE);
+__global__ void __launch_bounds__(256) k_clear(const __grid_constant__ ExploreArgs a) {
+    const uint32_t C = *a.cnt;
+    const int nc = a.no + a.ni;
+    const unsigned long long full = nc >= 64 ? ~0ull : ((1ull << nc) - 1ull);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < C; i += gridDim.x * blockDim.x) {
+        if (a.mask[i] != full) {
+            const uint32_t key = a.cands[i];
+            atomicAnd(a.Bu + (key >> 5), ~(1u << (key & 31)));
+        }
+    }
+}
+
+void run_explore(gps_ctx* c, const DevGraph& g, const ExploreArgs& a) {
+    if (a.no + a.ni == 0) return;
+    const uint32_t G = (uint32_t)c->nsm * 4;
+    launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), 0, k_explore<0>, g, a, c->d_bytes + GPS_K_EXPLORE);
+    launch(c, GPS_K_EXPLORE, dim3((uint32_t)c->nsm * 2), dim3(256), 0, k_clear, a);
+    if (a.propagate) launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), 0, k_explore<1>, g, a, c->d_bytes + GPS_K_EXPLORE);
 }
 
 // --------------------------------------------------------------- bit-and

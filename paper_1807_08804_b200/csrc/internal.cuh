@@ -10,6 +10,10 @@
 #include "../../include/gpsense.h"
 
 namespace gps {
+struct WorkerPool;
+}
+
+namespace gps {
 
 constexpr int kWarp = 32;
 constexpr uint32_t kFull = 0xffffffffu;
@@ -73,8 +77,16 @@ struct gps_ctx {
     unsigned long long* d_bytes = nullptr;   // [GPS_K_NCLASSES] device-accumulated algorithmic bytes
     uint64_t* d_info = nullptr;              // small device scratch (counts, totals)
     uint64_t* h_info = nullptr;              // pinned mirror
-    unsigned int* d_done = nullptr;          // last-block counters
+    unsigned int* d_done = nullptr;          // last-block counters [1 + GPS_MAX_QE], self-resetting
+    uint64_t* lb_status = nullptr;           // decoupled look-back status words
+    unsigned int* lb_ctr = nullptr;          // look-back tickets, self-resetting
+    uint32_t lb_tiles = 0;                   // tiles per slot currently allocated
+    uint32_t lb_epoch = 0;                   // launch epoch (never 0 once used)
     std::vector<gps_result*> results;        // live device results (freed at destroy)
+    // batch execution: worker sub-contexts (own stream + scratch) driven by a host thread pool
+    std::vector<gps_ctx*> workers;
+    gps::WorkerPool* pool = nullptr;
+    uint32_t nworkers_req = 0;               // 0 = default (8)
 };
 
 struct gps_graph {

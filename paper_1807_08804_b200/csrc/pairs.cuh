@@ -1,0 +1,129 @@
+// pairs.cuh -- load-balanced iteration over a "pair space".
+//
+// Rows (candidate keys, partial embeddings) own segments of work (adjacency
+// arcs, EC values) given by a non-decreasing offset function offs(i), i in
+// [0, nrows], offs(nrows) = P.  G persistent blocks each take an equal,
+// contiguous range of pairs -- so a hub row with 10^4 arcs is shared by many
+// blocks instead of stalling one warp (the imbalance P:784 addresses with
+// "an entire block instead of a warp").  Within a block, consecutive threads
+// get consecutive pairs (coalesced segment reads); the row of each pair is
+// found by binary search in a shared-memory window of offsets.
+#pragma once
+#include "prims.cuh"
+
+namespace gps {
+
+template <typename OffF>
+__device__ __forceinline__ uint64_t pairs_find_global(OffF offs, uint64_t lo, uint64_t hi, uint64_t p) {
+    // largest r in [lo, hi) with offs(r) <= p   (requires offs(lo) <= p)
+    while (hi - lo > 1) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        if (offs(mid) <= p) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t pairs_find_smem(const uint64_t* s, uint32_t n, uint64_t p) {
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (s[mid] <= p) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// Contiguous share [p0, p1) of P pairs for block b of G.
+__device__ __forceinline__ void pairs_range(uint64_t P, uint32_t b, uint32_t G, uint64_t& p0, uint64_t& p1) {
+    const uint64_t q = P / G, rem = P % G;
+    p0 = q * b + (b < rem ? b : rem);
+    p1 = p0 + q + (b < rem ? 1 : 0);
+}
+
+// Calls body(valid, p, row, j) for every item slot of the block's range, T*IPT
+// slots per chunk, all threads together (body may use block-wide barriers).
+// s_off must hold W+1 uint64 in shared memory.
+template <int T, int IPT, int W, typename OffF, typename Body>
+__device__ __forceinline__ void for_pairs(uint64_t p0, uint64_t p1, uint64_t nrows, OffF offs, uint64_t* s_off,
+                                          uint64_t* s_row, Body&& body) {
+    if (p0 >= p1) return;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) *s_row = pairs_find_global(offs, 0, nrows, p0);
+    __syncthreads();
+    uint64_t r0 = *s_row;
+    for (uint64_t cp = p0; cp < p1; cp += (uint64_t)T * IPT) {
+        const uint64_t cend = cp + (uint64_t)T * IPT < p1 ? cp + (uint64_t)T * IPT : p1;
+        const uint32_t wn = (uint32_t)((nrows - r0) < (uint64_t)W ? (nrows - r0) : (uint64_t)W);
+        for (uint32_t i = tid; i <= wn; i += T) s_off[i] = offs(r0 + i);
+        __syncthreads();
+        const uint64_t wend = s_off[wn];
+#pragma unroll 1
+        for (int it = 0; it < IPT; it++) {
+            const uint64_t p = cp + (uint64_t)it * T + tid;
+            const bool v = p < cend;
+            uint64_t row = 0, base = 0;
+            if (v) {
+                if (p < wend) {
+                    const uint32_t i = pairs_find_smem(s_off, wn, p);
+                    row = r0 + i;
+                    base = s_off[i];
+                } else {
+                    row = pairs_find_global(offs, r0 + wn, nrows, p);
+                    base = offs(row);
+                }
+            }
+            body(v, p, row, p - base);
+        }
+        __syncthreads();
+        if (cend < p1) {
+            if (tid == 0)
+                *s_row = (cend < wend) ? r0 + pairs_find_smem(s_off, wn, cend)
+                                       : pairs_find_global(offs, r0 + wn, nrows, cend);
+            __syncthreads();
+            r0 = *s_row;
+        }
+    }
+}
+
+// Warp-segmented reduction for lanes holding consecutive pairs: lanes with the
+// same key form one group (keys are non-decreasing across lanes).  Returns the
+// group's OR / sum in the group's lowest lane (is_leader), 0 elsewhere.
+__device__ __forceinline__ uint32_t warp_group_leader(uint32_t key, uint32_t& peers) {
+    peers = __match_any_sync(kFull, key);
+    return (uint32_t)(__ffs(peers) - 1);
+}
+
+// Last-block pattern: every block stores its count in blk[b]; the last block to
+// finish turns blk[0..G) into exclusive offsets, blk[G] = total, info[0] = P,
+// info[1] = total, and resets *done.
+__device__ __forceinline__ void last_block_scan(uint64_t* blk, uint32_t G, unsigned int* done, uint64_t* info,
+                                                uint64_t P, uint64_t my_count) {
+    __shared__ bool s_last;
+    my_count = block_sum(my_count);
+    if (threadIdx.x == 0) {
+        blk[blockIdx.x] = my_count;
+        __threadfence();
+        const unsigned prev = atomicAdd(done, 1u);
+        s_last = (prev == G - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        uint64_t carry = 0;
+        for (uint32_t b = 0; b < G; b += blockDim.x) {
+            const uint32_t i = b + threadIdx.x;
+            const uint64_t v = i < G ? __ldcg(blk + i) : 0ull;
+            uint64_t tot;
+            const uint64_t ex = block_excl_scan(v, &tot);
+            if (i < G) blk[i] = carry + ex;
+            carry += tot;
+        }
+        if (threadIdx.x == 0) {
+            blk[G] = carry;
+            info[0] = P;
+            info[1] = carry;
+            *done = 0u;
+        }
+    }
+}
+
+}  // namespace gps

@@ -97,6 +97,9 @@ def _load_lib():
         "gps_set_profiling": (S, [P, ctypes.c_uint32]),
         "gps_debug_plan": (S, [P, P, P, P, P, P, P]),
         "gps_debug_candidates": (S, [P, P, P, P, S, P]),
+        "gps_match_batch": (S, [P, P, P, ctypes.c_uint32, P, P, P]),
+        "gps_count_batch": (S, [P, P, P, ctypes.c_uint32, P, P, P]),
+        "gps_set_workers": (S, [P, ctypes.c_uint32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -109,7 +112,8 @@ lib = _load_lib()
 EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_graph", "gps_free_graph",
             "gps_graph_info", "gps_match", "gps_match_host", "gps_count", "gps_result_info",
             "gps_result_free", "gps_last_error", "gps_get_stats", "gps_reset_stats",
-            "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates"]
+            "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates", "gps_match_batch",
+            "gps_count_batch", "gps_set_workers"]
 
 
 def _check(st: int):
@@ -188,7 +192,7 @@ class Graph:
 class Context:
     """One gps_ctx: a device and a stream (default: a library-owned stream)."""
 
-    def __init__(self, device: int = 0, stream=None):
+    def __init__(self, device: int = 0, stream=None, workers: int = 0):
         o = CtxOpts(device, None, None, 0, 1)
         if stream is not None:
             o.stream = int(getattr(stream, "cuda_stream", stream))
@@ -196,6 +200,11 @@ class Context:
         _check(lib.gps_create(ctypes.byref(o), ctypes.byref(h)))
         self._h = h
         self.device = device
+        if workers:
+            self.set_workers(workers)
+
+    def set_workers(self, n: int):
+        _check(lib.gps_set_workers(self._h, int(n)))
 
     def close(self):
         if self._h:
@@ -271,6 +280,59 @@ class Context:
                                   ctypes.c_void_p(ptr), cap, ctypes.byref(rows)))
         flat = out.reshape(-1) if not hasattr(out, "data_ptr") else out.view(-1)
         return flat[: rows.value * qa.k].reshape(rows.value, qa.k)
+
+    def _batch_desc(self, queries):
+        qas = [_QueryArrays(q) for q in queries]
+        arr = (QueryDesc * max(len(qas), 1))()
+        for i, qa in enumerate(qas):
+            arr[i] = qa.desc
+        return qas, arr
+
+    def match_batch(self, graph: Graph, queries, opts: Optional[MatchOpts] = None, device: bool = True):
+        """All embeddings of every query, run concurrently by the library's worker pool.
+
+        Returns a list of torch uint32 (rows, k) CUDA tensors (zero-copy), or of
+        numpy arrays copied to host by the library when device=False."""
+        import torch
+        qas, arr = self._batch_desc(queries)
+        n = len(qas)
+        res = (ctypes.c_void_p * max(n, 1))()
+        st = np.zeros(max(n, 1), np.int32)
+        o = opts if opts is not None else default_opts()
+        o = MatchOpts(o.refine_rounds, o.reverse_refine, o.lowconn_threshold, 1 if device else 0)
+        rc = lib.gps_match_batch(self._h, graph.handle, arr, n, ctypes.byref(o), res,
+                                 ctypes.c_void_p(st.ctypes.data))
+        out = []
+        for i in range(n):
+            if not res[i]:
+                continue
+            rows, cols, ptr, ondev = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_void_p(), ctypes.c_int()
+            lib.gps_result_info(res[i], ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(ptr), ctypes.byref(ondev))
+            if not device:
+                nn = rows.value * cols.value
+                a = np.zeros((rows.value, cols.value), np.uint32)
+                if nn:
+                    ctypes.memmove(a.ctypes.data, ptr.value, nn * 4)
+                lib.gps_result_free(ctypes.c_void_p(res[i]))
+                out.append(a)
+                continue
+            holder = _DeviceRows(ctypes.c_void_p(res[i]), rows.value, cols.value, ptr.value)
+            if rows.value == 0:
+                del holder
+                out.append(torch.empty((0, cols.value), dtype=torch.uint32, device=f"cuda:{self.device}"))
+            else:
+                out.append(torch.as_tensor(holder, device=f"cuda:{self.device}"))
+        _check(rc)
+        return out
+
+    def count_batch(self, graph: Graph, queries, opts: Optional[MatchOpts] = None) -> np.ndarray:
+        qas, arr = self._batch_desc(queries)
+        n = len(qas)
+        counts = np.zeros(max(n, 1), np.uint64)
+        _check(lib.gps_count_batch(self._h, graph.handle, arr, n,
+                                   ctypes.byref(opts) if opts is not None else None,
+                                   ctypes.c_void_p(counts.ctypes.data), None))
+        return counts[:n]
 
     def count(self, graph: Graph, q, opts: Optional[MatchOpts] = None) -> int:
         qa = _QueryArrays(q)

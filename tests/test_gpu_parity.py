@@ -291,3 +291,33 @@ def test_stats_count_launches(ctx, cfg1):
     st = ctx.stats()
     assert st["queries"] == 1 and st["launches"] > 5
     assert st["kernels"]["join_count"]["launches"] >= 1
+
+
+# ------------------------------------------------------------ batched execution
+def test_cfg2_match_batch(ctx, cfg2):
+    """gps_match_batch (worker pool, concurrent streams) == stored oracle counts; sets for a sample."""
+    g, G, data = cfg2
+    qs = [Query.from_json(d["query"]) for d in data["queries"]]
+    outs = ctx.match_batch(G, qs)
+    assert len(outs) == len(qs)
+    for t, d in zip(outs, data["queries"]):
+        assert t.shape == (d["oracle_count"], 6)
+    og = oracle.OracleGraph(g)
+    small = sorted(range(len(qs)), key=lambda i: data["queries"][i]["oracle_count"])[:5]
+    for i in small:
+        assert np.array_equal(_rows(outs[i]), oracle.match(og, qs[i]))
+    counts = ctx.count_batch(G, qs)
+    assert counts.tolist() == [d["oracle_count"] for d in data["queries"]]
+
+
+def test_batch_workers_and_errors(gps, ctx, cfg1):
+    g, G, og = cfg1
+    qs = [triangle_tail(lab) for lab in [(-1, -1, -1, -1), (0, 1, 2, 3), (1, -1, 2, -1)]] * 5
+    for w in (1, 3, 8):
+        ctx.set_workers(w)
+        assert ctx.count_batch(G, qs).tolist() == [oracle.count(og, q) for q in qs]
+    bad = qs[:2] + [Query(3, [-1] * 3, [-1] * 3, [(0, 1, -1)])]
+    with pytest.raises(gps.GpsError) as e:
+        ctx.count_batch(G, bad)
+    assert e.value.status == gps.GPS_EDISCONNECTED
+    ctx.set_workers(0)
