@@ -160,8 +160,11 @@ GPS_API gps_status gps_match_batch(gps_ctx* ctx, const gps_graph* g, const gps_q
                                    const gps_match_opts* opts, gps_result** results, gps_status* statuses);
 GPS_API gps_status gps_count_batch(gps_ctx* ctx, const gps_graph* g, const gps_query* queries, uint32_t nq,
                                    const gps_match_opts* opts, uint64_t* counts, gps_status* statuses);
-/* Number of batch workers (1..64; 0 = default 8).  Destroys existing workers (and their results). */
+/* Number of batch workers (1..64; 0 = default 2).  Destroys existing workers (and their results). */
 GPS_API gps_status gps_set_workers(gps_ctx* ctx, uint32_t n);
+/* Queries per worker hand-out in the batch calls (each hand-out runs batch-synchronously:
+ * one launch per phase for all its queries); 0 = default 64. */
+GPS_API gps_status gps_set_slice(gps_ctx* ctx, uint32_t queries);
 
 /* rows, cols (= k), data (device or host pointer, owned by the result), on_device. */
 GPS_API gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols,

@@ -1,0 +1,238 @@
+// ctx.cu -- runtime plumbing of a gps_ctx: errors, stream-ordered device memory,
+// pinned staging for job uploads, pinned host results, decoupled look-back
+// scratch, event timing, and the host worker pool of the batch API.
+#include <algorithm>
+#include <cstring>
+
+#include "kernels.cuh"
+#include "runtime.h"
+
+namespace gps {
+
+static thread_local std::string g_err;
+void set_last_error(const std::string& m) { g_err = m; }
+const char* last_error() { return g_err.c_str(); }
+void fail(gps_status s, const std::string& m) { throw Error{s, m}; }
+void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    gps_status s = (e == cudaErrorMemoryAllocation) ? GPS_ENOMEM : GPS_ECUDA;
+    (void)cudaGetLastError();
+    throw Error{s, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" + std::to_string(line) + ")"};
+}
+
+cudaEvent_t ctx_event(gps_ctx* c) {
+    if (c->event_pool.empty()) {
+        cudaEvent_t e;
+        GPS_CK(cudaEventCreate(&e));
+        return e;
+    }
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+}
+void ctx_harvest(gps_ctx* c) {
+    for (auto& t : c->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, t.e0, t.e1) == cudaSuccess) {
+            c->stats.k_ms[t.cls] += ms;
+            c->stats.k_timed[t.cls]++;
+        }
+        c->event_pool.push_back(t.e0);
+        c->event_pool.push_back(t.e1);
+    }
+    c->pending.clear();
+}
+void ctx_sync(gps_ctx* c) {
+    GPS_CK(cudaStreamSynchronize(c->stream));
+    c->stats.host_syncs++;
+    c->h_arena_off = 0;   // every staged upload has completed
+    ctx_harvest(c);
+}
+
+void* dmalloc(gps_ctx* c, size_t bytes) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, c->stream);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        fail(GPS_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+    }
+    return p;
+}
+void dfree(gps_ctx* c, void* p) {
+    if (p) (void)cudaFreeAsync(p, c->stream);
+}
+
+DevBlock::~DevBlock() {
+    if (p && c) (void)cudaFreeAsync(p, c->stream);
+}
+Block make_block(gps_ctx* c, size_t bytes) {
+    auto b = std::make_shared<DevBlock>();
+    b->c = c;
+    b->p = dmalloc(c, bytes ? bytes : 16);
+    return b;
+}
+
+void* upload_bytes(gps_ctx* c, const void* src, size_t bytes, std::vector<DevPtr>& keep) {
+    const size_t need = (bytes + 255) & ~size_t(255);
+    if (c->h_arena_off + need > c->h_arena_cap) {
+        if (c->h_arena_off) ctx_sync(c);   // staged copies done: the arena can be reused
+        if (need > c->h_arena_cap) {
+            if (c->h_arena) cudaFreeHost(c->h_arena);
+            c->h_arena = nullptr;
+            size_t cap = std::max<size_t>(need, std::max<size_t>(c->h_arena_cap * 2, 4u << 20));
+            GPS_CK(cudaMallocHost(&c->h_arena, cap));
+            c->h_arena_cap = cap;
+        }
+    }
+    char* h = c->h_arena + c->h_arena_off;
+    c->h_arena_off += need;
+    if (bytes) std::memcpy(h, src, bytes);
+    keep.emplace_back(c, need ? need : 16);
+    void* d = keep.back().p;
+    if (bytes) GPS_CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    return d;
+}
+
+void* pinned_alloc(gps_ctx* c, size_t bytes, size_t* got) {
+    size_t want = std::max<size_t>(bytes, 4096);
+    auto it = c->pinned_free.lower_bound(want);
+    if (it != c->pinned_free.end() && it->first <= 2 * want + (1u << 20)) {
+        void* p = it->second;
+        *got = it->first;
+        c->pinned_free.erase(it);
+        return p;
+    }
+    size_t cap = 4096;
+    while (cap < want) cap <<= 1;
+    void* p = nullptr;
+    GPS_CK(cudaMallocHost(&p, cap));
+    *got = cap;
+    return p;
+}
+void pinned_release(gps_ctx* c, void* p, size_t bytes) {
+    if (p) c->pinned_free.emplace(bytes, p);
+}
+
+LbScratch lb_scratch(gps_ctx* c, uint32_t slots, uint32_t tiles) {
+    if (tiles == 0) tiles = 1;
+    if (slots == 0) slots = 1;
+    if (tiles > c->lb_tiles || slots > c->lb_slots) {
+        const uint32_t tcap = std::max<uint32_t>(std::max(tiles, c->lb_tiles), 64);
+        const uint32_t scap = std::max<uint32_t>(std::max(slots, c->lb_slots), 192);
+        if (c->lb_status) dfree(c, c->lb_status);
+        if (c->lb_ctr) dfree(c, c->lb_ctr);
+        c->lb_status = static_cast<uint64_t*>(dmalloc(c, sizeof(uint64_t) * (size_t)tcap * scap));
+        c->lb_ctr = static_cast<unsigned int*>(dmalloc(c, sizeof(unsigned int) * scap));
+        GPS_CK(cudaMemsetAsync(c->lb_status, 0, sizeof(uint64_t) * (size_t)tcap * scap, c->stream));
+        GPS_CK(cudaMemsetAsync(c->lb_ctr, 0, sizeof(unsigned int) * scap, c->stream));
+        c->lb_tiles = tcap;
+        c->lb_slots = scap;
+    }
+    return LbScratch{c->lb_status, c->lb_ctr, c->lb_tiles};
+}
+uint32_t lb_next_epoch(gps_ctx* c) {
+    c->lb_epoch++;
+    if (c->lb_epoch >= (1u << 20)) {   // wrap: clear stale words so old epochs cannot alias
+        GPS_CK(cudaMemsetAsync(c->lb_status, 0, sizeof(uint64_t) * (size_t)c->lb_tiles * c->lb_slots, c->stream));
+        c->lb_epoch = 1;
+    }
+    return c->lb_epoch;
+}
+
+void ctx_init(gps_ctx* c, int dev, cudaStream_t stream) {
+    c->device = dev;
+    GPS_CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (stream) {
+        c->stream = stream;
+    } else {
+        GPS_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    cudaMemPool_t pool;
+    GPS_CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = ~0ull;
+    GPS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    GPS_CK(cudaMalloc(&c->d_bytes, sizeof(unsigned long long) * GPS_K_NCLASSES));
+    GPS_CK(cudaMemset(c->d_bytes, 0, sizeof(unsigned long long) * GPS_K_NCLASSES));
+    GPS_CK(cudaMalloc(&c->d_info, sizeof(uint64_t) * 128));
+    GPS_CK(cudaMallocHost(&c->h_info, sizeof(uint64_t) * 128));
+    GPS_CK(cudaMalloc(&c->d_done, sizeof(unsigned int) * 64));
+    GPS_CK(cudaMemset(c->d_done, 0, sizeof(unsigned int) * 64));
+    GPS_CK(cudaDeviceSynchronize());
+}
+
+void ctx_release(gps_ctx* c) {
+    cudaStreamSynchronize(c->stream);
+    for (gps_result* r : c->results) {
+        if (r->on_device) {
+            r->hold.reset();
+        } else if (r->data) {
+            cudaFreeHost(r->data);
+        }
+        r->data = nullptr;
+        r->rows = 0;
+        r->ctx = nullptr;
+    }
+    c->results.clear();
+    if (c->lb_status) cudaFreeAsync(c->lb_status, c->stream);
+    if (c->lb_ctr) cudaFreeAsync(c->lb_ctr, c->stream);
+    c->lb_status = nullptr;
+    c->lb_ctr = nullptr;
+    cudaStreamSynchronize(c->stream);
+    for (auto& t : c->pending) {
+        c->event_pool.push_back(t.e0);
+        c->event_pool.push_back(t.e1);
+    }
+    c->pending.clear();
+    for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+    c->event_pool.clear();
+    for (auto& kv : c->pinned_free) cudaFreeHost(kv.second);
+    c->pinned_free.clear();
+    if (c->h_arena) cudaFreeHost(c->h_arena);
+    c->h_arena = nullptr;
+    cudaFree(c->d_bytes);
+    cudaFree(c->d_info);
+    cudaFreeHost(c->h_info);
+    cudaFree(c->d_done);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+}
+
+WorkerPool::WorkerPool(int n) {
+    for (int w = 0; w < n; w++)
+        th.emplace_back([this, w] {
+            uint64_t seen = 0;
+            for (;;) {
+                std::function<void(int)> f;
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return stop || gen != seen; });
+                    if (stop) return;
+                    seen = gen;
+                    f = job;
+                }
+                f(w);
+                {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (--remaining == 0) done_cv.notify_all();
+                }
+            }
+        });
+}
+void WorkerPool::run(std::function<void(int)> f) {
+    std::unique_lock<std::mutex> lk(mu);
+    job = std::move(f);
+    remaining = (int)th.size();
+    gen++;
+    cv.notify_all();
+    done_cv.wait(lk, [&] { return remaining == 0; });
+}
+WorkerPool::~WorkerPool() {
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : th) t.join();
+}
+
+}  // namespace gps

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -78,15 +80,20 @@ struct gps_ctx {
     uint64_t* d_info = nullptr;              // small device scratch (counts, totals)
     uint64_t* h_info = nullptr;              // pinned mirror
     unsigned int* d_done = nullptr;          // last-block counters [1 + GPS_MAX_QE], self-resetting
-    uint64_t* lb_status = nullptr;           // decoupled look-back status words
-    unsigned int* lb_ctr = nullptr;          // look-back tickets, self-resetting
+    uint64_t* lb_status = nullptr;           // decoupled look-back status words [lb_slots * lb_tiles]
+    unsigned int* lb_ctr = nullptr;          // look-back tickets [lb_slots], self-resetting
     uint32_t lb_tiles = 0;                   // tiles per slot currently allocated
+    uint32_t lb_slots = 0;                   // slots currently allocated
     uint32_t lb_epoch = 0;                   // launch epoch (never 0 once used)
+    char* h_arena = nullptr;                 // pinned staging for job uploads (bump, reset at every sync)
+    size_t h_arena_cap = 0, h_arena_off = 0;
+    std::multimap<size_t, void*> pinned_free;  // pinned host buffers for host results (reused)
     std::vector<gps_result*> results;        // live device results (freed at destroy)
     // batch execution: worker sub-contexts (own stream + scratch) driven by a host thread pool
     std::vector<gps_ctx*> workers;
     gps::WorkerPool* pool = nullptr;
-    uint32_t nworkers_req = 0;               // 0 = default (8)
+    uint32_t nworkers_req = 0;               // 0 = default (2)
+    uint32_t slice = 0;                      // queries per worker hand-out (0 = default 64)
 };
 
 struct gps_graph {
@@ -99,12 +106,25 @@ struct gps_graph {
     void* mem[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
+namespace gps {
+// A stream-ordered device allocation shared by several results (a batch writes
+// the final rows of many queries into one buffer).
+struct DevBlock {
+    gps_ctx* c = nullptr;
+    void* p = nullptr;
+    ~DevBlock();
+};
+using Block = std::shared_ptr<DevBlock>;
+}  // namespace gps
+
 struct gps_result {
     uint64_t rows = 0;
     uint32_t cols = 0;
     uint32_t* data = nullptr;
     int on_device = 0;
-    gps_ctx* ctx = nullptr;
+    gps_ctx* ctx = nullptr;       // owner (device rows / pinned host rows)
+    gps::Block hold;              // device rows live in this block
+    size_t host_bytes = 0;        // pinned host buffer size (on_device == 0)
 };
 
 namespace gps {
@@ -194,6 +214,17 @@ inline void scan_exclusive1(gps_ctx* c, const TI* in, TO* out, uint64_t n) {
 }
 // LSD radix sort of u64 keys on bits [0, nbits); result in *keys (ping-pong with tmp).
 void radix_sort_u64(gps_ctx* c, uint64_t* keys, uint64_t* tmp, uint64_t n, int nbits);
+
+// ---- pinned host memory (ctx.cu) --------------------------------------------
+void* pinned_alloc(gps_ctx* c, size_t bytes, size_t* got);
+void pinned_release(gps_ctx* c, void* p, size_t bytes);
+// Copy a host array into device memory via the pinned arena (stream-ordered).
+void* upload_bytes(gps_ctx* c, const void* src, size_t bytes, std::vector<DevPtr>& keep);
+template <typename T>
+T* upload(gps_ctx* c, const std::vector<T>& v, std::vector<DevPtr>& keep) {
+    return static_cast<T*>(upload_bytes(c, v.data(), sizeof(T) * v.size(), keep));
+}
+Block make_block(gps_ctx* c, size_t bytes);
 
 // ---- graph load (load.cu) ---------------------------------------------------
 void load_graph(gps_ctx* c, const gps_csr_desc* desc, gps_graph* g);

@@ -127,3 +127,41 @@ __device__ __forceinline__ void last_block_scan(uint64_t* blk, uint32_t G, unsig
 }
 
 }  // namespace gps
+
+namespace gps {
+
+// Exclusive prefix of per-job pair counts pj(i), i < nj, into s_jp[0..nj]
+// (shared memory).  All threads of the block call it.
+template <typename PF>
+__device__ __forceinline__ void job_prefix(uint32_t nj, PF pj, uint64_t* s_jp) {
+    uint64_t carry = 0;
+    for (uint32_t b = 0; b < nj; b += blockDim.x) {
+        const uint32_t i = b + threadIdx.x;
+        const uint64_t v = i < nj ? pj(i) : 0ull;
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(v, &tot);
+        if (i < nj) s_jp[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) s_jp[nj] = carry;
+    __syncthreads();
+}
+
+// Calls jb(j, lo, hi) for every job j whose pair range meets [p0, p1), with the
+// job-local sub-range [lo, hi).  Uniform across the block.
+template <typename JB>
+__device__ __forceinline__ void for_job_ranges(const uint64_t* s_jp, uint32_t nj, uint64_t p0, uint64_t p1, JB&& jb) {
+    if (p0 >= p1 || nj == 0) return;
+    uint32_t lo = 0, hi = nj;   // largest j < nj with s_jp[j] <= p0
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (s_jp[mid] <= p0) lo = mid; else hi = mid;
+    }
+    for (uint32_t j = lo; j < nj && s_jp[j] < p1; j++) {
+        const uint64_t a = p0 > s_jp[j] ? p0 : s_jp[j];
+        const uint64_t b = p1 < s_jp[j + 1] ? p1 : s_jp[j + 1];
+        if (a < b) jb(j, a - s_jp[j], b - s_jp[j]);
+    }
+}
+
+}  // namespace gps

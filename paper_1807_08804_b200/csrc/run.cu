@@ -1,0 +1,525 @@
+// run.cu -- the batch-synchronous executor of Alg. 1 FilteringAndJoining.
+//
+// A batch of queries runs phase by phase; every phase is ONE launch for all
+// queries (jobs), so launch count and host syncs are per batch, not per query:
+//
+//   plan (host)            per query: f(u), T, O, refine order (planner.cu)
+//   kernel_check                  1 launch                     (a2)
+//   filter step s = 0..S-1        collect, prune(+clear), propagate, bit-and (a3-a5)
+//   final collect                 1 launch, sync #1 -> |C(u)|   (a3)
+//   collect_edge_candidates       count, scan, sync #2 -> #EC(e) -> join order, write (a6, a7)
+//   join step s                   seg, count, sync, write      (a8, a9)
+//
+// Every query's outputs of a phase are concatenated in job order, so one global
+// scan / compaction serves the whole batch (two-step output scheme).
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "kernels.cuh"
+#include "planner.h"
+#include "runtime.h"
+
+namespace gps {
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr uint32_t kMaxBatch = 512;            // queries per chunk
+constexpr size_t kChunkBytes = size_t(6) << 30;  // filter arena budget per chunk
+
+struct Carve {
+    char* base = nullptr;
+    size_t off = 0;
+    template <typename T>
+    T* take(size_t n) {
+        off = (off + kAlign - 1) & ~(kAlign - 1);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += sizeof(T) * (n ? n : 1);
+        return p;
+    }
+};
+
+struct QS {                       // one query of a chunk
+    uint32_t idx = 0;             // position in the caller's array
+    Plan plan;
+    int k = 0, E = 0;
+    uint32_t cap[GPS_MAX_QV];     // c_array capacity per vertex: min(n, freq(u))
+    uint32_t* B = nullptr;
+    uint32_t* X = nullptr;
+    uint32_t* rp = nullptr;
+    uint32_t* carr[GPS_MAX_QV];
+    uint32_t* seg[GPS_MAX_QV][2];
+    uint32_t* cnt = nullptr;      // k counters, inside the chunk-wide counter array
+    unsigned long long* mask = nullptr;
+    uint32_t C[GPS_MAX_QV];
+    bool live = true;
+    int ecjob[GPS_MAX_QE][2];
+    std::vector<JoinStepPlan> steps;
+    int col_of[GPS_MAX_QV];
+    uint8_t vert_of_col[GPS_MAX_QV + 1];
+    const uint32_t* M = nullptr;
+    uint64_t R = 0;
+};
+
+struct Chunk {
+    gps_ctx* c;
+    const gps_graph* g;
+    std::vector<QS*> qs;
+    Block arena;                  // filter state of every query
+    uint32_t* cnt_all = nullptr;  // [Σ k] candidate counts, contiguous
+    std::vector<uint32_t> cnt_base;
+    std::vector<DevPtr> keep;     // uploaded job arrays
+    uint32_t nws = 0, rps = 0;
+    uint32_t* Bp(const QS& q, int u) const { return q.B + (size_t)u * nws; }
+    uint32_t* Xp(const QS& q, int s) const { return q.X + (size_t)s * nws; }
+    uint32_t* rpp(const QS& q, int u) const { return q.rp + (size_t)u * rps; }
+};
+
+size_t filter_bytes(const QS& q, uint32_t nws) {
+    size_t b = 0;
+    b += (size_t)q.k * nws * 4 + (size_t)std::max(q.E, 1) * nws * 4 + (size_t)q.k * (nws + 64) * 4;
+    uint32_t maxcap = 1;
+    for (int u = 0; u < q.k; u++) {
+        b += (size_t)q.cap[u] * 4 + 2 * ((size_t)q.cap[u] + 1) * 4 + 3 * kAlign;
+        maxcap = std::max(maxcap, q.cap[u]);
+    }
+    b += (size_t)maxcap * 8 + 8 * kAlign;
+    return b;
+}
+
+void carve_all(Chunk& ch, Carve& cv) {
+    const uint32_t nws = ch.nws, rps = ch.rps;
+    // X first (one memset), then counters (one D2H), then the rest
+    for (QS* q : ch.qs) q->X = cv.take<uint32_t>((size_t)std::max(q->E, 1) * nws);
+    size_t nc = 0;
+    ch.cnt_base.clear();
+    for (QS* q : ch.qs) {
+        ch.cnt_base.push_back((uint32_t)nc);
+        nc += (size_t)q->k;
+    }
+    ch.cnt_all = cv.take<uint32_t>(nc);
+    for (size_t i = 0; i < ch.qs.size(); i++) ch.qs[i]->cnt = ch.cnt_all + ch.cnt_base[i];
+    for (QS* q : ch.qs) {
+        q->B = cv.take<uint32_t>((size_t)q->k * nws);
+        q->rp = cv.take<uint32_t>((size_t)q->k * rps);
+        uint32_t maxcap = 1;
+        for (int u = 0; u < q->k; u++) {
+            q->carr[u] = cv.take<uint32_t>(q->cap[u]);
+            q->seg[u][0] = cv.take<uint32_t>((size_t)q->cap[u] + 1);
+            q->seg[u][1] = cv.take<uint32_t>((size_t)q->cap[u] + 1);
+            maxcap = std::max(maxcap, q->cap[u]);
+        }
+        q->mask = cv.take<unsigned long long>(maxcap);
+    }
+}
+
+// kernel_check + initialisation + refinement (stage 0 / 1 / 2).
+void filter_phase(Chunk& ch, int stage) {
+    gps_ctx* c = ch.c;
+    const DevGraph& d = ch.g->d;
+    std::vector<QDesc> qd;
+    uint32_t maxk = 0;
+    for (QS* q : ch.qs) {
+        QDesc x{};
+        x.k = q->k;
+        for (int u = 0; u < q->k; u++) {
+            x.lab[u] = q->plan.vlab[u];
+            x.bound[u] = q->plan.bound[u];
+            x.qout[u] = q->plan.qout[u];
+            x.qin[u] = q->plan.qin[u];
+        }
+        x.B = q->B;
+        qd.push_back(x);
+        maxk = std::max<uint32_t>(maxk, q->k);
+    }
+    run_check(c, d, upload(c, qd, ch.keep), (uint32_t)qd.size(), maxk);
+    if (stage < 1) return;
+    size_t S = 0;
+    for (QS* q : ch.qs) {
+        size_t s = q->plan.init_steps.size() + (stage >= 2 ? q->plan.refine_steps.size() : 0);
+        S = std::max(S, s);
+    }
+    for (size_t s = 0; s < S; s++) {
+        std::vector<CollectJob> cj;
+        std::vector<ExploreJob> ej, pj;
+        std::vector<Cons> cons;
+        std::vector<AndJob> aj;
+        std::vector<uint32_t*> xs;
+        for (QS* q : ch.qs) {
+            const Plan& p = q->plan;
+            const size_t ni = p.init_steps.size();
+            const size_t nr = stage >= 2 ? p.refine_steps.size() : 0;
+            if (s >= ni + nr) continue;
+            const FilterStep& st = s < ni ? p.init_steps[s] : p.refine_steps[s - ni];
+            const int u = st.u;
+            cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0], q->seg[u][1],
+                                    q->mask});
+            std::vector<Constraint> ord;
+            for (const Constraint& cs : st.cons)
+                if (cs.dir == 0) ord.push_back(cs);
+            const uint32_t no = (uint32_t)ord.size();
+            for (const Constraint& cs : st.cons)
+                if (cs.dir == 1) ord.push_back(cs);
+            if (ord.empty()) continue;
+            const uint32_t c0 = (uint32_t)cons.size();
+            for (size_t i = 0; i < ord.size(); i++)
+                cons.push_back(Cons{ch.Bp(*q, ord[i].v), st.propagate ? ch.Xp(*q, (int)i) : nullptr,
+                                    p.arcs[ord[i].arc].lab, ord[i].dir});
+            ExploreJob e{q->carr[u], q->cnt + u, q->seg[u][0], q->seg[u][1], q->mask, ch.Bp(*q, u),
+                         no, (uint32_t)ord.size() - no, c0, 0};
+            ej.push_back(e);
+            if (st.propagate) {
+                pj.push_back(e);
+                std::vector<int> targets;
+                for (const Constraint& cs : ord)
+                    if (std::find(targets.begin(), targets.end(), cs.v) == targets.end()) targets.push_back(cs.v);
+                for (int v : targets) {
+                    AndJob a{ch.Bp(*q, v), (uint32_t)xs.size(), 0};
+                    for (size_t i = 0; i < ord.size(); i++)
+                        if (ord[i].v == v) xs.push_back(ch.Xp(*q, (int)i));
+                    a.x1 = (uint32_t)xs.size();
+                    aj.push_back(a);
+                }
+            }
+        }
+        if (cj.empty()) continue;
+        run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
+        if (ej.empty()) continue;
+        const Cons* dcons = upload(c, cons, ch.keep);
+        run_prune(c, d, upload(c, ej, ch.keep), dcons, (uint32_t)ej.size());
+        if (!pj.empty()) {
+            run_propagate(c, d, upload(c, pj, ch.keep), dcons, (uint32_t)pj.size());
+            run_bitand(c, d, upload(c, aj, ch.keep), upload(c, xs, ch.keep), (uint32_t)aj.size());
+        }
+    }
+}
+
+void setup_chunk(Chunk& ch) {
+    gps_ctx* c = ch.c;
+    ch.nws = ch.g->d.nws;
+    ch.rps = ch.g->d.nws + 64;
+    Carve sz;
+    carve_all(ch, sz);
+    ch.arena = make_block(c, sz.off + kAlign);
+    Carve cv;
+    cv.base = static_cast<char*>(ch.arena->p);
+    carve_all(ch, cv);
+    size_t xbytes = 0;
+    for (QS* q : ch.qs) xbytes += (size_t)std::max(q->E, 1) * ch.nws * 4;
+    // X regions are carved first and back to back (modulo alignment): clear the whole span
+    const char* x0 = reinterpret_cast<const char*>(ch.qs.front()->X);
+    const char* x1 = reinterpret_cast<const char*>(ch.qs.back()->X) + (size_t)std::max(ch.qs.back()->E, 1) * ch.nws * 4;
+    GPS_CK(cudaMemsetAsync((void*)x0, 0, (size_t)(x1 - x0), c->stream));
+    (void)xbytes;
+}
+
+void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count_only, std::vector<QueryResult>& out) {
+    Chunk ch;
+    ch.c = c;
+    ch.g = g;
+    ch.qs = qsv;
+    const DevGraph& d = g->d;
+    setup_chunk(ch);
+    filter_phase(ch, 2);
+
+    // ---- final collect of every query vertex, sync #1 ----
+    {
+        std::vector<CollectJob> cj;
+        for (QS* q : ch.qs)
+            for (int u = 0; u < q->k; u++)
+                cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0],
+                                        q->seg[u][1], nullptr});
+        run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
+        size_t nc = cj.size(), got = 0;
+        uint32_t* h = static_cast<uint32_t*>(pinned_alloc(c, nc * 4, &got));
+        GPS_CK(cudaMemcpyAsync(h, ch.cnt_all, nc * 4, cudaMemcpyDeviceToHost, c->stream));
+        ctx_sync(c);
+        for (size_t i = 0; i < ch.qs.size(); i++) {
+            QS* q = ch.qs[i];
+            for (int u = 0; u < q->k; u++) q->C[u] = h[ch.cnt_base[i] + u];
+        }
+        pinned_release(c, h, got);
+    }
+    for (QS* q : ch.qs) {
+        QueryResult& r = out[q->idx];
+        r.cols = (uint32_t)q->k;
+        for (int u = 0; u < q->k; u++)
+            if (q->C[u] == 0) q->live = false;
+        if (!q->live) continue;
+        if (q->k == 1) {   // single-vertex query: the candidate set is the answer (reading R11)
+            r.rows = q->C[0];
+            if (!count_only) {
+                r.block = make_block(c, (size_t)r.rows * 4);
+                GPS_CK(cudaMemcpyAsync(r.block->p, q->carr[0], (size_t)r.rows * 4, cudaMemcpyDeviceToDevice,
+                                       c->stream));
+                r.data = static_cast<const uint32_t*>(r.block->p);
+            }
+            q->live = false;
+        }
+    }
+
+    // ---- collect_edge_candidates (both directions of every arc), sync #2 ----
+    std::vector<ECJob> ej;
+    std::vector<uint64_t> kc_off;
+    uint64_t kc_total = 0;
+    for (QS* q : ch.qs) {
+        if (!q->live) continue;
+        for (int e = 0; e < q->E; e++)
+            for (int dir = 0; dir < 2; dir++) {
+                const QArc& a = q->plan.arcs[e];
+                const int key = dir ? a.b : a.a, other = dir ? a.a : a.b;
+                q->ecjob[e][dir] = (int)ej.size();
+                ECJob j{};
+                j.keys = q->carr[key];
+                j.nkeys = q->cnt + key;
+                j.seg = q->seg[key][dir];
+                j.Bq = ch.Bp(*q, other);
+                j.lab = a.lab;
+                j.dir = (uint32_t)dir;
+                ej.push_back(j);
+                kc_off.push_back(kc_total);
+                kc_total += (uint64_t)q->C[key] + 1;
+            }
+    }
+    if (ej.empty()) return;
+    if (ej.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: EC job list too long");
+    const uint32_t nj = (uint32_t)ej.size();
+    const uint32_t G = (uint32_t)c->nsm * 4;
+    DevPtr kcnt(c, sizeof(uint32_t) * (kc_total + 1));
+    DevPtr ecoff(c, sizeof(uint32_t) * (kc_total + 2));
+    DevPtr jtot(c, sizeof(unsigned long long) * nj);
+    DevPtr blk(c, sizeof(uint64_t) * (G + 1));
+    GPS_CK(cudaMemsetAsync(kcnt.p, 0, sizeof(uint32_t) * (kc_total + 1), c->stream));
+    GPS_CK(cudaMemsetAsync(jtot.p, 0, sizeof(unsigned long long) * nj, c->stream));
+    for (uint32_t j = 0; j < nj; j++) {
+        ej[j].kcnt = kcnt.as<uint32_t>() + kc_off[j];
+        ej[j].total = jtot.as<unsigned long long>() + j;
+    }
+    const ECJob* dej = upload(c, ej, ch.keep);
+    PassCtl ctl{blk.as<uint64_t>(), c->d_done + 1, c->d_info};
+    run_ec(c, d, dej, nj, false, ctl, nullptr, G);
+    scan_exclusive1<uint32_t, uint32_t>(c, kcnt.as<uint32_t>(), ecoff.as<uint32_t>(), kc_total);
+    uint64_t ec_values = 0;
+    std::vector<uint64_t> ectot(nj);
+    {
+        size_t got = 0;
+        uint64_t* h = static_cast<uint64_t*>(pinned_alloc(c, (nj + 2) * 8, &got));
+        GPS_CK(cudaMemcpyAsync(h, jtot.p, nj * 8, cudaMemcpyDeviceToHost, c->stream));
+        GPS_CK(cudaMemcpyAsync(h + nj, c->d_info, 16, cudaMemcpyDeviceToHost, c->stream));
+        ctx_sync(c);
+        for (uint32_t j = 0; j < nj; j++) ectot[j] = h[j];
+        ec_values = h[nj + 1];
+        pinned_release(c, h, got);
+    }
+    if (ec_values >= (1ull << 32)) fail(GPS_EOVERFLOW, "more than 2^32 candidate edges in one batch");
+    for (QS* q : ch.qs) {
+        if (!q->live) continue;
+        std::vector<uint64_t> cnts(q->E);
+        for (int e = 0; e < q->E; e++) {
+            cnts[e] = ectot[q->ecjob[e][0]];
+            if (cnts[e] == 0) q->live = false;   // an edge with no candidate edge: no match
+        }
+        if (!q->live) continue;
+        q->steps = make_join_order(q->plan, cnts);
+    }
+    DevPtr val(c, sizeof(uint32_t) * (ec_values + 1));
+    run_ec(c, d, dej, nj, true, ctl, val.as<uint32_t>(), G);
+    c->stats.k_bytes[GPS_K_EC_WRITE] += 4.0 * (double)ec_values;
+    auto ec_off_of = [&](int job) { return ecoff.as<uint32_t>() + kc_off[job]; };
+
+    // ---- combine_edge_candidates: one join step for all queries at a time ----
+    for (QS* q : ch.qs) {
+        if (!q->live) continue;
+        for (int u = 0; u < GPS_MAX_QV; u++) q->col_of[u] = -1;
+        const JoinStepPlan& s0 = q->steps[0];
+        q->col_of[s0.key] = 0;
+        q->vert_of_col[0] = (uint8_t)s0.key;
+        q->M = q->carr[s0.key];
+        q->R = q->C[s0.key];
+    }
+    Block cur;   // holds the previous step's output while its rows are read
+    for (size_t s = 0;; s++) {
+        std::vector<QS*> act;
+        for (QS* q : ch.qs)
+            if (q->live && q->steps.size() > s) act.push_back(q);
+        if (act.empty()) break;
+        const uint32_t w = (uint32_t)s + 1;
+        std::vector<JoinJob> jj;
+        std::vector<CloseChk> cl;
+        uint64_t R = 0;
+        DevPtr jt(c, sizeof(unsigned long long) * act.size());
+        GPS_CK(cudaMemsetAsync(jt.p, 0, sizeof(unsigned long long) * act.size(), c->stream));
+        for (size_t i = 0; i < act.size(); i++) {
+            QS* q = act[i];
+            const JoinStepPlan& st = q->steps[s];
+            JoinJob j{};
+            j.row0 = R;
+            j.M = q->M;
+            j.Bx = ch.Bp(*q, st.key);
+            j.rpx = ch.rpp(*q, st.key);
+            j.ec_off = ec_off_of(q->ecjob[st.arc][st.key_dir]);
+            j.total = jt.as<unsigned long long>() + i;
+            j.x_col = (uint32_t)q->col_of[st.key];
+            j.close0 = (uint32_t)cl.size();
+            for (int ci : st.closing) {
+                const QArc& a = q->plan.arcs[ci];   // closing arcs use their source-keyed table
+                CloseChk x{};
+                x.key_new = a.a == st.nv;
+                x.key_col = x.key_new ? 0u : (uint32_t)q->col_of[a.a];
+                x.tgt_new = a.b == st.nv;
+                x.tgt_col = x.tgt_new ? 0u : (uint32_t)q->col_of[a.b];
+                x.Bk = ch.Bp(*q, a.a);
+                x.rpk = ch.rpp(*q, a.a);
+                x.off = ec_off_of(q->ecjob[ci][0]);
+                cl.push_back(x);
+            }
+            j.nclose = (uint32_t)st.closing.size();
+            const bool last = s + 1 == q->steps.size();
+            j.final_ = last ? 1u : 0u;
+            j.nowrite = (last && count_only) ? 1u : 0u;
+            if (last) {
+                for (uint32_t col = 0; col < w; col++) j.perm[col] = q->vert_of_col[col];
+                j.perm[w] = (uint8_t)st.nv;
+            }
+            jj.push_back(j);
+            R += q->R;
+        }
+        if (jj.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: join job list too long");
+        DevPtr s0(c, sizeof(uint32_t) * (R + 1));
+        DevPtr poff(c, sizeof(uint64_t) * (R + 1));
+        JoinStep js{};
+        js.w = w;
+        js.wout = w + 1;
+        js.R = R;
+        js.jobs = upload(c, jj, ch.keep);
+        js.nj = (uint32_t)jj.size();
+        js.cl = cl.empty() ? nullptr : upload(c, cl, ch.keep);
+        js.ec_val = val.as<uint32_t>();
+        js.s0 = s0.as<uint32_t>();
+        js.poff = poff.as<uint64_t>();
+        js.ctl = PassCtl{blk.as<uint64_t>(), c->d_done, c->d_info};
+        run_join_seg(c, js);
+        run_join_count(c, js, G);
+        std::vector<uint64_t> tot(act.size());
+        uint64_t P = 0, writes = 0;
+        {
+            size_t got = 0;
+            uint64_t* h = static_cast<uint64_t*>(pinned_alloc(c, (act.size() + 2) * 8, &got));
+            GPS_CK(cudaMemcpyAsync(h, jt.p, act.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+            GPS_CK(cudaMemcpyAsync(h + act.size(), c->d_info, 16, cudaMemcpyDeviceToHost, c->stream));
+            ctx_sync(c);
+            for (size_t i = 0; i < act.size(); i++) tot[i] = h[i];
+            P = h[act.size()];
+            writes = h[act.size() + 1];
+            pinned_release(c, h, got);
+        }
+        c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)P;
+        Block ob;
+        if (writes) {
+            if (writes > (~0ull) / (4ull * (w + 1))) fail(GPS_EOVERFLOW, "result size overflows");
+            ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
+            js.out = static_cast<uint32_t*>(ob->p);
+            run_join_write(c, js, G);
+            c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)P + 4.0 * (w + 1) * (double)writes;
+        }
+        uint64_t off = 0;
+        for (size_t i = 0; i < act.size(); i++) {
+            QS* q = act[i];
+            const JoinStepPlan& st = q->steps[s];
+            QueryResult& r = out[q->idx];
+            const uint64_t t = tot[i];
+            const bool last = s + 1 == q->steps.size();
+            const bool wrote = !(last && count_only);
+            if (last) {
+                r.rows = t;
+                if (wrote && t) {
+                    r.block = ob;
+                    r.data = static_cast<const uint32_t*>(ob->p) + off * (w + 1);
+                }
+                q->live = false;
+            } else if (t == 0) {
+                r.rows = 0;
+                q->live = false;
+            } else {
+                q->M = static_cast<const uint32_t*>(ob->p) + off * (w + 1);
+                q->R = t;
+                q->col_of[st.nv] = (int)w;
+                q->vert_of_col[w] = (uint8_t)st.nv;
+            }
+            if (wrote) off += t;
+        }
+        cur = ob;   // the previous output block is released once no query reads it
+    }
+}
+
+}  // namespace
+
+void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t nq, const gps_match_opts& o,
+                 bool count_only, std::vector<QueryResult>& out) {
+    out.assign(nq, QueryResult{});
+    std::vector<QS> all(nq);
+    std::vector<QS*> todo;
+    const uint32_t n = g->d.n;
+    for (uint32_t i = 0; i < nq; i++) {
+        QS& q = all[i];
+        q.idx = i;
+        out[i].cols = qs[i].n_vertices;
+        try {
+            q.plan = make_plan(&qs[i], n, g->undirected, g->lab_hist, o);
+        } catch (const Error& e) {
+            out[i].status = e.status;
+            out[i].error = e.msg;
+            continue;
+        }
+        q.k = q.plan.k;
+        q.E = (int)q.plan.arcs.size();
+        if (q.plan.empty) continue;   // a label no data vertex carries: no candidates
+        for (int u = 0; u < q.k; u++) q.cap[u] = (uint32_t)std::min<uint64_t>(n, q.plan.freq[u]);
+        todo.push_back(&q);
+    }
+    // chunk: bounded queries, EC jobs and filter-arena bytes per chunk
+    size_t i = 0;
+    while (i < todo.size()) {
+        std::vector<QS*> chunk;
+        size_t bytes = 0, ecj = 0, vtx = 0;
+        while (i < todo.size()) {
+            QS* q = todo[i];
+            size_t b = filter_bytes(*q, g->d.nws);
+            if (!chunk.empty() && (chunk.size() >= kMaxBatch || bytes + b > kChunkBytes ||
+                                   ecj + 2 * (size_t)q->E > kMaxJobsPerLaunch || vtx + q->k > kMaxJobsPerLaunch))
+                break;
+            chunk.push_back(q);
+            bytes += b;
+            ecj += 2 * (size_t)q->E;
+            vtx += (size_t)q->k;
+            i++;
+        }
+        run_chunk(c, g, chunk, count_only, out);
+    }
+    for (uint32_t j = 0; j < nq; j++)
+        if (out[j].status == GPS_OK) {
+            c->stats.queries++;
+            c->stats.embeddings += out[j].rows;
+        }
+}
+
+void run_filter_debug(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts& o, int stage,
+                      uint32_t* host_bitmaps) {
+    QS one;
+    one.plan = make_plan(q, g->d.n, g->undirected, g->lab_hist, o);
+    one.k = one.plan.k;
+    one.E = (int)one.plan.arcs.size();
+    for (int u = 0; u < one.k; u++) one.cap[u] = (uint32_t)std::min<uint64_t>(g->d.n, std::max<uint64_t>(1, one.plan.freq[u]));
+    Chunk ch;
+    ch.c = c;
+    ch.g = g;
+    ch.qs = {&one};
+    setup_chunk(ch);
+    filter_phase(ch, stage);
+    GPS_CK(cudaMemcpy2DAsync(host_bitmaps, sizeof(uint32_t) * g->d.nw, one.B, sizeof(uint32_t) * ch.nws,
+                             sizeof(uint32_t) * g->d.nw, one.k, cudaMemcpyDeviceToHost, c->stream));
+    ctx_sync(c);
+}
+
+}  // namespace gps

@@ -70,7 +70,7 @@ void scan_exclusive(gps_ctx* c, const ScanBatch<TI, TO>& b) {
     uint64_t nt = (maxn + kScanTile - 1) / kScanTile;
     if (nt == 0) nt = 1;
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "scan too large");
-    LbScratch lb = lb_scratch(c, (uint32_t)nt);
+    LbScratch lb = lb_scratch(c, (uint32_t)b.nseg, (uint32_t)nt);
     launch(c, GPS_K_SCAN, dim3((uint32_t)nt, b.nseg), dim3(kScanThreads), 0, k_scan<TI, TO>, b, lb,
            lb_next_epoch(c));
 }

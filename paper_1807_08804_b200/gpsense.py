@@ -100,6 +100,7 @@ def _load_lib():
         "gps_match_batch": (S, [P, P, P, ctypes.c_uint32, P, P, P]),
         "gps_count_batch": (S, [P, P, P, ctypes.c_uint32, P, P, P]),
         "gps_set_workers": (S, [P, ctypes.c_uint32]),
+        "gps_set_slice": (S, [P, ctypes.c_uint32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -113,7 +114,7 @@ EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_grap
             "gps_graph_info", "gps_match", "gps_match_host", "gps_count", "gps_result_info",
             "gps_result_free", "gps_last_error", "gps_get_stats", "gps_reset_stats",
             "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates", "gps_match_batch",
-            "gps_count_batch", "gps_set_workers"]
+            "gps_count_batch", "gps_set_workers", "gps_set_slice"]
 
 
 def _check(st: int):
@@ -205,6 +206,9 @@ class Context:
 
     def set_workers(self, n: int):
         _check(lib.gps_set_workers(self._h, int(n)))
+
+    def set_slice(self, n: int):
+        _check(lib.gps_set_slice(self._h, int(n)))
 
     def close(self):
         if self._h:
