@@ -136,7 +136,13 @@ void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32
 // -------------------------------------------------------------- a4 explore
 constexpr int kET = 256;
 constexpr int kEI = 4;
-constexpr int kEW = 1024;
+constexpr int kEW = 512;
+
+struct ExMeta {             // one candidate row of an explore job, staged per chunk
+    uint32_t row, key;
+    uint32_t bo, dout;      // out-adjacency base / length of the candidate
+    uint32_t bi, din;       // in-adjacency base / length
+};
 
 template <int MODE>   // 0: prune (mark satisfied constraints), 1: propagate
 __global__ void __launch_bounds__(kET) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs,
@@ -144,6 +150,7 @@ __global__ void __launch_bounds__(kET) k_explore(DevGraph g, const ExploreJob* _
                                                  unsigned long long* bytes_acc) {
     extern __shared__ uint64_t s_jp[];      // [nj+1] job pair prefix
     __shared__ uint64_t s_off[kEW + 1];
+    __shared__ ExMeta s_meta[kEW];
     __shared__ uint64_t s_row;
     job_prefix(nj, [&](uint32_t j) -> uint64_t {
         const ExploreJob& J = jobs[j];
@@ -158,44 +165,63 @@ __global__ void __launch_bounds__(kET) k_explore(DevGraph g, const ExploreJob* _
         const uint64_t no = J.no, ni = J.ni;
         const int nc = (int)(J.no + J.ni);
         const unsigned long long full = nc >= 64 ? ~0ull : ((1ull << nc) - 1ull);
+        const Cons* jc = cons + J.c0;
         auto offs = [&](uint64_t i) -> uint64_t {
             return no * __ldg(J.seg_out + i) + ni * __ldg(J.seg_in + i);
         };
-        for_pairs<kET, kEI, kEW>(lo, hi, (uint64_t)C, offs, s_off, &s_row,
-                                 [&](bool v, uint64_t p, uint64_t row, uint64_t j) {
-            unsigned long long bits = 0;
-            bool fits = false;
-            uint32_t ci = 0;
-            uint32_t d = 0;
-            if (v) {
-                const uint32_t key = __ldg(J.cands + row);
-                const uint32_t dout = __ldg(J.seg_out + row + 1) - __ldg(J.seg_out + row);
-                const uint32_t din = __ldg(J.seg_in + row + 1) - __ldg(J.seg_in + row);
-                uint32_t arc;
-                if (j < no * dout) {
-                    ci = (uint32_t)(j / dout);
-                    arc = __ldg(g.arc_out + __ldg(g.off_out + key) + (uint32_t)(j % dout));
-                } else {
-                    const uint64_t jj2 = j - no * dout;
-                    ci = J.no + (uint32_t)(jj2 / din);
-                    arc = __ldg(g.arc_in + __ldg(g.off_in + key) + (uint32_t)(jj2 % din));
+        auto load = [&](uint64_t r) -> ExMeta {
+            ExMeta m;
+            m.row = (uint32_t)r;
+            m.key = __ldg(J.cands + r);
+            m.dout = __ldg(J.seg_out + r + 1) - __ldg(J.seg_out + r);
+            m.din = __ldg(J.seg_in + r + 1) - __ldg(J.seg_in + r);
+            m.bo = __ldg(g.off_out + m.key);
+            m.bi = __ldg(g.off_in + m.key);
+            return m;
+        };
+        pair_chunks<ExMeta, kET, kEI, kEW>(lo, hi, (uint64_t)C, offs, load, s_meta, s_off, &s_row,
+                                           [&](const bool (&v)[kEI], const ExMeta (&m)[kEI], const uint64_t (&j)[kEI]) {
+            uint32_t arc[kEI], ci[kEI];
+#pragma unroll
+            for (int it = 0; it < kEI; it++) {
+                arc[it] = 0;
+                ci[it] = 0;
+                if (v[it]) {
+                    const uint64_t nout = no * m[it].dout;
+                    if (j[it] < nout) {
+                        ci[it] = (uint32_t)(j[it] / m[it].dout);
+                        arc[it] = __ldg(g.arc_out + m[it].bo + (uint32_t)(j[it] - (uint64_t)ci[it] * m[it].dout));
+                    } else {
+                        const uint64_t jj2 = j[it] - nout;
+                        const uint32_t cin = (uint32_t)(jj2 / m[it].din);
+                        ci[it] = J.no + cin;
+                        arc[it] = __ldg(g.arc_in + m[it].bi + (uint32_t)(jj2 - (uint64_t)cin * m[it].din));
+                    }
                 }
-                const Cons& cs = cons[J.c0 + ci];
-                d = arc >> g.lbits;
-                fits = lab_ok(arc, g.lmask, cs.lab) && d != key && bit_test(cs.Bv, d);
-                if (MODE == 1) fits = fits && __ldg(J.mask + row) == full;
-                bits = fits ? (1ull << ci) : 0ull;
             }
-            if (MODE == 0) {
-                uint32_t peers;
-                const uint32_t leader = warp_group_leader(v ? (uint32_t)row : 0xffffffffu, peers);
-                const uint32_t lo32 = __reduce_or_sync(peers, (uint32_t)bits);
-                const uint32_t hi32 = __reduce_or_sync(peers, (uint32_t)(bits >> 32));
-                const unsigned long long agg = ((unsigned long long)hi32 << 32) | lo32;
-                if (v && lane_id() == leader && agg && (__ldcg(J.mask + row) & agg) != agg)
-                    atomicOr(J.mask + row, agg);
-            } else {
-                if (fits) atomicOr(cons[J.c0 + ci].X + (d >> 5), 1u << (d & 31));
+            bool fits[kEI];
+#pragma unroll
+            for (int it = 0; it < kEI; it++) {
+                const uint32_t d = arc[it] >> g.lbits;
+                fits[it] = v[it] && lab_ok(arc[it], g.lmask, jc[ci[it]].lab) && d != m[it].key &&
+                           bit_test(jc[ci[it]].Bv, d);
+                if (MODE == 1) fits[it] = fits[it] && __ldg(J.mask + m[it].row) == full;
+            }
+#pragma unroll
+            for (int it = 0; it < kEI; it++) {
+                if (MODE == 0) {
+                    const unsigned long long bits = fits[it] ? (1ull << ci[it]) : 0ull;
+                    uint32_t peers;
+                    const uint32_t leader = warp_group_leader(v[it] ? m[it].row : 0xffffffffu, peers);
+                    const uint32_t lo32 = __reduce_or_sync(peers, (uint32_t)bits);
+                    const uint32_t hi32 = __reduce_or_sync(peers, (uint32_t)(bits >> 32));
+                    const unsigned long long agg = ((unsigned long long)hi32 << 32) | lo32;
+                    if (v[it] && lane_id() == leader && agg && (__ldcg(J.mask + m[it].row) & agg) != agg)
+                        atomicOr(J.mask + m[it].row, agg);
+                } else if (fits[it]) {
+                    const uint32_t d = arc[it] >> g.lbits;
+                    atomicOr(jc[ci[it]].X + (d >> 5), 1u << (d & 31));
+                }
             }
         });
     });
@@ -220,7 +246,7 @@ static size_t jp_smem(uint32_t nj) { return sizeof(uint64_t) * (nj + 1); }
 void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, const Cons* d_cons, uint32_t nj) {
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
-    const uint32_t G = (uint32_t)c->nsm * 4;
+    const uint32_t G = (uint32_t)c->nsm * 6;
     launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), jp_smem(nj), k_explore<0>, g, d_jobs, d_cons, nj,
            c->d_bytes + GPS_K_EXPLORE);
     launch(c, GPS_K_EXPLORE, dim3(std::max<uint32_t>(1, (uint32_t)c->nsm * 2 / nj + 1), nj), dim3(256), 0, k_clear,
@@ -230,7 +256,7 @@ void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, const Co
 void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, const Cons* d_cons, uint32_t nj) {
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
-    const uint32_t G = (uint32_t)c->nsm * 4;
+    const uint32_t G = (uint32_t)c->nsm * 6;
     launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), jp_smem(nj), k_explore<1>, g, d_jobs, d_cons, nj,
            c->d_bytes + GPS_K_EXPLORE);
 }

@@ -28,11 +28,16 @@ constexpr int kPW = 1024;   // rows of offsets staged in shared memory
 static size_t jp_smem(uint32_t nj) { return sizeof(uint64_t) * (nj + 1); }
 
 // ------------------------------------------------------------ a6 EC build
+struct EcMeta {             // one key row of an EC job
+    uint32_t row, key, base, pad;
+};
+
 template <bool WRITE>
 __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict__ jobs, uint32_t nj, PassCtl ctl,
                                            uint32_t* __restrict__ val, unsigned long long* bytes_acc) {
     extern __shared__ uint64_t s_jp[];
     __shared__ uint64_t s_off[kPW + 1];
+    __shared__ EcMeta s_meta[kPW];
     __shared__ uint64_t s_row;
     job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].nkeys); }, s_jp);
     const uint64_t P = s_jp[nj];
@@ -45,37 +50,49 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
         const uint32_t* off = J.dir ? g.off_in : g.off_out;
         const uint32_t* arcs = J.dir ? g.arc_in : g.arc_out;
         auto offs = [&](uint64_t i) -> uint64_t { return (uint64_t)__ldg(J.seg + i); };
+        auto load = [&](uint64_t r) -> EcMeta {
+            EcMeta m;
+            m.row = (uint32_t)r;
+            m.key = __ldg(J.keys + r);
+            m.base = __ldg(off + m.key);
+            m.pad = 0;
+            return m;
+        };
         uint32_t jcount = 0;
-        for_pairs<kPT, kPI, kPW>(lo, hi, (uint64_t)*J.nkeys, offs, s_off, &s_row,
-                                 [&](bool v, uint64_t p, uint64_t row, uint64_t j) {
-            bool pred = false;
-            uint32_t d = 0;
-            if (v) {
-                const uint32_t key = __ldg(J.keys + row);
-                const uint32_t base = __ldg(off + key);
-                const uint32_t x = __ldg(arcs + base + j);
-                d = x >> g.lbits;
-                if (lab_ok(x, g.lmask, J.lab) && d != key && bit_test(J.Bq, d)) {
-                    bool dup = false;   // parallel arcs to the same v' (reading R5): count v' once
-                    if (j > 0) {
-                        const uint32_t xp = __ldg(arcs + base + j - 1);
-                        dup = (xp >> g.lbits) == d && lab_ok(xp, g.lmask, J.lab);
-                    }
-                    pred = !dup;
+        pair_chunks<EcMeta, kPT, kPI, kPW>(lo, hi, (uint64_t)*J.nkeys, offs, load, s_meta, s_off, &s_row,
+                                           [&](const bool (&v)[kPI], const EcMeta (&m)[kPI], const uint64_t (&j)[kPI]) {
+            uint32_t x[kPI], xp[kPI];
+#pragma unroll
+            for (int it = 0; it < kPI; it++) {
+                x[it] = v[it] ? __ldg(arcs + m[it].base + j[it]) : 0u;
+                xp[it] = (v[it] && j[it] > 0) ? __ldg(arcs + m[it].base + j[it] - 1) : 0xffffffffu;
+            }
+            bool pred[kPI];
+#pragma unroll
+            for (int it = 0; it < kPI; it++) {
+                const uint32_t d = x[it] >> g.lbits;
+                pred[it] = false;
+                if (v[it] && lab_ok(x[it], g.lmask, J.lab) && d != m[it].key && bit_test(J.Bq, d)) {
+                    // parallel arcs to the same v' (reading R5): count v' once
+                    const bool dup = j[it] > 0 && (xp[it] >> g.lbits) == d && lab_ok(xp[it], g.lmask, J.lab);
+                    pred[it] = !dup;
                 }
             }
-            if (!WRITE) {
-                uint32_t peers;
-                const uint32_t leader = warp_group_leader(v ? (uint32_t)row : 0xffffffffu, peers);
-                const uint32_t nvalid = __popc(__ballot_sync(kFull, pred) & peers);
-                if (v && lane_id() == leader && nvalid) atomicAdd(J.kcnt + row, nvalid);
-                count += pred ? 1 : 0;
-                jcount += pred ? 1 : 0;
-            } else {
-                uint32_t tot;
-                const uint32_t rank = block_excl_scan((uint32_t)pred, &tot);
-                if (pred) val[running + rank] = d;
-                running += tot;
+#pragma unroll
+            for (int it = 0; it < kPI; it++) {
+                if (!WRITE) {
+                    uint32_t peers;
+                    const uint32_t leader = warp_group_leader(v[it] ? m[it].row : 0xffffffffu, peers);
+                    const uint32_t nvalid = __popc(__ballot_sync(kFull, pred[it]) & peers);
+                    if (v[it] && lane_id() == leader && nvalid) atomicAdd(J.kcnt + m[it].row, nvalid);
+                    count += pred[it] ? 1 : 0;
+                    jcount += pred[it] ? 1 : 0;
+                } else {
+                    uint32_t tot;
+                    const uint32_t rank = block_excl_scan((uint32_t)pred[it], &tot);
+                    if (pred[it]) val[running + rank] = x[it] >> g.lbits;
+                    running += tot;
+                }
             }
         });
         if (!WRITE) {
@@ -186,53 +203,77 @@ __device__ __forceinline__ bool pair_ok(const JoinStep& a, const JoinJob& J, con
     return true;
 }
 
+struct JMeta {              // one input row of a join step
+    const uint32_t* rowp;   // its w values
+    uint32_t s0;            // start of its EC segment in ec_val
+    uint32_t job;
+};
+
 template <bool WRITE>
 __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a) {
     extern __shared__ uint64_t s_jr[];   // [nj+1] first row of every job
     __shared__ uint64_t s_off[kPW + 1];
+    __shared__ JMeta s_meta[kPW];
     __shared__ uint64_t s_row;
     for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
     if (threadIdx.x == 0) s_jr[a.nj] = a.R;
     __syncthreads();
     auto offs = [&](uint64_t i) -> uint64_t { return __ldg(a.poff + i); };
+    auto load = [&](uint64_t r) -> JMeta {
+        JMeta m;
+        m.job = pairs_find_smem(s_jr, a.nj, r);
+        const JoinJob& J = a.jobs[m.job];
+        m.rowp = J.M + (r - J.row0) * a.w;
+        m.s0 = __ldg(a.s0 + r);
+        return m;
+    };
     const uint64_t P = offs(a.R);
     uint64_t p0, p1;
     pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
     uint64_t running = WRITE ? a.ctl.blk[blockIdx.x] : 0ull;
     uint64_t count = 0;
-    for_pairs<kPT, kPI, kPW>(p0, p1, a.R, offs, s_off, &s_row, [&](bool v, uint64_t p, uint64_t r, uint64_t jpos) {
-        bool valid = false, writes = false;
-        uint32_t cand = 0, job = 0xffffffffu;
-        const uint32_t* row = nullptr;
-        if (v) {
-            job = pairs_find_smem(s_jr, a.nj, r);
-            const JoinJob& J = a.jobs[job];
-            row = J.M + (r - J.row0) * a.w;
-            cand = __ldg(a.ec_val + __ldg(a.s0 + r) + jpos);
-            valid = pair_ok(a, J, row, cand);
-            writes = valid && !J.nowrite;
-        }
-        if (WRITE) {
-            uint32_t tot;
-            const uint32_t rank = block_excl_scan((uint32_t)writes, &tot);
-            if (writes) {
-                const JoinJob& J = a.jobs[job];
-                uint32_t* dst = a.out + (running + rank) * a.wout;
-                if (J.final_) {
-                    for (uint32_t c = 0; c < a.w; c++) dst[J.perm[c]] = __ldg(row + c);
-                    dst[J.perm[a.w]] = cand;
-                } else {
-                    for (uint32_t c = 0; c < a.w; c++) dst[c] = __ldg(row + c);
-                    dst[a.w] = cand;
-                }
+    pair_chunks<JMeta, kPT, kPI, kPW>(p0, p1, a.R, offs, load, s_meta, s_off, &s_row,
+                                      [&](const bool (&v)[kPI], const JMeta (&m)[kPI], const uint64_t (&j)[kPI]) {
+        uint32_t cand[kPI];
+#pragma unroll
+        for (int it = 0; it < kPI; it++) cand[it] = v[it] ? __ldg(a.ec_val + m[it].s0 + j[it]) : 0u;
+        bool valid[kPI], writes[kPI];
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            valid[it] = false;
+            writes[it] = false;
+            if (v[it]) {
+                const JoinJob& J = a.jobs[m[it].job];
+                valid[it] = pair_ok(a, J, m[it].rowp, cand[it]);
+                writes[it] = valid[it] && !J.nowrite;
             }
-            running += tot;
-        } else {
-            uint32_t peers;
-            const uint32_t leader = warp_group_leader(job, peers);
-            const uint32_t nvalid = __popc(__ballot_sync(kFull, valid) & peers);
-            if (v && lane_id() == leader && nvalid) atomicAdd(a.jobs[job].total, (unsigned long long)nvalid);
-            count += writes ? 1 : 0;
+        }
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            if (WRITE) {
+                uint32_t tot;
+                const uint32_t rank = block_excl_scan((uint32_t)writes[it], &tot);
+                if (writes[it]) {
+                    const JoinJob& J = a.jobs[m[it].job];
+                    const uint32_t* row = m[it].rowp;
+                    uint32_t* dst = a.out + (running + rank) * a.wout;
+                    if (J.final_) {
+                        for (uint32_t c = 0; c < a.w; c++) dst[J.perm[c]] = __ldg(row + c);
+                        dst[J.perm[a.w]] = cand[it];
+                    } else {
+                        for (uint32_t c = 0; c < a.w; c++) dst[c] = __ldg(row + c);
+                        dst[a.w] = cand[it];
+                    }
+                }
+                running += tot;
+            } else {
+                uint32_t peers;
+                const uint32_t leader = warp_group_leader(v[it] ? m[it].job : 0xffffffffu, peers);
+                const uint32_t nvalid = __popc(__ballot_sync(kFull, valid[it]) & peers);
+                if (v[it] && lane_id() == leader && nvalid)
+                    atomicAdd(a.jobs[m[it].job].total, (unsigned long long)nvalid);
+                count += writes[it] ? 1 : 0;
+            }
         }
     });
     if (!WRITE) last_block_scan(a.ctl.blk, gridDim.x, a.ctl.done, a.ctl.info, P, count);

@@ -20,7 +20,7 @@ struct LbScratch {
 LbScratch lb_scratch(gps_ctx* c, uint32_t slots, uint32_t tiles_needed);
 uint32_t lb_next_epoch(gps_ctx* c);
 
-constexpr uint32_t kMaxJobsPerLaunch = 4096;   // job prefix staged in shared memory
+constexpr uint32_t kMaxJobsPerLaunch = 2048;   // job prefix staged in shared memory
 
 // ---- a2 kernel_check (Def. 3; Alg. 2 line 7 P:723) -------------------
 struct QDesc {

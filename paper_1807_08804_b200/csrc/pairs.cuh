@@ -165,3 +165,66 @@ __device__ __forceinline__ void for_job_ranges(const uint64_t* s_jp, uint32_t nj
 }
 
 }  // namespace gps
+
+namespace gps {
+
+// Chunked pair iteration with per-row metadata staged in shared memory.
+//
+// Per chunk of T*IPT consecutive pairs: the offsets of a window of W rows are
+// staged (coalesced), then load_meta(row) -> Meta is evaluated ONCE per row that
+// meets the chunk (in parallel) and kept in s_meta, so a pair costs a
+// shared-memory binary search + shared-memory metadata instead of a chain of
+// dependent global loads.  body(v[], m[], j[]) receives all IPT items of the
+// thread at once (so it can issue their global loads back to back); rows
+// outside the window (runs of empty rows) fall back to load_meta from global.
+// body may use block-wide barriers (called uniformly).
+template <typename Meta, int T, int IPT, int W, typename OffF, typename LoadMeta, typename Body>
+__device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t nrows, OffF offs, LoadMeta load_meta,
+                                            Meta* s_meta, uint64_t* s_off, uint64_t* s_row, Body&& body) {
+    if (p0 >= p1) return;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) *s_row = pairs_find_global(offs, 0, nrows, p0);
+    __syncthreads();
+    uint64_t r0 = *s_row;
+    for (uint64_t cp = p0; cp < p1; cp += (uint64_t)T * IPT) {
+        const uint64_t cend = cp + (uint64_t)T * IPT < p1 ? cp + (uint64_t)T * IPT : p1;
+        const uint32_t wn = (uint32_t)((nrows - r0) < (uint64_t)W ? (nrows - r0) : (uint64_t)W);
+        for (uint32_t i = tid; i <= wn; i += T) s_off[i] = offs(r0 + i);
+        __syncthreads();
+        const uint64_t wend = s_off[wn];
+        for (uint32_t i = tid; i < wn; i += T)
+            if (s_off[i] < cend && s_off[i + 1] > s_off[i]) s_meta[i] = load_meta(r0 + i);
+        __syncthreads();
+        bool v[IPT];
+        Meta m[IPT];
+        uint64_t j[IPT];
+#pragma unroll
+        for (int it = 0; it < IPT; it++) {
+            const uint64_t p = cp + (uint64_t)it * T + tid;
+            v[it] = p < cend;
+            j[it] = 0;
+            if (v[it]) {
+                if (p < wend) {
+                    const uint32_t i = pairs_find_smem(s_off, wn, p);
+                    m[it] = s_meta[i];
+                    j[it] = p - s_off[i];
+                } else {
+                    const uint64_t row = pairs_find_global(offs, r0 + wn, nrows, p);
+                    m[it] = load_meta(row);
+                    j[it] = p - offs(row);
+                }
+            }
+        }
+        body(v, m, j);
+        __syncthreads();
+        if (cend < p1) {
+            if (tid == 0)
+                *s_row = (cend < wend) ? r0 + pairs_find_smem(s_off, wn, cend)
+                                       : pairs_find_global(offs, r0 + wn, nrows, cend);
+            __syncthreads();
+            r0 = *s_row;
+        }
+    }
+}
+
+}  // namespace gps
