@@ -187,15 +187,16 @@ __global__ void __launch_bounds__(kET) k_explore(DevGraph g, const ExploreJob* _
                 arc[it] = 0;
                 ci[it] = 0;
                 if (v[it]) {
-                    const uint64_t nout = no * m[it].dout;
-                    if (j[it] < nout) {
-                        ci[it] = (uint32_t)(j[it] / m[it].dout);
-                        arc[it] = __ldg(g.arc_out + m[it].bo + (uint32_t)(j[it] - (uint64_t)ci[it] * m[it].dout));
+                    const uint32_t jj32 = (uint32_t)j[it];        // < (no + ni) * degree < 2^32
+                    const uint32_t nout = J.no * m[it].dout;
+                    if (jj32 < nout) {
+                        ci[it] = jj32 / m[it].dout;
+                        arc[it] = __ldg(g.arc_out + m[it].bo + (jj32 - ci[it] * m[it].dout));
                     } else {
-                        const uint64_t jj2 = j[it] - nout;
-                        const uint32_t cin = (uint32_t)(jj2 / m[it].din);
+                        const uint32_t r = jj32 - nout;
+                        const uint32_t cin = r / m[it].din;
                         ci[it] = J.no + cin;
-                        arc[it] = __ldg(g.arc_in + m[it].bi + (uint32_t)(jj2 - (uint64_t)cin * m[it].din));
+                        arc[it] = __ldg(g.arc_in + m[it].bi + (r - cin * m[it].din));
                     }
                 }
             }
@@ -207,21 +208,24 @@ __global__ void __launch_bounds__(kET) k_explore(DevGraph g, const ExploreJob* _
                            bit_test(jc[ci[it]].Bv, d);
                 if (MODE == 1) fits[it] = fits[it] && __ldg(J.mask + m[it].row) == full;
             }
+            if (MODE == 0) {
+                uint32_t key[kEI];
+                unsigned long long bits[kEI];
 #pragma unroll
-            for (int it = 0; it < kEI; it++) {
-                if (MODE == 0) {
-                    const unsigned long long bits = fits[it] ? (1ull << ci[it]) : 0ull;
-                    uint32_t peers;
-                    const uint32_t leader = warp_group_leader(v[it] ? m[it].row : 0xffffffffu, peers);
-                    const uint32_t lo32 = __reduce_or_sync(peers, (uint32_t)bits);
-                    const uint32_t hi32 = __reduce_or_sync(peers, (uint32_t)(bits >> 32));
-                    const unsigned long long agg = ((unsigned long long)hi32 << 32) | lo32;
-                    if (v[it] && lane_id() == leader && agg && (__ldcg(J.mask + m[it].row) & agg) != agg)
-                        atomicOr(J.mask + m[it].row, agg);
-                } else if (fits[it]) {
-                    const uint32_t d = arc[it] >> g.lbits;
-                    atomicOr(jc[ci[it]].X + (d >> 5), 1u << (d & 31));
+                for (int it = 0; it < kEI; it++) {
+                    key[it] = m[it].row;
+                    bits[it] = fits[it] ? (1ull << ci[it]) : 0ull;
                 }
+                run_or64<kEI>(v, key, bits, [&](uint32_t row, unsigned long long agg) {
+                    if ((__ldcg(J.mask + row) & agg) != agg) atomicOr(J.mask + row, agg);
+                });
+            } else {
+#pragma unroll
+                for (int it = 0; it < kEI; it++)
+                    if (fits[it]) {
+                        const uint32_t d = arc[it] >> g.lbits;
+                        atomicOr(jc[ci[it]].X + (d >> 5), 1u << (d & 31));
+                    }
             }
         });
     });

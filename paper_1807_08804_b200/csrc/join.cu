@@ -78,21 +78,26 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
                     pred[it] = !dup;
                 }
             }
+            if (!WRITE) {
+                uint32_t key[kPI], one[kPI];
 #pragma unroll
-            for (int it = 0; it < kPI; it++) {
-                if (!WRITE) {
-                    uint32_t peers;
-                    const uint32_t leader = warp_group_leader(v[it] ? m[it].row : 0xffffffffu, peers);
-                    const uint32_t nvalid = __popc(__ballot_sync(kFull, pred[it]) & peers);
-                    if (v[it] && lane_id() == leader && nvalid) atomicAdd(J.kcnt + m[it].row, nvalid);
-                    count += pred[it] ? 1 : 0;
-                    jcount += pred[it] ? 1 : 0;
-                } else {
-                    uint32_t tot;
-                    const uint32_t rank = block_excl_scan((uint32_t)pred[it], &tot);
-                    if (pred[it]) val[running + rank] = x[it] >> g.lbits;
-                    running += tot;
+                for (int it = 0; it < kPI; it++) {
+                    key[it] = m[it].row;
+                    one[it] = pred[it] ? 1u : 0u;
+                    count += one[it];
+                    jcount += one[it];
                 }
+                run_sum<kPI>(v, key, one, [&](uint32_t row, uint32_t n) { atomicAdd(J.kcnt + row, n); });
+            } else {
+                uint32_t mine = 0;
+#pragma unroll
+                for (int it = 0; it < kPI; it++) mine += pred[it] ? 1u : 0u;
+                uint32_t tot;
+                uint64_t pos = running + block_excl_scan(mine, &tot);
+#pragma unroll
+                for (int it = 0; it < kPI; it++)
+                    if (pred[it]) val[pos++] = x[it] >> g.lbits;
+                running += tot;
             }
         });
         if (!WRITE) {
@@ -248,32 +253,38 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
                 writes[it] = valid[it] && !J.nowrite;
             }
         }
+        if (WRITE) {
+            uint32_t mine = 0;
 #pragma unroll
-        for (int it = 0; it < kPI; it++) {
-            if (WRITE) {
-                uint32_t tot;
-                const uint32_t rank = block_excl_scan((uint32_t)writes[it], &tot);
-                if (writes[it]) {
-                    const JoinJob& J = a.jobs[m[it].job];
-                    const uint32_t* row = m[it].rowp;
-                    uint32_t* dst = a.out + (running + rank) * a.wout;
-                    if (J.final_) {
-                        for (uint32_t c = 0; c < a.w; c++) dst[J.perm[c]] = __ldg(row + c);
-                        dst[J.perm[a.w]] = cand[it];
-                    } else {
-                        for (uint32_t c = 0; c < a.w; c++) dst[c] = __ldg(row + c);
-                        dst[a.w] = cand[it];
-                    }
+            for (int it = 0; it < kPI; it++) mine += writes[it] ? 1u : 0u;
+            uint32_t tot;
+            uint64_t pos = running + block_excl_scan(mine, &tot);
+#pragma unroll
+            for (int it = 0; it < kPI; it++) {
+                if (!writes[it]) continue;
+                const JoinJob& J = a.jobs[m[it].job];
+                const uint32_t* row = m[it].rowp;
+                uint32_t* dst = a.out + (pos++) * a.wout;
+                if (J.final_) {
+                    for (uint32_t c = 0; c < a.w; c++) dst[J.perm[c]] = __ldg(row + c);
+                    dst[J.perm[a.w]] = cand[it];
+                } else {
+                    for (uint32_t c = 0; c < a.w; c++) dst[c] = __ldg(row + c);
+                    dst[a.w] = cand[it];
                 }
-                running += tot;
-            } else {
-                uint32_t peers;
-                const uint32_t leader = warp_group_leader(v[it] ? m[it].job : 0xffffffffu, peers);
-                const uint32_t nvalid = __popc(__ballot_sync(kFull, valid[it]) & peers);
-                if (v[it] && lane_id() == leader && nvalid)
-                    atomicAdd(a.jobs[m[it].job].total, (unsigned long long)nvalid);
-                count += writes[it] ? 1 : 0;
             }
+            running += tot;
+        } else {
+            uint32_t key[kPI], one[kPI];
+#pragma unroll
+            for (int it = 0; it < kPI; it++) {
+                key[it] = m[it].job;
+                one[it] = valid[it] ? 1u : 0u;
+                count += writes[it] ? 1u : 0u;
+            }
+            run_sum<kPI>(v, key, one, [&](uint32_t job, uint32_t n) {
+                atomicAdd(a.jobs[job].total, (unsigned long long)n);
+            });
         }
     });
     if (!WRITE) last_block_scan(a.ctl.blk, gridDim.x, a.ctl.done, a.ctl.info, P, count);

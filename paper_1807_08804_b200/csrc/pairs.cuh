@@ -172,12 +172,13 @@ namespace gps {
 //
 // Per chunk of T*IPT consecutive pairs: the offsets of a window of W rows are
 // staged (coalesced), then load_meta(row) -> Meta is evaluated ONCE per row that
-// meets the chunk (in parallel) and kept in s_meta, so a pair costs a
-// shared-memory binary search + shared-memory metadata instead of a chain of
-// dependent global loads.  body(v[], m[], j[]) receives all IPT items of the
-// thread at once (so it can issue their global loads back to back); rows
-// outside the window (runs of empty rows) fall back to load_meta from global.
-// body may use block-wide barriers (called uniformly).
+// meets the chunk (in parallel) and kept in s_meta.  Thread t owns the IPT
+// CONSECUTIVE pairs cp + t*IPT + [0, IPT): one shared-memory binary search finds
+// the row of its first pair, the rest walk forward.  body(v[], m[], j[])
+// receives all IPT items at once (rows non-decreasing across the items and
+// across the threads of the block), so it can issue their global loads back to
+// back and aggregate per row.  Rows outside the window (runs of empty rows) fall
+// back to load_meta from global.  body may use block-wide barriers.
 template <typename Meta, int T, int IPT, int W, typename OffF, typename LoadMeta, typename Body>
 __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t nrows, OffF offs, LoadMeta load_meta,
                                             Meta* s_meta, uint64_t* s_off, uint64_t* s_row, Body&& body) {
@@ -198,14 +199,16 @@ __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t n
         bool v[IPT];
         Meta m[IPT];
         uint64_t j[IPT];
+        const uint64_t pt = cp + (uint64_t)tid * IPT;
+        uint32_t i = (pt < cend && pt < wend) ? pairs_find_smem(s_off, wn, pt) : 0;
 #pragma unroll
         for (int it = 0; it < IPT; it++) {
-            const uint64_t p = cp + (uint64_t)it * T + tid;
+            const uint64_t p = pt + it;
             v[it] = p < cend;
             j[it] = 0;
             if (v[it]) {
                 if (p < wend) {
-                    const uint32_t i = pairs_find_smem(s_off, wn, p);
+                    while (s_off[i + 1] <= p) i++;
                     m[it] = s_meta[i];
                     j[it] = p - s_off[i];
                 } else {
@@ -224,6 +227,70 @@ __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t n
             __syncthreads();
             r0 = *s_row;
         }
+    }
+}
+
+// Per-key aggregation of a thread's IPT consecutive items (keys non-decreasing
+// across items and lanes): runs wholly inside the thread are emitted directly;
+// the thread's first and last runs (which may continue in the neighbouring
+// lanes) are combined across the warp with __match_any_sync + redux, so a hub
+// row spanning a whole warp costs one emit.  emit(key, agg) is called by one lane.
+template <int IPT, typename Emit>
+__device__ __forceinline__ void run_sum(const bool (&v)[IPT], const uint32_t (&key)[IPT], const uint32_t (&val)[IPT],
+                                        Emit&& emit) {
+    const uint32_t NONE = 0xffffffffu;
+    uint32_t fk = NONE, fa = 0, ck = NONE, ca = 0;
+    int nr = 0;
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        if (!v[it]) continue;
+        if (nr == 0) { ck = key[it]; ca = val[it]; nr = 1; }
+        else if (key[it] == ck) ca += val[it];
+        else {
+            if (nr == 1) { fk = ck; fa = ca; } else if (ca) emit(ck, ca);
+            ck = key[it]; ca = val[it]; nr++;
+        }
+    }
+    {
+        const uint32_t k1 = nr >= 2 ? fk : NONE;
+        const uint32_t peers = __match_any_sync(kFull, k1);
+        const uint32_t s = __reduce_add_sync(peers, nr >= 2 ? fa : 0u);
+        if (k1 != NONE && lane_id() == (uint32_t)(__ffs(peers) - 1) && s) emit(k1, s);
+    }
+    {
+        const uint32_t k2 = nr >= 1 ? ck : NONE;
+        const uint32_t peers = __match_any_sync(kFull, k2);
+        const uint32_t s = __reduce_add_sync(peers, nr >= 1 ? ca : 0u);
+        if (k2 != NONE && lane_id() == (uint32_t)(__ffs(peers) - 1) && s) emit(k2, s);
+    }
+}
+
+template <int IPT, typename Emit>
+__device__ __forceinline__ void run_or64(const bool (&v)[IPT], const uint32_t (&key)[IPT],
+                                         const unsigned long long (&val)[IPT], Emit&& emit) {
+    const uint32_t NONE = 0xffffffffu;
+    uint32_t fk = NONE, ck = NONE;
+    unsigned long long fa = 0, ca = 0;
+    int nr = 0;
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        if (!v[it]) continue;
+        if (nr == 0) { ck = key[it]; ca = val[it]; nr = 1; }
+        else if (key[it] == ck) ca |= val[it];
+        else {
+            if (nr == 1) { fk = ck; fa = ca; } else if (ca) emit(ck, ca);
+            ck = key[it]; ca = val[it]; nr++;
+        }
+    }
+#pragma unroll
+    for (int pass = 0; pass < 2; pass++) {
+        const uint32_t k = pass == 0 ? (nr >= 2 ? fk : NONE) : (nr >= 1 ? ck : NONE);
+        const unsigned long long a = pass == 0 ? (nr >= 2 ? fa : 0ull) : (nr >= 1 ? ca : 0ull);
+        const uint32_t peers = __match_any_sync(kFull, k);
+        const uint32_t lo = __reduce_or_sync(peers, (uint32_t)a);
+        const uint32_t hi = __reduce_or_sync(peers, (uint32_t)(a >> 32));
+        const unsigned long long agg = ((unsigned long long)hi << 32) | lo;
+        if (k != NONE && lane_id() == (uint32_t)(__ffs(peers) - 1) && agg) emit(k, agg);
     }
 }
 

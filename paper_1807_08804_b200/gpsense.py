@@ -161,8 +161,11 @@ class _DeviceRows:
                                          "stream": None}
 
     def __del__(self):
-        if self._res:
-            lib.gps_result_free(self._res)
+        if self._res and lib is not None:
+            try:
+                lib.gps_result_free(self._res)
+            except Exception:
+                pass
             self._res = None
 
 
