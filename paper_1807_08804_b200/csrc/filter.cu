@@ -135,96 +135,73 @@ void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32
 
 // -------------------------------------------------------------- a4 explore
 constexpr int kET = 256;
-constexpr int kEI = 4;
-constexpr int kEW = 512;
+constexpr int kEI = 8;
+constexpr int kEW = 1024;
 
 struct ExMeta {             // one candidate row of an explore job, staged per chunk
-    uint32_t row, key;
-    uint32_t bo, dout;      // out-adjacency base / length of the candidate
-    uint32_t bi, din;       // in-adjacency base / length
+    uint32_t row, key, base, skip;
 };
 
 template <int MODE>   // 0: prune (mark satisfied constraints), 1: propagate
-__global__ void __launch_bounds__(kET) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs,
-                                                 const Cons* __restrict__ cons, uint32_t nj,
+__global__ void __launch_bounds__(kET) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
                                                  unsigned long long* bytes_acc) {
     extern __shared__ uint64_t s_jp[];      // [nj+1] job pair prefix
     __shared__ uint64_t s_off[kEW + 1];
     __shared__ ExMeta s_meta[kEW];
     __shared__ uint64_t s_row;
-    job_prefix(nj, [&](uint32_t j) -> uint64_t {
-        const ExploreJob& J = jobs[j];
-        const uint32_t C = *J.cnt;
-        return (uint64_t)J.no * __ldg(J.seg_out + C) + (uint64_t)J.ni * __ldg(J.seg_in + C);
-    }, s_jp);
+    job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].cnt); }, s_jp);
     uint64_t p0, p1;
     pairs_range(s_jp[nj], blockIdx.x, gridDim.x, p0, p1);
     for_job_ranges(s_jp, nj, p0, p1, [&](uint32_t jj, uint64_t lo, uint64_t hi) {
-        const ExploreJob& J = jobs[jj];
+        const ExploreJob J = jobs[jj];             // by value: fields stay in registers across atomics
         const uint32_t C = *J.cnt;
-        const uint64_t no = J.no, ni = J.ni;
-        const int nc = (int)(J.no + J.ni);
-        const unsigned long long full = nc >= 64 ? ~0ull : ((1ull << nc) - 1ull);
-        const Cons* jc = cons + J.c0;
-        auto offs = [&](uint64_t i) -> uint64_t {
-            return no * __ldg(J.seg_out + i) + ni * __ldg(J.seg_in + i);
-        };
+        const uint32_t* off = J.dir ? g.off_in : g.off_out;
+        const uint32_t* arcs = J.dir ? g.arc_in : g.arc_out;
+        const unsigned long long bitm = 1ull << J.bit;
+        const unsigned long long full = J.nc >= 64 ? ~0ull : ((1ull << J.nc) - 1ull);
+        auto offs = [&](uint64_t i) -> uint64_t { return (uint64_t)__ldg(J.seg + i); };
         auto load = [&](uint64_t r) -> ExMeta {
             ExMeta m;
             m.row = (uint32_t)r;
             m.key = __ldg(J.cands + r);
-            m.dout = __ldg(J.seg_out + r + 1) - __ldg(J.seg_out + r);
-            m.din = __ldg(J.seg_in + r + 1) - __ldg(J.seg_in + r);
-            m.bo = __ldg(g.off_out + m.key);
-            m.bi = __ldg(g.off_in + m.key);
+            m.base = __ldg(off + m.key);
+            const unsigned long long mk = __ldcg(J.mask + r);
+            // prune: constraint already satisfied (an earlier chunk found a fitting arc) -> skip the row;
+            // propagate: only candidates that satisfied every constraint propagate
+            m.skip = MODE == 0 ? ((mk & bitm) != 0) : (mk != full);
             return m;
         };
         pair_chunks<ExMeta, kET, kEI, kEW>(lo, hi, (uint64_t)C, offs, load, s_meta, s_off, &s_row,
                                            [&](const bool (&v)[kEI], const ExMeta (&m)[kEI], const uint64_t (&j)[kEI]) {
-            uint32_t arc[kEI], ci[kEI];
+            uint32_t arc[kEI];
+            bool live[kEI];
 #pragma unroll
             for (int it = 0; it < kEI; it++) {
-                arc[it] = 0;
-                ci[it] = 0;
-                if (v[it]) {
-                    const uint32_t jj32 = (uint32_t)j[it];        // < (no + ni) * degree < 2^32
-                    const uint32_t nout = J.no * m[it].dout;
-                    if (jj32 < nout) {
-                        ci[it] = jj32 / m[it].dout;
-                        arc[it] = __ldg(g.arc_out + m[it].bo + (jj32 - ci[it] * m[it].dout));
-                    } else {
-                        const uint32_t r = jj32 - nout;
-                        const uint32_t cin = r / m[it].din;
-                        ci[it] = J.no + cin;
-                        arc[it] = __ldg(g.arc_in + m[it].bi + (r - cin * m[it].din));
-                    }
-                }
+                live[it] = v[it] && !m[it].skip;
+                arc[it] = live[it] ? __ldg(arcs + m[it].base + (uint32_t)j[it]) : 0u;
             }
             bool fits[kEI];
 #pragma unroll
             for (int it = 0; it < kEI; it++) {
                 const uint32_t d = arc[it] >> g.lbits;
-                fits[it] = v[it] && lab_ok(arc[it], g.lmask, jc[ci[it]].lab) && d != m[it].key &&
-                           bit_test(jc[ci[it]].Bv, d);
-                if (MODE == 1) fits[it] = fits[it] && __ldg(J.mask + m[it].row) == full;
+                fits[it] = live[it] && lab_ok(arc[it], g.lmask, J.lab) && d != m[it].key && bit_test(J.Bv, d);
             }
             if (MODE == 0) {
-                uint32_t key[kEI];
-                unsigned long long bits[kEI];
+                uint32_t key[kEI], one[kEI];
 #pragma unroll
                 for (int it = 0; it < kEI; it++) {
                     key[it] = m[it].row;
-                    bits[it] = fits[it] ? (1ull << ci[it]) : 0ull;
+                    one[it] = fits[it] ? 1u : 0u;
                 }
-                run_or64<kEI>(v, key, bits, [&](uint32_t row, unsigned long long agg) {
-                    if ((__ldcg(J.mask + row) & agg) != agg) atomicOr(J.mask + row, agg);
+                run_sum<kEI>(v, key, one, [&](uint32_t row, uint32_t) {
+                    if (!(__ldcg(J.mask + row) & bitm)) atomicOr(J.mask + row, bitm);
                 });
             } else {
 #pragma unroll
                 for (int it = 0; it < kEI; it++)
                     if (fits[it]) {
                         const uint32_t d = arc[it] >> g.lbits;
-                        atomicOr(jc[ci[it]].X + (d >> 5), 1u << (d & 31));
+                        atomicOr(J.X + (d >> 5), 1u << (d & 31));
                     }
             }
         });
@@ -232,11 +209,10 @@ __global__ void __launch_bounds__(kET) k_explore(DevGraph g, const ExploreJob* _
     if (bytes_acc && threadIdx.x == 0 && p1 > p0) atomicAdd(bytes_acc, (unsigned long long)(p1 - p0) * 4ull);
 }
 
-__global__ void __launch_bounds__(256) k_clear(const ExploreJob* __restrict__ jobs) {
-    const ExploreJob& J = jobs[blockIdx.y];
+__global__ void __launch_bounds__(256) k_clear(const ClearJob* __restrict__ jobs) {
+    const ClearJob J = jobs[blockIdx.y];
     const uint32_t C = *J.cnt;
-    const int nc = (int)(J.no + J.ni);
-    const unsigned long long full = nc >= 64 ? ~0ull : ((1ull << nc) - 1ull);
+    const unsigned long long full = J.nc >= 64 ? ~0ull : ((1ull << J.nc) - 1ull);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < C; i += gridDim.x * blockDim.x) {
         if (J.mask[i] != full) {
             const uint32_t key = J.cands[i];
@@ -247,21 +223,22 @@ __global__ void __launch_bounds__(256) k_clear(const ExploreJob* __restrict__ jo
 
 static size_t jp_smem(uint32_t nj) { return sizeof(uint64_t) * (nj + 1); }
 
-void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, const Cons* d_cons, uint32_t nj) {
+void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, const ClearJob* d_clear,
+               uint32_t nclear) {
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
     const uint32_t G = (uint32_t)c->nsm * 6;
-    launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), jp_smem(nj), k_explore<0>, g, d_jobs, d_cons, nj,
+    launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), jp_smem(nj), k_explore<0>, g, d_jobs, nj,
            c->d_bytes + GPS_K_EXPLORE);
-    launch(c, GPS_K_EXPLORE, dim3(std::max<uint32_t>(1, (uint32_t)c->nsm * 2 / nj + 1), nj), dim3(256), 0, k_clear,
-           d_jobs);
+    launch(c, GPS_K_EXPLORE, dim3(std::max<uint32_t>(1, (uint32_t)c->nsm * 2 / nclear + 1), nclear), dim3(256), 0,
+           k_clear, d_clear);
 }
 
-void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, const Cons* d_cons, uint32_t nj) {
+void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj) {
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
     const uint32_t G = (uint32_t)c->nsm * 6;
-    launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), jp_smem(nj), k_explore<1>, g, d_jobs, d_cons, nj,
+    launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), jp_smem(nj), k_explore<1>, g, d_jobs, nj,
            c->d_bytes + GPS_K_EXPLORE);
 }
 

@@ -53,26 +53,32 @@ void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32
 // ---- a4/a5 kernel_explore (Alg. 2 lines 14-22) --------------------
 // Constraint of a candidate u' of u for one query arc between u and v:
 // adj_dir(u') must hold some v' != u' with a fitting label and v' in B[v].
-struct Cons {
-    const uint32_t* Bv;   // bitmap of the neighbour v
-    uint32_t* X;          // propagation scratch for v
-    int32_t lab;          // edge label or -1
-    int dir;              // 0: arc u -> v (out-adjacency of u'), 1: arc v -> u (in-adjacency)
-};
+// One (query vertex u, constraint c) pair of an explore step: the pair space is
+// (candidate u' of u, arc of adj_dir(u')).
 struct ExploreJob {
     const uint32_t* cands;  // c_array[u]
     const uint32_t* cnt;    // device |C(u)|
-    const uint32_t* seg_out;
-    const uint32_t* seg_in;
+    const uint32_t* seg;    // degree prefix of the candidates in direction dir
     unsigned long long* mask;  // [|C(u)|] satisfied-constraint bits (zeroed by collect)
-    uint32_t* Bu;           // bitmap of u (pruned bits cleared)
-    uint32_t no, ni;        // constraints cons[c0 .. c0+no) are out-arcs, then ni in-arcs
-    uint32_t c0;
-    uint32_t pad;
+    const uint32_t* Bv;     // bitmap of the neighbour v
+    uint32_t* X;            // propagation scratch for v
+    int32_t lab;            // edge label or -1
+    uint32_t dir;           // 0: arc u -> v (out-adjacency of u'), 1: arc v -> u (in-adjacency)
+    uint32_t bit;           // constraint index (bit in mask)
+    uint32_t nc;            // constraints of this (query, u) step (full mask = 2^nc - 1)
 };
-// prune (+ clear) over all jobs; propagate over the listed (initialisation) jobs
-void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, const Cons* d_cons, uint32_t nj);
-void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, const Cons* d_cons, uint32_t nj);
+// prune over all (u, constraint) jobs; clear over the (u) jobs; propagate over the
+// constraints of initialisation steps
+struct ClearJob {
+    const uint32_t* cands;
+    const uint32_t* cnt;
+    const unsigned long long* mask;
+    uint32_t* Bu;
+    uint32_t nc, pad;
+};
+void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, const ClearJob* d_clear,
+               uint32_t nclear);
+void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj);
 
 // B &= X[x0] & ... & X[x1-1], then the scratch is zeroed.
 struct AndJob {

@@ -143,7 +143,7 @@ void filter_phase(Chunk& ch, int stage) {
     for (size_t s = 0; s < S; s++) {
         std::vector<CollectJob> cj;
         std::vector<ExploreJob> ej, pj;
-        std::vector<Cons> cons;
+        std::vector<ClearJob> clj;
         std::vector<AndJob> aj;
         std::vector<uint32_t*> xs;
         for (QS* q : ch.qs) {
@@ -155,29 +155,33 @@ void filter_phase(Chunk& ch, int stage) {
             const int u = st.u;
             cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0], q->seg[u][1],
                                     q->mask});
-            std::vector<Constraint> ord;
-            for (const Constraint& cs : st.cons)
-                if (cs.dir == 0) ord.push_back(cs);
-            const uint32_t no = (uint32_t)ord.size();
-            for (const Constraint& cs : st.cons)
-                if (cs.dir == 1) ord.push_back(cs);
-            if (ord.empty()) continue;
-            const uint32_t c0 = (uint32_t)cons.size();
-            for (size_t i = 0; i < ord.size(); i++)
-                cons.push_back(Cons{ch.Bp(*q, ord[i].v), st.propagate ? ch.Xp(*q, (int)i) : nullptr,
-                                    p.arcs[ord[i].arc].lab, ord[i].dir});
-            ExploreJob e{q->carr[u], q->cnt + u, q->seg[u][0], q->seg[u][1], q->mask, ch.Bp(*q, u),
-                         no, (uint32_t)ord.size() - no, c0, 0};
-            ej.push_back(e);
+            const uint32_t nc = (uint32_t)st.cons.size();
+            if (nc == 0) continue;
+            for (uint32_t i = 0; i < nc; i++) {
+                const Constraint& cs = st.cons[i];
+                ExploreJob e{};
+                e.cands = q->carr[u];
+                e.cnt = q->cnt + u;
+                e.seg = q->seg[u][cs.dir];
+                e.mask = q->mask;
+                e.Bv = ch.Bp(*q, cs.v);
+                e.X = st.propagate ? ch.Xp(*q, (int)i) : nullptr;
+                e.lab = p.arcs[cs.arc].lab;
+                e.dir = (uint32_t)cs.dir;
+                e.bit = i;
+                e.nc = nc;
+                ej.push_back(e);
+                if (st.propagate) pj.push_back(e);
+            }
+            clj.push_back(ClearJob{q->carr[u], q->cnt + u, q->mask, ch.Bp(*q, u), nc, 0});
             if (st.propagate) {
-                pj.push_back(e);
                 std::vector<int> targets;
-                for (const Constraint& cs : ord)
+                for (const Constraint& cs : st.cons)
                     if (std::find(targets.begin(), targets.end(), cs.v) == targets.end()) targets.push_back(cs.v);
                 for (int v : targets) {
                     AndJob a{ch.Bp(*q, v), (uint32_t)xs.size(), 0};
-                    for (size_t i = 0; i < ord.size(); i++)
-                        if (ord[i].v == v) xs.push_back(ch.Xp(*q, (int)i));
+                    for (uint32_t i = 0; i < nc; i++)
+                        if (st.cons[i].v == v) xs.push_back(ch.Xp(*q, (int)i));
                     a.x1 = (uint32_t)xs.size();
                     aj.push_back(a);
                 }
@@ -186,10 +190,9 @@ void filter_phase(Chunk& ch, int stage) {
         if (cj.empty()) continue;
         run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
         if (ej.empty()) continue;
-        const Cons* dcons = upload(c, cons, ch.keep);
-        run_prune(c, d, upload(c, ej, ch.keep), dcons, (uint32_t)ej.size());
+        run_prune(c, d, upload(c, ej, ch.keep), (uint32_t)ej.size(), upload(c, clj, ch.keep), (uint32_t)clj.size());
         if (!pj.empty()) {
-            run_propagate(c, d, upload(c, pj, ch.keep), dcons, (uint32_t)pj.size());
+            run_propagate(c, d, upload(c, pj, ch.keep), (uint32_t)pj.size());
             run_bitand(c, d, upload(c, aj, ch.keep), upload(c, xs, ch.keep), (uint32_t)aj.size());
         }
     }
@@ -487,7 +490,7 @@ void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t n
             QS* q = todo[i];
             size_t b = filter_bytes(*q, g->d.nws);
             if (!chunk.empty() && (chunk.size() >= kMaxBatch || bytes + b > kChunkBytes ||
-                                   ecj + 2 * (size_t)q->E > kMaxJobsPerLaunch || vtx + q->k > kMaxJobsPerLaunch))
+                                   ecj + 2 * (size_t)std::max(q->E, 1) > kMaxJobsPerLaunch || vtx + q->k > kMaxJobsPerLaunch))
                 break;
             chunk.push_back(q);
             bytes += b;
