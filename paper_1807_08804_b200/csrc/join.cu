@@ -22,7 +22,7 @@
 namespace gps {
 
 constexpr int kPT = 256;    // threads per block
-constexpr int kPI = 8;      // pairs per thread per chunk
+constexpr int kPI = 4;      // pairs per thread per chunk
 constexpr int kPW = 1024;   // rows of offsets staged in shared memory
 
 static size_t jp_smem(uint32_t nj) { return sizeof(uint64_t) * (nj + 1); }
