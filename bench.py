@@ -150,7 +150,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--workers", type=int, default=8, help="library batch workers (0 = one query at a time)")
+    ap.add_argument("--workers", type=int, default=4, help="library batch workers (0 = one query at a time)")
+    ap.add_argument("--slice", type=int, default=25, help="queries per worker hand-out (batch-synchronous unit)")
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
 
@@ -183,6 +184,7 @@ def main():
 
     if args.workers:
         ctx.set_workers(args.workers)
+        ctx.set_slice(args.slice)
 
     def step():
         if args.workers:
@@ -279,7 +281,9 @@ def main():
         "config": {"workload": WORKLOAD, "queries_per_step_per_gpu": len(queries),
                    "embeddings_per_step_per_gpu": emb_total // args.steps,
                    "parallelism": f"graph replicated, queries sharded over {world} GPU(s); "
-                                  f"{args.workers or 1} concurrent query streams per GPU (gps_match_batch)",
+                                  f"gps_match_batch: {args.workers} worker streams x {args.slice}-query "
+                                  f"batch-synchronous slices per GPU" if args.workers else
+                                  f"graph replicated, queries sharded over {world} GPU(s); one query at a time",
                    "l2": "flushed between timed steps (256 MiB write outside the events); the 15 MB graph "
                          "is L2-resident within a step" if flush is not None else "not flushed"},
         "gpu_launches": st["launches"] // args.steps * args.steps,

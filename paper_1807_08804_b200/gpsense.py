@@ -169,6 +169,23 @@ class _DeviceRows:
             self._res = None
 
 
+class _HostRows:
+    """Owner of a host (pinned) gps_result; exposes __array_interface__ for numpy (zero-copy)."""
+
+    def __init__(self, res, rows, cols, ptr):
+        self._res = res
+        self.__array_interface__ = {"shape": (int(rows), int(cols)), "typestr": "<u4",
+                                    "data": (int(ptr), False), "version": 3}
+
+    def __del__(self):
+        if self._res and lib is not None:
+            try:
+                lib.gps_result_free(self._res)
+            except Exception:
+                pass
+            self._res = None
+
+
 class Graph:
     def __init__(self, ctx: "Context", handle):
         self.ctx = ctx
@@ -316,12 +333,11 @@ class Context:
             rows, cols, ptr, ondev = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_void_p(), ctypes.c_int()
             lib.gps_result_info(res[i], ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(ptr), ctypes.byref(ondev))
             if not device:
-                nn = rows.value * cols.value
-                a = np.zeros((rows.value, cols.value), np.uint32)
-                if nn:
-                    ctypes.memmove(a.ctypes.data, ptr.value, nn * 4)
-                lib.gps_result_free(ctypes.c_void_p(res[i]))
-                out.append(a)
+                if rows.value == 0:
+                    lib.gps_result_free(ctypes.c_void_p(res[i]))
+                    out.append(np.zeros((0, cols.value), np.uint32))
+                else:   # zero-copy view of the library's pinned host rows
+                    out.append(np.asarray(_HostRows(ctypes.c_void_p(res[i]), rows.value, cols.value, ptr.value)))
                 continue
             holder = _DeviceRows(ctypes.c_void_p(res[i]), rows.value, cols.value, ptr.value)
             if rows.value == 0:
