@@ -160,6 +160,14 @@ GPS_API gps_status gps_match_batch(gps_ctx* ctx, const gps_graph* g, const gps_q
                                    const gps_match_opts* opts, gps_result** results, gps_status* statuses);
 GPS_API gps_status gps_count_batch(gps_ctx* ctx, const gps_graph* g, const gps_query* queries, uint32_t nq,
                                    const gps_match_opts* opts, uint64_t* counts, gps_status* statuses);
+/* Batched execution with every result copied into ONE caller-owned host buffer
+ * (pinned memory recommended) of cap_words uint32: query i's rows (row-major,
+ * rows[i] x k_i) start at word offset offsets[i] (the order of the segments in
+ * the buffer is unspecified).  GPS_EOVERFLOW if the results do not fit (rows[]
+ * are still filled). */
+GPS_API gps_status gps_match_batch_host(gps_ctx* ctx, const gps_graph* g, const gps_query* queries, uint32_t nq,
+                                        const gps_match_opts* opts, uint32_t* host_out, uint64_t cap_words,
+                                        uint64_t* offsets, uint64_t* rows, gps_status* statuses);
 /* Number of batch workers (1..64; 0 = default 2).  Destroys existing workers (and their results). */
 GPS_API gps_status gps_set_workers(gps_ctx* ctx, uint32_t n);
 /* Queries per worker hand-out in the batch calls (each hand-out runs batch-synchronously:
@@ -178,7 +186,8 @@ GPS_API const char* gps_last_error(void);
 /* Kernel classes for stats / profiling. */
 enum {
     GPS_K_CHECK = 0, GPS_K_COLLECT, GPS_K_EXPLORE, GPS_K_BITAND, GPS_K_EC_COUNT, GPS_K_EC_WRITE,
-    GPS_K_SCAN, GPS_K_JOIN_LEN, GPS_K_JOIN_COUNT, GPS_K_JOIN_WRITE, GPS_K_LOAD, GPS_K_NCLASSES
+    GPS_K_SCAN, GPS_K_JOIN_LEN, GPS_K_JOIN_COUNT, GPS_K_JOIN_WRITE, GPS_K_LOAD, GPS_K_PROPAGATE, GPS_K_CLEAR,
+    GPS_K_NCLASSES
 };
 
 typedef struct {

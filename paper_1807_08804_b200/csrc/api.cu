@@ -334,6 +334,45 @@ gps_status gps_match_batch(gps_ctx* c, const gps_graph* g, const gps_query* qs, 
     });
 }
 
+gps_status gps_match_batch_host(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t nq,
+                                const gps_match_opts* opts, uint32_t* host_out, uint64_t cap_words,
+                                uint64_t* offsets, uint64_t* rows, gps_status* statuses) {
+    return guarded([&] {
+        check_args(c, g);
+        if (nq && (!qs || !offsets || !rows)) fail(GPS_EINVAL, "null queries/offsets/rows");
+        DeviceGuard dg(c->device);
+        const gps_match_opts o = resolve_opts(opts);
+        std::vector<gps_status> st(nq, GPS_OK);
+        std::atomic<uint64_t> bump{0};
+        std::atomic<bool> overflow{false};
+        run_sliced(c, nq, [&](gps_ctx* sc, uint32_t lo, uint32_t cnt) {
+            std::vector<QueryResult> qr;
+            run_queries(sc, g, qs + lo, cnt, o, false, qr);
+            for (uint32_t i = 0; i < cnt; i++) {
+                st[lo + i] = qr[i].status;
+                const uint64_t words = qr[i].rows * qr[i].cols;
+                rows[lo + i] = qr[i].rows;
+                const uint64_t at = bump.fetch_add(words);
+                offsets[lo + i] = at;
+                if (at + words > cap_words) {
+                    overflow = true;
+                    continue;
+                }
+                if (words && host_out)
+                    GPS_CK(cudaMemcpyAsync(host_out + at, qr[i].data, words * 4, cudaMemcpyDeviceToHost, sc->stream));
+            }
+            ctx_sync(sc);
+        });
+        gps_status first = GPS_OK;
+        for (uint32_t i = 0; i < nq; i++) {
+            if (statuses) statuses[i] = st[i];
+            if (st[i] != GPS_OK && first == GPS_OK) first = st[i];
+        }
+        if (first != GPS_OK) fail(first, "some queries of the batch failed (see statuses)");
+        if (overflow) fail(GPS_EOVERFLOW, "results exceed cap_words");
+    });
+}
+
 gps_status gps_count_batch(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t nq,
                            const gps_match_opts* opts, uint64_t* counts, gps_status* statuses) {
     return guarded([&] {

@@ -230,7 +230,7 @@ void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t
     const uint32_t G = (uint32_t)c->nsm * 6;
     launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), jp_smem(nj), k_explore<0>, g, d_jobs, nj,
            c->d_bytes + GPS_K_EXPLORE);
-    launch(c, GPS_K_EXPLORE, dim3(std::max<uint32_t>(1, (uint32_t)c->nsm * 2 / nclear + 1), nclear), dim3(256), 0,
+    launch(c, GPS_K_CLEAR, dim3(std::max<uint32_t>(1, (uint32_t)c->nsm * 2 / nclear + 1), nclear), dim3(256), 0,
            k_clear, d_clear);
 }
 
@@ -238,8 +238,8 @@ void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
     const uint32_t G = (uint32_t)c->nsm * 6;
-    launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), jp_smem(nj), k_explore<1>, g, d_jobs, nj,
-           c->d_bytes + GPS_K_EXPLORE);
+    launch(c, GPS_K_PROPAGATE, dim3(G), dim3(kET), jp_smem(nj), k_explore<1>, g, d_jobs, nj,
+           c->d_bytes + GPS_K_PROPAGATE);
 }
 
 // --------------------------------------------------------------- bit-and

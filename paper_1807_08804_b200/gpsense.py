@@ -23,7 +23,7 @@ GPS_ANY = -1
 GPS_FREE = -1
 GPS_DIRECTED, GPS_UNDIRECTED = 0, 1
 KERNEL_CLASSES = ["check", "collect", "explore", "bitand", "ec_count", "ec_write", "scan", "join_len",
-                  "join_count", "join_write", "load"]
+                  "join_count", "join_write", "load", "propagate", "clear"]
 NK = len(KERNEL_CLASSES)
 K = {name: i for i, name in enumerate(KERNEL_CLASSES)}
 
@@ -101,6 +101,7 @@ def _load_lib():
         "gps_count_batch": (S, [P, P, P, ctypes.c_uint32, P, P, P]),
         "gps_set_workers": (S, [P, ctypes.c_uint32]),
         "gps_set_slice": (S, [P, ctypes.c_uint32]),
+        "gps_match_batch_host": (S, [P, P, P, ctypes.c_uint32, P, P, ctypes.c_uint64, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -114,7 +115,7 @@ EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_grap
             "gps_graph_info", "gps_match", "gps_match_host", "gps_count", "gps_result_info",
             "gps_result_free", "gps_last_error", "gps_get_stats", "gps_reset_stats",
             "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates", "gps_match_batch",
-            "gps_count_batch", "gps_set_workers", "gps_set_slice"]
+            "gps_count_batch", "gps_set_workers", "gps_set_slice", "gps_match_batch_host"]
 
 
 def _check(st: int):
@@ -184,6 +185,48 @@ class _HostRows:
             except Exception:
                 pass
             self._res = None
+
+
+class BatchResult:
+    """Result handles of a gps_match_batch call; rows() is cheap, tensor(i) wraps lazily."""
+
+    def __init__(self, ctx, res, n):
+        self.ctx, self._res, self.n = ctx, res, n
+        self._rows = np.zeros(n, np.uint64)
+        for i in range(n):
+            if res[i]:
+                r = ctypes.c_uint64()
+                lib.gps_result_info(res[i], ctypes.byref(r), None, None, None)
+                self._rows[i] = r.value
+
+    def rows(self) -> np.ndarray:
+        return self._rows
+
+    def tensor(self, i):
+        import torch
+        rows, cols, ptr, ondev = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_void_p(), ctypes.c_int()
+        lib.gps_result_info(self._res[i], ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(ptr),
+                            ctypes.byref(ondev))
+        if rows.value == 0:
+            return torch.empty((0, cols.value), dtype=torch.uint32, device=f"cuda:{self.ctx.device}")
+        h = _DeviceRows(None, rows.value, cols.value, ptr.value)   # owned by this BatchResult
+        t = torch.as_tensor(h, device=f"cuda:{self.ctx.device}")
+        t._gps_owner = self
+        return t
+
+    def free(self):
+        if self._res is not None and lib is not None:
+            for i in range(self.n):
+                if self._res[i]:
+                    lib.gps_result_free(self._res[i])
+                    self._res[i] = None
+        self._res = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 class Graph:
@@ -347,6 +390,32 @@ class Context:
                 out.append(torch.as_tensor(holder, device=f"cuda:{self.device}"))
         _check(rc)
         return out
+
+    def match_batch_raw(self, graph: Graph, queries, opts: Optional[MatchOpts] = None) -> "BatchResult":
+        """Like match_batch but returns a BatchResult (row counts + lazily wrapped tensors)."""
+        qas, arr = self._batch_desc(queries)
+        n = len(qas)
+        res = (ctypes.c_void_p * max(n, 1))()
+        o = opts if opts is not None else default_opts()
+        o = MatchOpts(o.refine_rounds, o.reverse_refine, o.lowconn_threshold, 1)
+        rc = lib.gps_match_batch(self._h, graph.handle, arr, n, ctypes.byref(o), res, None)
+        br = BatchResult(self, res, n)
+        _check(rc)
+        return br
+
+    def match_batch_host(self, graph: Graph, queries, out, opts: Optional[MatchOpts] = None):
+        """All embeddings copied by the library into ONE host buffer `out` (numpy uint32 or a
+        pinned torch tensor).  Returns (offsets, rows) numpy arrays (word offsets into out)."""
+        qas, arr = self._batch_desc(queries)
+        n = len(qas)
+        offs = np.zeros(max(n, 1), np.uint64)
+        rows = np.zeros(max(n, 1), np.uint64)
+        ptr, cap = (out.data_ptr(), out.numel()) if hasattr(out, "data_ptr") else (out.ctypes.data, out.size)
+        _check(lib.gps_match_batch_host(self._h, graph.handle, arr, n,
+                                        ctypes.byref(opts) if opts is not None else None, ctypes.c_void_p(ptr),
+                                        cap, ctypes.c_void_p(offs.ctypes.data), ctypes.c_void_p(rows.ctypes.data),
+                                        None))
+        return offs[:n], rows[:n]
 
     def count_batch(self, graph: Graph, queries, opts: Optional[MatchOpts] = None) -> np.ndarray:
         qas, arr = self._batch_desc(queries)

@@ -321,3 +321,22 @@ def test_batch_workers_and_errors(gps, ctx, cfg1):
         ctx.count_batch(G, bad)
     assert e.value.status == gps.GPS_EDISCONNECTED
     ctx.set_workers(0)
+
+
+def test_cfg2_match_batch_host(ctx, cfg2):
+    """gps_match_batch_host: every result copied into one caller-owned host buffer."""
+    g, G, data = cfg2
+    qs = [Query.from_json(d["query"]) for d in data["queries"][:40]]
+    want_rows = [d["oracle_count"] for d in data["queries"][:40]]
+    buf = np.zeros(sum(r * 6 for r in want_rows) + 10, np.uint32)
+    offs, rows = ctx.match_batch_host(G, qs, buf)
+    assert rows.tolist() == want_rows
+    og = oracle.OracleGraph(g)
+    for i in sorted(range(40), key=lambda i: want_rows[i])[:4]:
+        got = buf[int(offs[i]): int(offs[i]) + int(rows[i]) * 6].reshape(-1, 6)
+        assert np.array_equal(oracle.sort_rows(got), oracle.match(og, qs[i]))
+    br = ctx.match_batch_raw(G, qs[:5])
+    assert br.rows().tolist() == want_rows[:5]
+    t = br.tensor(0)
+    assert t.shape == (want_rows[0], 6)
+    br.free()
