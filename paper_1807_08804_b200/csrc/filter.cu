@@ -136,18 +136,18 @@ void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32
 // -------------------------------------------------------------- a4 explore
 constexpr int kET = 256;
 constexpr int kEI = 8;
-constexpr int kEW = 1024;
+constexpr int kEW = 512;
 
 struct ExMeta {             // one candidate row of an explore job, staged per chunk
     uint32_t row, key, base, skip;
 };
 
 template <int MODE>   // 0: prune (mark satisfied constraints), 1: propagate
-__global__ void __launch_bounds__(kET) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
+__global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
                                                  unsigned long long* bytes_acc) {
     extern __shared__ uint64_t s_jp[];      // [nj+1] job pair prefix
-    __shared__ uint64_t s_off[kEW + 1];
-    __shared__ ExMeta s_meta[kEW];
+    __shared__ uint64_t s_off[2 * (kEW + 1)];
+    __shared__ ExMeta s_meta[2 * kEW];
     __shared__ uint64_t s_row;
     job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].cnt); }, s_jp);
     uint64_t p0, p1;

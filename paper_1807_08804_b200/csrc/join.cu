@@ -23,7 +23,7 @@ namespace gps {
 
 constexpr int kPT = 256;    // threads per block
 constexpr int kPI = 4;      // pairs per thread per chunk
-constexpr int kPW = 1024;   // rows of offsets staged in shared memory
+constexpr int kPW = 512;    // rows of offsets staged in shared memory (double-buffered)
 
 static size_t jp_smem(uint32_t nj) { return sizeof(uint64_t) * (nj + 1); }
 
@@ -36,8 +36,8 @@ template <bool WRITE>
 __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict__ jobs, uint32_t nj, PassCtl ctl,
                                            uint32_t* __restrict__ val, unsigned long long* bytes_acc) {
     extern __shared__ uint64_t s_jp[];
-    __shared__ uint64_t s_off[kPW + 1];
-    __shared__ EcMeta s_meta[kPW];
+    __shared__ uint64_t s_off[2 * (kPW + 1)];
+    __shared__ EcMeta s_meta[2 * kPW];
     __shared__ uint64_t s_row;
     job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].nkeys); }, s_jp);
     const uint64_t P = s_jp[nj];
@@ -217,8 +217,8 @@ struct JMeta {              // one input row of a join step
 template <bool WRITE>
 __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a) {
     extern __shared__ uint64_t s_jr[];   // [nj+1] first row of every job
-    __shared__ uint64_t s_off[kPW + 1];
-    __shared__ JMeta s_meta[kPW];
+    __shared__ uint64_t s_off[2 * (kPW + 1)];
+    __shared__ JMeta s_meta[2 * kPW];
     __shared__ uint64_t s_row;
     for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
     if (threadIdx.x == 0) s_jr[a.nj] = a.R;

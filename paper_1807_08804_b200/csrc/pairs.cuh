@@ -182,25 +182,34 @@ namespace gps {
 template <typename Meta, int T, int IPT, int W, typename OffF, typename LoadMeta, typename Body>
 __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t nrows, OffF offs, LoadMeta load_meta,
                                             Meta* s_meta, uint64_t* s_off, uint64_t* s_row, Body&& body) {
+    // s_off holds 2*(W+1) and s_meta 2*W entries: the window is double-buffered, so a
+    // chunk needs ONE block barrier (between staging and use); the row of the next
+    // chunk is recomputed by every thread from the current window (no broadcast).
+    (void)s_row;
     if (p0 >= p1) return;
     const uint32_t tid = threadIdx.x;
-    if (tid == 0) *s_row = pairs_find_global(offs, 0, nrows, p0);
-    __syncthreads();
-    uint64_t r0 = *s_row;
-    for (uint64_t cp = p0; cp < p1; cp += (uint64_t)T * IPT) {
+    uint64_t r0 = pairs_find_global(offs, 0, nrows, p0);
+    int buf = 0;
+    for (uint64_t cp = p0; cp < p1; cp += (uint64_t)T * IPT, buf ^= 1) {
+        uint64_t* so = s_off + buf * (W + 1);
+        Meta* sm = s_meta + buf * W;
         const uint64_t cend = cp + (uint64_t)T * IPT < p1 ? cp + (uint64_t)T * IPT : p1;
         const uint32_t wn = (uint32_t)((nrows - r0) < (uint64_t)W ? (nrows - r0) : (uint64_t)W);
-        for (uint32_t i = tid; i <= wn; i += T) s_off[i] = offs(r0 + i);
+        for (uint32_t i = tid; i <= wn; i += T) {
+            const uint64_t a = offs(r0 + i);
+            so[i] = a;
+            if (i < wn && a < cend) {
+                const uint64_t b = offs(r0 + i + 1);
+                if (b > a) sm[i] = load_meta(r0 + i);
+            }
+        }
         __syncthreads();
-        const uint64_t wend = s_off[wn];
-        for (uint32_t i = tid; i < wn; i += T)
-            if (s_off[i] < cend && s_off[i + 1] > s_off[i]) s_meta[i] = load_meta(r0 + i);
-        __syncthreads();
+        const uint64_t wend = so[wn];
         bool v[IPT];
         Meta m[IPT];
         uint64_t j[IPT];
         const uint64_t pt = cp + (uint64_t)tid * IPT;
-        uint32_t i = (pt < cend && pt < wend) ? pairs_find_smem(s_off, wn, pt) : 0;
+        uint32_t i = (pt < cend && pt < wend) ? pairs_find_smem(so, wn, pt) : 0;
 #pragma unroll
         for (int it = 0; it < IPT; it++) {
             const uint64_t p = pt + it;
@@ -208,9 +217,9 @@ __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t n
             j[it] = 0;
             if (v[it]) {
                 if (p < wend) {
-                    while (s_off[i + 1] <= p) i++;
-                    m[it] = s_meta[i];
-                    j[it] = p - s_off[i];
+                    while (so[i + 1] <= p) i++;
+                    m[it] = sm[i];
+                    j[it] = p - so[i];
                 } else {
                     const uint64_t row = pairs_find_global(offs, r0 + wn, nrows, p);
                     m[it] = load_meta(row);
@@ -219,15 +228,10 @@ __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t n
             }
         }
         body(v, m, j);
-        __syncthreads();
-        if (cend < p1) {
-            if (tid == 0)
-                *s_row = (cend < wend) ? r0 + pairs_find_smem(s_off, wn, cend)
-                                       : pairs_find_global(offs, r0 + wn, nrows, cend);
-            __syncthreads();
-            r0 = *s_row;
-        }
+        if (cend < p1)
+            r0 = (cend < wend) ? r0 + pairs_find_smem(so, wn, cend) : pairs_find_global(offs, r0 + wn, nrows, cend);
     }
+    __syncthreads();   // the caller may reuse the shared buffers
 }
 
 // Per-key aggregation of a thread's IPT consecutive items (keys non-decreasing
