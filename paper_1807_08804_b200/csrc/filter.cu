@@ -145,10 +145,11 @@ struct ExMeta {             // one candidate row of an explore job, staged per c
 template <int MODE>   // 0: prune (mark satisfied constraints), 1: propagate
 __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
                                                  unsigned long long* bytes_acc) {
-    extern __shared__ uint64_t s_jp[];      // [nj+1] job pair prefix
-    __shared__ uint64_t s_off[2 * (kEW + 1)];
-    __shared__ ExMeta s_meta[2 * kEW];
-    __shared__ uint64_t s_row;
+    extern __shared__ __align__(16) char s_dyn[];
+    using SM = PairSmem<ExMeta, kEW, 2>;
+    uint64_t* s_jp = reinterpret_cast<uint64_t*>(s_dyn);          // [nj+1] job pair prefix
+    uint64_t* s_off = reinterpret_cast<uint64_t*>(s_dyn + SM::off_off(nj));
+    ExMeta* s_meta = reinterpret_cast<ExMeta*>(s_dyn + SM::meta_off(nj));
     job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].cnt); }, s_jp);
     uint64_t p0, p1;
     pairs_range(s_jp[nj], blockIdx.x, gridDim.x, p0, p1);
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
             m.skip = MODE == 0 ? ((mk & bitm) != 0) : (mk != full);
             return m;
         };
-        pair_chunks<ExMeta, kET, kEI, kEW>(lo, hi, (uint64_t)C, offs, load, s_meta, s_off, &s_row,
+        pair_chunks<ExMeta, kET, kEI, kEW, 2>(lo, hi, (uint64_t)C, offs, load, s_meta, s_off,
                                            [&](const bool (&v)[kEI], const ExMeta (&m)[kEI], const uint64_t (&j)[kEI]) {
             uint32_t arc[kEI];
             bool live[kEI];
@@ -221,14 +222,14 @@ __global__ void __launch_bounds__(256) k_clear(const ClearJob* __restrict__ jobs
     }
 }
 
-static size_t jp_smem(uint32_t nj) { return sizeof(uint64_t) * (nj + 1); }
+static size_t ex_smem(uint32_t nj) { return PairSmem<ExMeta, kEW, 2>::bytes(nj, 0); }
 
 void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, const ClearJob* d_clear,
                uint32_t nclear) {
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
     const uint32_t G = (uint32_t)c->nsm * 6;
-    launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), jp_smem(nj), k_explore<0>, g, d_jobs, nj,
+    launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), ex_smem(nj), k_explore<0>, g, d_jobs, nj,
            c->d_bytes + GPS_K_EXPLORE);
     launch(c, GPS_K_CLEAR, dim3(std::max<uint32_t>(1, (uint32_t)c->nsm * 2 / nclear + 1), nclear), dim3(256), 0,
            k_clear, d_clear);
@@ -238,7 +239,7 @@ void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
     const uint32_t G = (uint32_t)c->nsm * 6;
-    launch(c, GPS_K_PROPAGATE, dim3(G), dim3(kET), jp_smem(nj), k_explore<1>, g, d_jobs, nj,
+    launch(c, GPS_K_PROPAGATE, dim3(G), dim3(kET), ex_smem(nj), k_explore<1>, g, d_jobs, nj,
            c->d_bytes + GPS_K_PROPAGATE);
 }
 

@@ -23,9 +23,10 @@ namespace gps {
 
 constexpr int kPT = 256;    // threads per block
 constexpr int kPI = 4;      // pairs per thread per chunk
-constexpr int kPW = 512;    // rows of offsets staged in shared memory (double-buffered)
+constexpr int kPW = 512;    // EC: rows of offsets staged in shared memory (double-buffered)
+constexpr int kJW = 1024;   // join: rows staged (single buffer; fan-out can be 1)
+constexpr uint32_t kStageW = 8;   // join write: stage output rows of width <= 8 in shared memory
 
-static size_t jp_smem(uint32_t nj) { return sizeof(uint64_t) * (nj + 1); }
 
 // ------------------------------------------------------------ a6 EC build
 struct EcMeta {             // one key row of an EC job
@@ -35,10 +36,11 @@ struct EcMeta {             // one key row of an EC job
 template <bool WRITE>
 __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict__ jobs, uint32_t nj, PassCtl ctl,
                                            uint32_t* __restrict__ val, unsigned long long* bytes_acc) {
-    extern __shared__ uint64_t s_jp[];
-    __shared__ uint64_t s_off[2 * (kPW + 1)];
-    __shared__ EcMeta s_meta[2 * kPW];
-    __shared__ uint64_t s_row;
+    extern __shared__ __align__(16) char s_dyn[];
+    using SM = PairSmem<EcMeta, kPW, 2>;
+    uint64_t* s_jp = reinterpret_cast<uint64_t*>(s_dyn);
+    uint64_t* s_off = reinterpret_cast<uint64_t*>(s_dyn + SM::off_off(nj));
+    EcMeta* s_meta = reinterpret_cast<EcMeta*>(s_dyn + SM::meta_off(nj));
     job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].nkeys); }, s_jp);
     const uint64_t P = s_jp[nj];
     uint64_t p0, p1;
@@ -59,7 +61,7 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
             return m;
         };
         uint32_t jcount = 0;
-        pair_chunks<EcMeta, kPT, kPI, kPW>(lo, hi, (uint64_t)*J.nkeys, offs, load, s_meta, s_off, &s_row,
+        pair_chunks<EcMeta, kPT, kPI, kPW, 2>(lo, hi, (uint64_t)*J.nkeys, offs, load, s_meta, s_off,
                                            [&](const bool (&v)[kPI], const EcMeta (&m)[kPI], const uint64_t (&j)[kPI]) {
             uint32_t x[kPI], xp[kPI];
 #pragma unroll
@@ -109,15 +111,17 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
     if (bytes_acc && threadIdx.x == 0 && p1 > p0) atomicAdd(bytes_acc, (unsigned long long)(p1 - p0) * 4ull);
 }
 
+static size_t ec_smem_n(uint32_t nj) { return PairSmem<EcMeta, kPW, 2>::bytes(nj, 0); }
+
 void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, bool write, PassCtl ctl,
             uint32_t* val, uint32_t G) {
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many EC jobs per launch");
     if (write)
-        launch(c, GPS_K_EC_WRITE, dim3(G), dim3(kPT), jp_smem(nj), k_ec<true>, g, d_jobs, nj, ctl, val,
+        launch(c, GPS_K_EC_WRITE, dim3(G), dim3(kPT), ec_smem_n(nj), k_ec<true>, g, d_jobs, nj, ctl, val,
                c->d_bytes + GPS_K_EC_WRITE);
     else
-        launch(c, GPS_K_EC_COUNT, dim3(G), dim3(kPT), jp_smem(nj), k_ec<false>, g, d_jobs, nj, ctl, val,
+        launch(c, GPS_K_EC_COUNT, dim3(G), dim3(kPT), ec_smem_n(nj), k_ec<false>, g, d_jobs, nj, ctl, val,
                c->d_bytes + GPS_K_EC_COUNT);
 }
 
@@ -216,10 +220,13 @@ struct JMeta {              // one input row of a join step
 
 template <bool WRITE>
 __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a) {
-    extern __shared__ uint64_t s_jr[];   // [nj+1] first row of every job
-    __shared__ uint64_t s_off[2 * (kPW + 1)];
-    __shared__ JMeta s_meta[2 * kPW];
-    __shared__ uint64_t s_row;
+    extern __shared__ __align__(16) char s_dyn[];
+    using SM = PairSmem<JMeta, kJW, 1>;
+    uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);      // [nj+1] first row of every job
+    uint64_t* s_off = reinterpret_cast<uint64_t*>(s_dyn + SM::off_off(a.nj));
+    JMeta* s_meta = reinterpret_cast<JMeta*>(s_dyn + SM::meta_off(a.nj));
+    uint32_t* s_out = reinterpret_cast<uint32_t*>(s_dyn + SM::extra_off(a.nj));   // staged output tile
+    const bool stage = WRITE && a.wout <= kStageW;
     for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
     if (threadIdx.x == 0) s_jr[a.nj] = a.R;
     __syncthreads();
@@ -237,8 +244,8 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
     pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
     uint64_t running = WRITE ? a.ctl.blk[blockIdx.x] : 0ull;
     uint64_t count = 0;
-    pair_chunks<JMeta, kPT, kPI, kPW>(p0, p1, a.R, offs, load, s_meta, s_off, &s_row,
-                                      [&](const bool (&v)[kPI], const JMeta (&m)[kPI], const uint64_t (&j)[kPI]) {
+    pair_chunks<JMeta, kPT, kPI, kJW, 1>(p0, p1, a.R, offs, load, s_meta, s_off,
+                                         [&](const bool (&v)[kPI], const JMeta (&m)[kPI], const uint64_t (&j)[kPI]) {
         uint32_t cand[kPI];
 #pragma unroll
         for (int it = 0; it < kPI; it++) cand[it] = v[it] ? __ldg(a.ec_val + m[it].s0 + j[it]) : 0u;
@@ -258,13 +265,15 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
 #pragma unroll
             for (int it = 0; it < kPI; it++) mine += writes[it] ? 1u : 0u;
             uint32_t tot;
-            uint64_t pos = running + block_excl_scan(mine, &tot);
+            const uint32_t ex = block_excl_scan(mine, &tot);
+            uint64_t pos = running + ex;   // global output row
+            uint32_t lpos = ex;            // row within the block's tile
 #pragma unroll
             for (int it = 0; it < kPI; it++) {
                 if (!writes[it]) continue;
                 const JoinJob& J = a.jobs[m[it].job];
                 const uint32_t* row = m[it].rowp;
-                uint32_t* dst = a.out + (pos++) * a.wout;
+                uint32_t* dst = stage ? s_out + (size_t)(lpos++) * a.wout : a.out + (pos++) * a.wout;
                 if (J.final_) {
                     for (uint32_t c = 0; c < a.w; c++) dst[J.perm[c]] = __ldg(row + c);
                     dst[J.perm[a.w]] = cand[it];
@@ -272,6 +281,13 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
                     for (uint32_t c = 0; c < a.w; c++) dst[c] = __ldg(row + c);
                     dst[a.w] = cand[it];
                 }
+            }
+            if (stage) {
+                // the block's rows are contiguous in the output: coalesced copy of the tile
+                __syncthreads();
+                uint32_t* g = a.out + running * a.wout;
+                const uint32_t words = tot * a.wout;
+                for (uint32_t x = threadIdx.x; x < words; x += blockDim.x) g[x] = s_out[x];
             }
             running += tot;
         } else {
@@ -290,11 +306,24 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
     if (!WRITE) last_block_scan(a.ctl.blk, gridDim.x, a.ctl.done, a.ctl.info, P, count);
 }
 
+static size_t join_smem(uint32_t nj, bool write) {
+    return PairSmem<JMeta, kJW, 1>::bytes(nj, write ? sizeof(uint32_t) * kPT * kPI * kStageW : 0);
+}
+
+template <typename K>
+static void allow_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024) GPS_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G) {
-    launch(c, GPS_K_JOIN_COUNT, dim3(G), dim3(kPT), jp_smem(s.nj), k_join<false>, s);
+    const size_t sm = join_smem(s.nj, false);
+    allow_smem(k_join<false>, sm);
+    launch(c, GPS_K_JOIN_COUNT, dim3(G), dim3(kPT), sm, k_join<false>, s);
 }
 void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G) {
-    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), jp_smem(s.nj), k_join<true>, s);
+    const size_t sm = join_smem(s.nj, true);
+    allow_smem(k_join<true>, sm);
+    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), sm, k_join<true>, s);
 }
 
 }  // namespace gps

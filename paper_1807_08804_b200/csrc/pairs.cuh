@@ -179,18 +179,17 @@ namespace gps {
 // across the threads of the block), so it can issue their global loads back to
 // back and aggregate per row.  Rows outside the window (runs of empty rows) fall
 // back to load_meta from global.  body may use block-wide barriers.
-template <typename Meta, int T, int IPT, int W, typename OffF, typename LoadMeta, typename Body>
+template <typename Meta, int T, int IPT, int W, int NB, typename OffF, typename LoadMeta, typename Body>
 __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t nrows, OffF offs, LoadMeta load_meta,
-                                            Meta* s_meta, uint64_t* s_off, uint64_t* s_row, Body&& body) {
-    // s_off holds 2*(W+1) and s_meta 2*W entries: the window is double-buffered, so a
-    // chunk needs ONE block barrier (between staging and use); the row of the next
-    // chunk is recomputed by every thread from the current window (no broadcast).
-    (void)s_row;
+                                            Meta* s_meta, uint64_t* s_off, Body&& body) {
+    // s_off holds NB*(W+1) and s_meta NB*W entries.  NB = 2 double-buffers the
+    // window, so a chunk needs ONE block barrier (between staging and use); the row
+    // of the next chunk is recomputed by every thread from the current window.
     if (p0 >= p1) return;
     const uint32_t tid = threadIdx.x;
     uint64_t r0 = pairs_find_global(offs, 0, nrows, p0);
     int buf = 0;
-    for (uint64_t cp = p0; cp < p1; cp += (uint64_t)T * IPT, buf ^= 1) {
+    for (uint64_t cp = p0; cp < p1; cp += (uint64_t)T * IPT, buf = (NB == 2) ? buf ^ 1 : 0) {
         uint64_t* so = s_off + buf * (W + 1);
         Meta* sm = s_meta + buf * W;
         const uint64_t cend = cp + (uint64_t)T * IPT < p1 ? cp + (uint64_t)T * IPT : p1;
@@ -230,9 +229,21 @@ __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t n
         body(v, m, j);
         if (cend < p1)
             r0 = (cend < wend) ? r0 + pairs_find_smem(so, wn, cend) : pairs_find_global(offs, r0 + wn, nrows, cend);
+        if (NB == 1) __syncthreads();   // the single window is restaged next
     }
-    __syncthreads();   // the caller may reuse the shared buffers
+    if (NB == 2) __syncthreads();   // the caller may reuse the shared buffers
 }
+
+// Dynamic shared memory of a pair kernel: [job prefix (nj+1)] [offset window
+// NB*(W+1)] [row metadata NB*W] [extra].
+template <typename Meta, int W, int NB>
+struct PairSmem {
+    static __host__ __device__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+    static __host__ __device__ size_t off_off(uint32_t nj) { return a16(sizeof(uint64_t) * (nj + 1)); }
+    static __host__ __device__ size_t meta_off(uint32_t nj) { return off_off(nj) + a16(sizeof(uint64_t) * NB * (W + 1)); }
+    static __host__ __device__ size_t extra_off(uint32_t nj) { return meta_off(nj) + a16(sizeof(Meta) * NB * W); }
+    static __host__ __device__ size_t bytes(uint32_t nj, size_t extra) { return extra_off(nj) + extra; }
+};
 
 // Per-key aggregation of a thread's IPT consecutive items (keys non-decreasing
 // across items and lanes): runs wholly inside the thread are emitted directly;
