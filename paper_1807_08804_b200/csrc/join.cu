@@ -15,6 +15,8 @@
 //                injectivity + every fused closing arc (binary search in the closing arc's
 //                sorted EC segment); count (W=false, last block scans the block counts)
 //                or write (W=true).
+#include <mutex>
+
 #include "kernels.cuh"
 #include "lookback.cuh"
 #include "pairs.cuh"
@@ -310,20 +312,26 @@ static size_t join_smem(uint32_t nj, bool write) {
     return PairSmem<JMeta, kJW, 1>::bytes(nj, write ? sizeof(uint32_t) * kPT * kPI * kStageW : 0);
 }
 
-template <typename K>
-static void allow_smem(K kernel, size_t bytes) {
-    if (bytes > 48 * 1024) GPS_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+// Opt the join kernels in to their largest dynamic shared memory ONCE (the
+// attribute is per function; setting it per launch would race between the
+// batch worker threads).
+static void allow_join_smem() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        GPS_CK(cudaFuncSetAttribute(k_join<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)join_smem(kMaxJobsPerLaunch, false)));
+        GPS_CK(cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)join_smem(kMaxJobsPerLaunch, true)));
+    });
 }
 
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G) {
-    const size_t sm = join_smem(s.nj, false);
-    allow_smem(k_join<false>, sm);
-    launch(c, GPS_K_JOIN_COUNT, dim3(G), dim3(kPT), sm, k_join<false>, s);
+    allow_join_smem();
+    launch(c, GPS_K_JOIN_COUNT, dim3(G), dim3(kPT), join_smem(s.nj, false), k_join<false>, s);
 }
 void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G) {
-    const size_t sm = join_smem(s.nj, true);
-    allow_smem(k_join<true>, sm);
-    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), sm, k_join<true>, s);
+    allow_join_smem();
+    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), join_smem(s.nj, true), k_join<true>, s);
 }
 
 }  // namespace gps
