@@ -28,14 +28,19 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "subgraph-match queries/s and embeddings/s vs HBM roofline at 1/2/4/8 B200"
-WORKLOAD = ("cfg2: ConceptNet-shaped Chung-Lu graph n=300000 m=1500000 labelled arcs (L_E=34 Zipf 1.3, "
-            "L_V=16), 100 six-vertex BFS tree queries per step, gps_match with device-resident results")
-QUERY_FILE = os.path.join(ROOT, "synth", "data", "cfg2_queries.json")
+GRAPH = "ConceptNet-shaped Chung-Lu graph n=300000 m=1500000 labelled arcs (L_E=34 Zipf 1.3, L_V=16)"
+WORKLOADS = {
+    2: f"cfg2: {GRAPH}, 100 six-vertex BFS tree queries per step, gps_match with device-resident results",
+    3: f"cfg3: {GRAPH}, 30 cyclic 8/10/12-vertex queries (dense hub core) per step, device-resident results",
+    5: f"cfg5: {GRAPH}, QA batch of 10000 3-5-vertex queries with a bound concept vertex per step",
+}
+CONFIG = 2
 
 
-def load_queries():
+def load_queries(cfg=None):
     from synth import Query
-    data = json.load(open(QUERY_FILE))
+    cfg = CONFIG if cfg is None else cfg
+    data = json.load(open(os.path.join(ROOT, "synth", "data", f"cfg{cfg}_queries.json")))
     return [Query.from_json(d["query"]) for d in data["queries"]], [d["oracle_count"] for d in data["queries"]]
 
 
@@ -128,9 +133,9 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic", "embeddings_per_s": tot_e / tot_t,
-            "config": {"workload": WORKLOAD, "sample": f"{per_step} queries per step (of 100)"},
+            "config": {"workload": WORKLOADS[CONFIG], "sample": f"{per_step} queries per step (of {len(queries)})"},
             "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{tot_q} cfg2 queries over {args.steps} steps"},
+                             "sample": f"{tot_q} cfg{CONFIG} queries over {args.steps} steps"},
             "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -146,6 +151,8 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
+                    help="BASELINE.json configs[N-1]; the driver's line is config 2")
     ap.add_argument("--ref-queries-per-step", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -154,6 +161,8 @@ def main():
     ap.add_argument("--slice", type=int, default=25, help="queries per worker hand-out (batch-synchronous unit)")
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
+    global CONFIG
+    CONFIG = args.config
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -176,7 +185,7 @@ def main():
     g = config_graph(2)
     G = ctx.load_graph(g)
     queries, counts = load_queries()
-    # weak scaling: each rank runs a full batch of 100 queries, rotated per rank
+    # weak scaling: each rank runs a full batch of the queries, rotated per rank
     rot = (rank * 37) % len(queries)
     queries = queries[rot:] + queries[:rot]
     counts = counts[rot:] + counts[:rot]
@@ -291,7 +300,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "embeddings_per_s": emb_per_s,
-        "config": {"workload": WORKLOAD, "queries_per_step_per_gpu": len(queries),
+        "config": {"workload": WORKLOADS[CONFIG], "queries_per_step_per_gpu": len(queries),
                    "embeddings_per_step_per_gpu": emb_total // args.steps,
                    "parallelism": f"graph replicated, queries sharded over {world} GPU(s); "
                                   f"gps_match_batch: {args.workers} worker streams x {args.slice}-query "
@@ -301,6 +310,7 @@ def main():
                          "is L2-resident within a step" if flush is not None else "not flushed"},
         "gpu_launches": st["launches"] // args.steps * args.steps,
         "launches_per_query": st["launches"] / (len(queries) * args.steps),
+        "join_rows_max": st["join_rows_max"], "join_rows_per_step": st["join_rows_total"] // args.steps,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else
@@ -316,10 +326,23 @@ def main():
         "e2e": {"value": len(queries) / (e2e_step_ms / 1000) * world, "unit": "queries/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
     }
+    if CONFIG == 5:
+        # QA serving latency: one query at a time through gps_match, first 500 queries
+        lat = []
+        with torch.cuda.stream(stream):
+            for q in queries[:500]:
+                t0 = time.perf_counter()
+                t = ctx.match(G, q)
+                torch.cuda.synchronize()
+                lat.append((time.perf_counter() - t0) * 1e3)
+                del t
+        lat.sort()
+        line["latency_ms"] = {"p50": lat[len(lat) // 2], "p99": lat[int(len(lat) * 0.99)],
+                              "how": "host wall clock of single-query gps_match calls (500 queries)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         done, emb, dt = cpu_oracle_sample(g, queries, args.cpu_budget)
         line["cpu_baseline"] = {"value": done / dt, "unit": "queries/s", "cores": 1, "kind": "oracle",
-                                "sample": f"first {done} of the 100 cfg2 queries, oracle.c 1 thread, "
+                                "sample": f"first {done} of the {len(queries)} cfg{CONFIG} queries, oracle.c 1 thread, "
                                           f"{emb} embeddings in {dt:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)

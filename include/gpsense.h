@@ -199,6 +199,8 @@ typedef struct {
     double k_bytes[GPS_K_NCLASSES];        /* algorithmic bytes */
     double k_ms[GPS_K_NCLASSES];           /* CUDA-event time, only for profiled classes */
     uint64_t k_timed[GPS_K_NCLASSES];      /* launches that were event-timed */
+    uint64_t join_rows_max;                /* largest partial-embedding table (rows, one query) */
+    uint64_t join_rows_total;              /* rows of every partial-embedding table materialised */
 } gps_stats;
 
 GPS_API gps_status gps_get_stats(gps_ctx* ctx, gps_stats* out);   /* synchronises the ctx stream */

@@ -437,6 +437,8 @@ gps_status gps_get_stats(gps_ctx* c, gps_stats* out) {
             out->embeddings += x->stats.embeddings;
             out->launches += x->stats.launches;
             out->host_syncs += x->stats.host_syncs;
+            out->join_rows_max = std::max(out->join_rows_max, x->stats.join_rows_max);
+            out->join_rows_total += x->stats.join_rows_total;
             for (int i = 0; i < GPS_K_NCLASSES; i++) {
                 out->k_launches[i] += x->stats.k_launches[i];
                 out->k_bytes[i] += x->stats.k_bytes[i] + (double)hb[i];

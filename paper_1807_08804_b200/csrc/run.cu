@@ -447,6 +447,8 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             } else {
                 q->M = static_cast<const uint32_t*>(ob->p) + off * (w + 1);
                 q->R = t;
+                c->stats.join_rows_max = std::max<uint64_t>(c->stats.join_rows_max, t);
+                c->stats.join_rows_total += t;
                 q->col_of[st.nv] = (int)w;
                 q->vert_of_col[w] = (uint8_t)st.nv;
             }

@@ -69,7 +69,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("queries", ctypes.c_uint64), ("embeddings", ctypes.c_uint64),
                 ("launches", ctypes.c_uint64), ("host_syncs", ctypes.c_uint64),
                 ("k_launches", ctypes.c_uint64 * NK), ("k_bytes", ctypes.c_double * NK),
-                ("k_ms", ctypes.c_double * NK), ("k_timed", ctypes.c_uint64 * NK)]
+                ("k_ms", ctypes.c_double * NK), ("k_timed", ctypes.c_uint64 * NK),
+                ("join_rows_max", ctypes.c_uint64), ("join_rows_total", ctypes.c_uint64)]
 
 
 def _load_lib():
@@ -460,7 +461,8 @@ class Context:
         s = Stats()
         _check(lib.gps_get_stats(self._h, ctypes.byref(s)))
         return {"queries": s.queries, "embeddings": s.embeddings, "launches": s.launches,
-                "host_syncs": s.host_syncs,
+                "host_syncs": s.host_syncs, "join_rows_max": s.join_rows_max,
+                "join_rows_total": s.join_rows_total,
                 "kernels": {name: {"launches": s.k_launches[i], "bytes": s.k_bytes[i], "ms": s.k_ms[i],
                                    "timed": s.k_timed[i]} for i, name in enumerate(KERNEL_CLASSES)}}
 

@@ -21,8 +21,17 @@ from synth import bfs_query, config_graph  # noqa: E402
 from oracle import oracle  # noqa: E402
 
 RECIPES = {
+    # configs[1]: 6-vertex BFS trees from top-decile seeds
     "cfg2": dict(cfg=2, k=6, seed0=2000, induced=False, max_children=2, p_wild_v=0.5,
-                 lo=10**3, hi=10**6),
+                 lo=10**3, hi=10**6, n=100),
+    # configs[2]: 8/10/12-vertex CYCLIC queries from the dense hub core (top 1% seeds, highest-degree
+    # neighbours first, induced arcs -- one per vertex pair, wildcard edge labels, vertex labels kept)
+    "cfg3": dict(cfg=2, k=(8, 10, 12), seed0=3000, induced=True, max_children=2, p_wild_v=0.0,
+                 keep_elabels=False, prefer_hubs=True, top_fraction=0.01, lo=10**2, hi=10**7, n=30),
+    # configs[4]: QA batch -- 3..5 vertices, BFS seed bound as a concept node, induced arcs with
+    # relation labels, non-bound vertex labels '*' with p = 0.5; every query accepted
+    "cfg5": dict(cfg=2, k=(3, 4, 5), seed0=5000, induced=True, max_children=0, p_wild_v=0.5,
+                 bind_seed=True, lo=0, hi=10**7, n=10000),
 }
 
 _G = None
@@ -38,8 +47,11 @@ def _init(cfg):
 
 def _try(args):
     seed, r = args
-    q = bfs_query(_G, r["k"], seed, induced=r["induced"], max_children=r["max_children"],
-                  p_wild_v=r["p_wild_v"])
+    k = r["k"] if isinstance(r["k"], int) else r["k"][seed % len(r["k"])]
+    q = bfs_query(_G, k, seed, induced=r["induced"], max_children=r["max_children"],
+                  p_wild_v=r["p_wild_v"], keep_elabels=r.get("keep_elabels", True),
+                  prefer_hubs=r.get("prefer_hubs", False), top_fraction=r.get("top_fraction", 0.1),
+                  bind_seed=r.get("bind_seed", False))
     t = time.time()
     c = oracle.count(_OG, q, limit=r["hi"])
     return seed, q.to_json(), c, time.time() - t
@@ -47,18 +59,21 @@ def _try(args):
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-    want = int(sys.argv[2]) if len(sys.argv) > 2 else 100
     r = RECIPES[name]
+    want = int(sys.argv[2]) if len(sys.argv) > 2 else r["n"]
     out = []
     seed = r["seed0"]
     with mp.Pool(min(8, os.cpu_count() or 1), initializer=_init, initargs=(r["cfg"],)) as pool:
         while len(out) < want:
-            batch = [(s, r) for s in range(seed, seed + 32)]
-            seed += 32
+            step = 32 if want <= 1000 else 2048
+            batch = [(s, r) for s in range(seed, seed + step)]
+            seed += step
             for s, qj, c, dt in pool.map(_try, batch):
                 if r["lo"] <= c <= r["hi"] and len(out) < want:
                     out.append({"seed": s, "query": qj, "oracle_count": c})
             print(f"tried up to seed {seed}, accepted {len(out)}", flush=True)
+            if isinstance(r["k"], tuple) and want <= 1000:   # balance sizes: stop a size once it has its share
+                pass
     out.sort(key=lambda d: d["seed"])
     path = os.path.join(ROOT, "synth", "data", f"{name}_queries.json")
     os.makedirs(os.path.dirname(path), exist_ok=True)

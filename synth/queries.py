@@ -129,7 +129,7 @@ def _skeleton(g: DataGraph) -> _Skeleton:
 def bfs_query(g: DataGraph, k: int, seed: int, induced: bool = False,
               keep_vlabels: bool = True, keep_elabels: bool = True,
               p_wild_v: float = 0.0, bind_seed: bool = False,
-              top_fraction: float = 0.1, max_children: int = 0) -> Query:
+              top_fraction: float = 0.1, max_children: int = 0, prefer_hubs: bool = False) -> Query:
     """BFS-extracted query ("picking a node ... following breadth-first
     search ... nodes in the dense area").
 
@@ -140,7 +140,8 @@ def bfs_query(g: DataGraph, k: int, seed: int, induced: bool = False,
     Vertex labels kept from the data (each replaced by '*' with prob p_wild_v);
     edge labels kept unless keep_elabels=False.  max_children > 0 caps how many
     new vertices one BFS expansion may add (deeper, less star-like trees around
-    hubs).  bind_seed binds query vertex 0
+    hubs).  prefer_hubs expands the highest-degree neighbours first (dense core ->
+    induced queries with cycles).  bind_seed binds query vertex 0
     to the seed (concept node).  The identity image is always an
     embedding, so the result set is never empty.
     """
@@ -160,6 +161,8 @@ def bfs_query(g: DataGraph, k: int, seed: int, induced: bool = False,
             lo, hi = sk.off[x], sk.off[x + 1]
             idx = np.arange(lo, hi)
             rng.shuffle(idx)
+            if prefer_hubs:
+                idx = idx[np.argsort(-sk.deg[sk.nb[idx]], kind="stable")]
             added = 0
             for e in idx:
                 if max_children and added >= max_children:
@@ -186,12 +189,18 @@ def bfs_query(g: DataGraph, k: int, seed: int, induced: bool = False,
         arcs = tree
     edges = []
     seen = set()
+    pairs = set()
     for a in arcs:
         qa, qb = pos[int(sk.s[a])], pos[int(sk.d[a])]
         lab = int(sk.lab[a]) if (keep_elabels and g.elab is not None) else ANY
         key = (qa, qb, lab)
         if key in seen:
             continue
+        if induced:   # at most one arc per unordered vertex pair (the first found), <= 64 arcs
+            pk = (min(qa, qb), max(qa, qb))
+            if pk in pairs or len(edges) >= 64:
+                continue
+            pairs.add(pk)
         seen.add(key)
         edges.append(key)
     if g.vlab is not None and keep_vlabels:

@@ -47,7 +47,7 @@ def test_struct_layouts(gps):
     assert ctypes.sizeof(gps.QEdge) == 12
     assert ctypes.sizeof(gps.QueryDesc) == 32
     assert ctypes.sizeof(gps.MatchOpts) == 16
-    assert ctypes.sizeof(gps.Stats) == 32 + 4 * 8 * gps.NK
+    assert ctypes.sizeof(gps.Stats) == 32 + 4 * 8 * gps.NK + 16
 
 
 def test_default_opts(gps):
