@@ -25,9 +25,11 @@
 namespace gps {
 
 // ---------------------------------------------------------------- a2 check
-__global__ void __launch_bounds__(256) k_check(DevGraph g, const QDesc* __restrict__ qs) {
-    const QDesc& q = qs[blockIdx.y];
-    const int k = q.k;
+// One warp per bitmap word (32 data vertices): the vertex data (label, out/in
+// degree) is read ONCE into registers and tested against every query vertex of
+// every query of the launch (one __ballot_sync per query vertex), so a batch of
+// queries streams vlab / off_out / off_in once instead of once per query.
+__global__ void __launch_bounds__(256) k_check(DevGraph g, const QDesc* __restrict__ qs, uint32_t nq) {
     const uint32_t lane = lane_id();
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < g.nw; w += nwarps) {
@@ -39,22 +41,29 @@ __global__ void __launch_bounds__(256) k_check(DevGraph g, const QDesc* __restri
             od = g.off_out[v + 1] - g.off_out[v];
             id = g.off_in[v + 1] - g.off_in[v];
         }
-        uint32_t mine = 0;
-        for (int u = 0; u < k; u++) {
-            bool p = valid && (q.lab[u] < 0 || lab == (uint32_t)q.lab[u]) &&
-                     (q.bound[u] < 0 || (int64_t)v == q.bound[u]) && od >= q.qout[u] && id >= q.qin[u];
-            uint32_t m = __ballot_sync(kFull, p);
-            if ((int)lane == u) mine = m;
+        for (uint32_t qi = 0; qi < nq; qi++) {
+            const QDesc& q = qs[qi];
+            const int k = q.k;
+            uint32_t mine = 0;
+            for (int u = 0; u < k; u++) {
+                const int32_t ql = __ldg(&q.lab[u]);
+                const int64_t qb = __ldg(&q.bound[u]);
+                bool p = valid && (ql < 0 || lab == (uint32_t)ql) && (qb < 0 || (int64_t)v == qb) &&
+                         od >= __ldg(&q.qout[u]) && id >= __ldg(&q.qin[u]);
+                uint32_t m = __ballot_sync(kFull, p);
+                if ((int)lane == u) mine = m;
+            }
+            if ((int)lane < k) q.B[(size_t)lane * g.nws + w] = mine;
         }
-        if ((int)lane < k) q.B[(size_t)lane * g.nws + w] = mine;
     }
 }
 
 void run_check(gps_ctx* c, const DevGraph& g, const QDesc* d_q, uint32_t nq, uint32_t max_k) {
     if (nq == 0) return;
-    uint32_t blocks = std::min<uint32_t>((g.nw + 7) / 8, std::max<uint32_t>(1, (uint32_t)c->nsm * 8 / nq + 1));
-    launch(c, GPS_K_CHECK, dim3(blocks, nq), dim3(256), 0, k_check, g, d_q);
-    c->stats.k_bytes[GPS_K_CHECK] += (double)nq * ((double)g.n * 10.0 + (double)max_k * g.nw * 4.0);
+    uint32_t blocks = std::min<uint32_t>((g.nw + 7) / 8, (uint32_t)c->nsm * 8);
+    launch(c, GPS_K_CHECK, dim3(blocks), dim3(256), 0, k_check, g, d_q, nq);
+    // algorithmic: the vertex data once + k/8 bytes of bitmap per vertex and query
+    c->stats.k_bytes[GPS_K_CHECK] += (double)g.n * 10.0 + (double)nq * max_k * g.nw * 4.0;
 }
 
 // -------------------------------------------------------------- a3 collect
