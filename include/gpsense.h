@@ -70,8 +70,9 @@ typedef struct {
     int device;              /* CUDA ordinal */
     void* stream;            /* cudaStream_t to run on (e.g. torch.cuda.current_stream().cuda_stream);
                                 NULL = the library creates its own non-blocking stream */
-    void* nccl_comm;         /* reserved (row-sharded join); must be NULL */
-    int rank, world;         /* reserved; world <= 1 */
+    void* nccl_comm;         /* ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()) for the row-sharded
+                                join; NULL / world <= 1 = single GPU */
+    int rank, world;         /* this process's rank and the number of ranks of nccl_comm */
 } gps_ctx_opts;
 
 /* Data graph as CSR ("nodes array ... edges array ... two additional
@@ -115,6 +116,8 @@ typedef struct {
     int32_t reverse_refine;      /* refine in reversed visit order; default 1 */
     uint32_t lowconn_threshold;  /* query degree <= this is "low connectivity"; default 1 */
     int32_t result_on_device;    /* gps_match: 1 = rows stay in device memory (default), 0 = host copy */
+    float rebalance_threshold;   /* row-sharded join: exchange rows when max/mean pairs per rank exceeds
+                                    this (default 1.10; 0 = always, very large = never) */
 } gps_match_opts;
 
 GPS_API gps_status gps_default_opts(gps_match_opts* opts);
@@ -173,6 +176,24 @@ GPS_API gps_status gps_set_workers(gps_ctx* ctx, uint32_t n);
 /* Queries per worker hand-out in the batch calls (each hand-out runs batch-synchronously:
  * one launch per phase for all its queries); 0 = default 64. */
 GPS_API gps_status gps_set_slice(gps_ctx* ctx, uint32_t queries);
+
+/* ---- multi-GPU (row-sharded join, SPMD) ------------------------------------
+ * With a ctx of world > 1 every rank calls gps_match / gps_count with the same
+ * graph and query (batches run one query at a time).  Filtering and edge
+ * candidates are computed on every rank (replicated); the join's pair space is
+ * split across ranks, the per-step counts are all-gathered and partial
+ * embeddings are exchanged when the load is unbalanced.  gps_count returns the
+ * GLOBAL count on every rank; gps_match returns this rank's shard (shards in rank
+ * order = the global result); gps_result_global_rows gives the global size. */
+GPS_API gps_status gps_result_global_rows(const gps_result* r, uint64_t* global_rows);
+
+/* In-process ranks on one device (threads sharing a hub): the same sharded path
+ * with device-to-device copies instead of NCCL -- used to test sharding and
+ * rebalancing with several ranks on one GPU. */
+typedef struct gps_local_comm gps_local_comm;
+GPS_API gps_status gps_local_comm_create(int world, gps_local_comm** out);
+GPS_API gps_status gps_local_comm_destroy(gps_local_comm* comm);
+GPS_API gps_status gps_create_local_rank(const gps_ctx_opts* opts, gps_local_comm* comm, int rank, gps_ctx** out);
 
 /* rows, cols (= k), data (device or host pointer, owned by the result), on_device. */
 GPS_API gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols,

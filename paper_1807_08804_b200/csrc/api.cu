@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "kernels.cuh"
 #include "planner.h"
 #include "runtime.h"
@@ -58,6 +59,7 @@ static gps_result* wrap_result(gps_ctx* c, QueryResult& qr, bool on_device) {
     r->rows = qr.rows;
     r->cols = qr.cols;
     r->ctx = c;
+    r->global_rows = qr.global_rows;
     const size_t bytes = sizeof(uint32_t) * qr.rows * qr.cols;
     if (on_device) {
         r->on_device = 1;
@@ -107,6 +109,10 @@ static void drop_workers(gps_ctx* c) {
 // each worker runs its slice batch-synchronously on its own stream
 // (run_queries).  body(worker ctx, first query, count) fills the outputs.
 static void run_sliced(gps_ctx* c, uint32_t nq, const std::function<void(gps_ctx*, uint32_t, uint32_t)>& body) {
+    if (c->comm && c->comm->world > 1) {   // SPMD ranks: every rank walks the batch in the same order
+        body(c, 0, nq);
+        return;
+    }
     ensure_workers(c);
     const uint32_t W = (uint32_t)c->workers.size();
     cudaEvent_t start;
@@ -165,6 +171,7 @@ gps_status gps_default_opts(gps_match_opts* o) {
     o->reverse_refine = 1;
     o->lowconn_threshold = 1;
     o->result_on_device = 1;
+    o->rebalance_threshold = 1.10f;
     return GPS_OK;
 }
 
@@ -174,7 +181,8 @@ gps_status gps_create(const gps_ctx_opts* opts, gps_ctx** out) {
     return guarded([&] {
         if (!out) fail(GPS_EINVAL, "null out");
         int dev = opts ? opts->device : 0;
-        if (opts && (opts->nccl_comm || opts->world > 1)) fail(GPS_EUNSUPPORTED, "row-sharded join not built yet");
+        if (opts && opts->world > 1 && (opts->rank < 0 || opts->rank >= opts->world || !opts->nccl_comm))
+            fail(GPS_EINVAL, "world > 1 needs an nccl_comm and 0 <= rank < world");
         int ndev = 0;
         GPS_CK(cudaGetDeviceCount(&ndev));
         if (dev < 0 || dev >= ndev) fail(GPS_EINVAL, "bad device ordinal");
@@ -182,6 +190,7 @@ gps_status gps_create(const gps_ctx_opts* opts, gps_ctx** out) {
         gps_ctx* c = new gps_ctx();
         try {
             ctx_init(c, dev, opts ? (cudaStream_t)opts->stream : nullptr);
+            if (opts && opts->world > 1) c->comm = make_nccl_comm(opts->nccl_comm, opts->rank, opts->world);
         } catch (...) {
             delete c;
             throw;
@@ -196,7 +205,43 @@ gps_status gps_destroy(gps_ctx* c) {
         DeviceGuard dg(c->device);
         drop_workers(c);
         ctx_release(c);
+        delete c->comm;
         delete c;
+    });
+}
+
+gps_status gps_result_global_rows(const gps_result* r, uint64_t* g) {
+    if (!r || !g) return GPS_EINVAL;
+    *g = r->global_rows;
+    return GPS_OK;
+}
+
+gps_status gps_local_comm_create(int world, gps_local_comm** out) {
+    return guarded([&] {
+        if (world < 1 || !out) fail(GPS_EINVAL, "world >= 1 and out required");
+        *out = new gps_local_comm(world);
+    });
+}
+
+gps_status gps_local_comm_destroy(gps_local_comm* comm) {
+    delete comm;
+    return GPS_OK;
+}
+
+gps_status gps_create_local_rank(const gps_ctx_opts* opts, gps_local_comm* comm, int rank, gps_ctx** out) {
+    return guarded([&] {
+        if (!comm || !out || rank < 0 || rank >= comm->hub.world) fail(GPS_EINVAL, "bad local rank");
+        int dev = opts ? opts->device : 0;
+        DeviceGuard dg(dev);
+        gps_ctx* c = new gps_ctx();
+        try {
+            ctx_init(c, dev, opts ? (cudaStream_t)opts->stream : nullptr);
+            c->comm = make_local_comm(&comm->hub, rank);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
     });
 }
 
@@ -303,7 +348,7 @@ gps_status gps_count(gps_ctx* c, const gps_graph* g, const gps_query* q, const g
         run_queries(c, g, q, 1, o, true, qr);
         ctx_sync(c);
         if (qr[0].status != GPS_OK) fail(qr[0].status, qr[0].error);
-        *count = qr[0].rows;
+        *count = qr[0].global_rows;   // = rows on one GPU; the sum over ranks when sharded
     });
 }
 
@@ -387,7 +432,7 @@ gps_status gps_count_batch(gps_ctx* c, const gps_graph* g, const gps_query* qs, 
             ctx_sync(sc);
             for (uint32_t i = 0; i < cnt; i++) {
                 st[lo + i] = qr[i].status;
-                counts[lo + i] = qr[i].rows;
+                counts[lo + i] = qr[i].global_rows;
             }
         });
         gps_status first = GPS_OK;

@@ -13,6 +13,7 @@
 
 namespace gps {
 struct WorkerPool;
+struct Comm;
 }
 
 namespace gps {
@@ -94,6 +95,7 @@ struct gps_ctx {
     gps::WorkerPool* pool = nullptr;
     uint32_t nworkers_req = 0;               // 0 = default (2)
     uint32_t slice = 0;                      // queries per worker hand-out (0 = default 64)
+    gps::Comm* comm = nullptr;               // row-sharded join across ranks (world > 1)
 };
 
 struct gps_graph {
@@ -124,6 +126,7 @@ struct gps_result {
     int on_device = 0;
     gps_ctx* ctx = nullptr;       // owner (device rows / pinned host rows)
     gps::Block hold;              // device rows live in this block
+    uint64_t global_rows = 0;     // rows over all ranks (row-sharded join); = rows otherwise
     size_t host_bytes = 0;        // pinned host buffer size (on_device == 0)
 };
 

@@ -241,9 +241,12 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
         m.s0 = __ldg(a.s0 + r);
         return m;
     };
-    const uint64_t P = offs(a.R);
+    const uint64_t plo = a.plo, phi = a.phi == ~0ull ? offs(a.R) : a.phi;
+    const uint64_t P = phi > plo ? phi - plo : 0;
     uint64_t p0, p1;
     pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
+    p0 += plo;
+    p1 += plo;
     uint64_t running = WRITE ? a.ctl.blk[blockIdx.x] : 0ull;
     uint64_t count = 0;
     pair_chunks<JMeta, kPT, kPI, kJW, 1>(p0, p1, a.R, offs, load, s_meta, s_off,
@@ -323,6 +326,35 @@ static void allow_join_smem() {
         GPS_CK(cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)join_smem(kMaxJobsPerLaunch, true)));
     });
+}
+
+__global__ void k_rows_for_ranges(const uint64_t* __restrict__ poff, uint64_t R, const uint64_t* __restrict__ lohi,
+                                  uint32_t n, uint64_t* __restrict__ rows) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t lo = lohi[2 * t], hi = lohi[2 * t + 1];
+    if (lo >= hi || R == 0) {
+        rows[3 * t] = rows[3 * t + 1] = rows[3 * t + 2] = 0;
+        return;
+    }
+    // i0 = largest row with poff[i0] <= lo; i1 = 1 + largest row with poff[i] <= hi - 1
+    auto find = [&](uint64_t p) {
+        uint64_t a = 0, b = R;
+        while (b - a > 1) {
+            uint64_t m = a + (b - a) / 2;
+            if (poff[m] <= p) a = m; else b = m;
+        }
+        return a;
+    };
+    const uint64_t i0 = find(lo);
+    rows[3 * t] = i0;
+    rows[3 * t + 1] = find(hi - 1) + 1;
+    rows[3 * t + 2] = poff[i0];
+}
+
+void run_rows_for_ranges(gps_ctx* c, const uint64_t* poff, uint64_t R, const uint64_t* d_lohi, uint32_t n,
+                         uint64_t* d_rows) {
+    launch(c, GPS_K_JOIN_LEN, dim3((n + 63) / 64), dim3(64), 0, k_rows_for_ranges, poff, R, d_lohi, n, d_rows);
 }
 
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G) {

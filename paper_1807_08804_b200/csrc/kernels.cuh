@@ -143,7 +143,13 @@ struct JoinStep {
     uint64_t* poff;        // [R+1] exclusive scan of segment lengths (pair space)
     PassCtl ctl;
     uint32_t* out;         // output rows of the writing jobs, job order
+    uint64_t plo = 0, phi = ~0ull;   // pair sub-range to process (row-sharded join); phi == ~0: all pairs
 };
+// Row-sharded join: for each target pair range [lo[t], hi[t]) of the local pair
+// space (poff[0..R]), the local row range [i0, i1) covering it and poff[i0]
+// (rows[3t .. 3t+2]).
+void run_rows_for_ranges(gps_ctx* c, const uint64_t* poff, uint64_t R, const uint64_t* d_lohi, uint32_t n,
+                         uint64_t* d_rows);
 void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (one look-back pass)
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G);
 void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G);

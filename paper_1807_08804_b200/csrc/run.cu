@@ -16,6 +16,7 @@
 #include <cstring>
 #include <numeric>
 
+#include "comm.h"
 #include "kernels.cuh"
 #include "planner.h"
 #include "runtime.h"
@@ -39,6 +40,13 @@ struct Carve {
         return p;
     }
 };
+
+// host mirror of pairs_range (pairs.cuh): contiguous share of P items for part b of G
+void pairs_range_host(uint64_t P, uint32_t b, uint32_t G, uint64_t& p0, uint64_t& p1) {
+    const uint64_t q = P / G, rem = P % G;
+    p0 = q * b + (b < rem ? b : rem);
+    p1 = p0 + q + (b < rem ? 1 : 0);
+}
 
 struct QS {                       // one query of a chunk
     uint32_t idx = 0;             // position in the caller's array
@@ -70,6 +78,7 @@ struct Chunk {
     uint32_t* cnt_all = nullptr;  // [Σ k] candidate counts, contiguous
     std::vector<uint32_t> cnt_base;
     std::vector<DevPtr> keep;     // uploaded job arrays
+    float rebalance = 1.10f;      // row-sharded join threshold
     uint32_t nws = 0, rps = 0;
     uint32_t* Bp(const QS& q, int u) const { return q.B + (size_t)u * nws; }
     uint32_t* Xp(const QS& q, int s) const { return q.X + (size_t)s * nws; }
@@ -217,11 +226,213 @@ void setup_chunk(Chunk& ch) {
     (void)xbytes;
 }
 
-void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count_only, std::vector<QueryResult>& out) {
+// Host copy of n u64 that a collective left in device memory (stream-ordered + sync).
+std::vector<uint64_t> d2h_u64(gps_ctx* c, const uint64_t* d, size_t n) {
+    size_t got = 0;
+    uint64_t* h = static_cast<uint64_t*>(pinned_alloc(c, n * 8 + 8, &got));
+    GPS_CK(cudaMemcpyAsync(h, d, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    ctx_sync(c);
+    std::vector<uint64_t> v(h, h + n);
+    pinned_release(c, h, got);
+    return v;
+}
+
+// Row-sharded join of ONE query across the ranks of c->comm.  The
+// seed table is replicated, so its pair space is split evenly by pair index.  From
+// then on every rank extends its own rows; each step all-gathers the per-rank pair
+// counts and, when max/mean exceeds the threshold, moves rows so that rank r owns
+// the rows of the global pair range [r*P/N, (r+1)*P/N) (rows at a boundary are
+// sent to both sides; each side processes only its pair sub-range).  Global pair
+// order = rank order, so the shards in rank order are the global result.
+void join_sharded(Chunk& ch, QS* q, const uint32_t* ec_val, const std::function<const uint32_t*(int)>& ec_off_of,
+                  uint64_t* blk, bool count_only, float thr, QueryResult& r) {
+    gps_ctx* c = ch.c;
+    Comm* cm = c->comm;
+    const int N = cm->world, me = cm->rank;
+    const uint32_t G = (uint32_t)c->nsm * 4;
+    DevPtr coll(c, sizeof(uint64_t) * (4 * (size_t)N * N + 8 * N + 16));
+    uint64_t* d_send = coll.as<uint64_t>();
+    uint64_t* d_all = d_send + 4 * N;
+    Block cur;
+    const uint32_t* M = q->M;
+    uint64_t R = q->R;
+    bool replicated = true;
+    for (size_t s = 0; s < q->steps.size(); s++) {
+        const JoinStepPlan& st = q->steps[s];
+        const uint32_t w = (uint32_t)s + 1;
+        const bool last = s + 1 == q->steps.size();
+        DevPtr jt(c, sizeof(unsigned long long));
+        GPS_CK(cudaMemsetAsync(jt.p, 0, sizeof(unsigned long long), c->stream));
+        JoinJob j{};
+        j.row0 = 0;
+        j.Bx = ch.Bp(*q, st.key);
+        j.rpx = ch.rpp(*q, st.key);
+        j.ec_off = ec_off_of(q->ecjob[st.arc][st.key_dir]);
+        j.total = jt.as<unsigned long long>();
+        j.x_col = (uint32_t)q->col_of[st.key];
+        std::vector<CloseChk> cl;
+        for (int ci : st.closing) {
+            const QArc& a = q->plan.arcs[ci];
+            CloseChk x{};
+            x.key_new = a.a == st.nv;
+            x.key_col = x.key_new ? 0u : (uint32_t)q->col_of[a.a];
+            x.tgt_new = a.b == st.nv;
+            x.tgt_col = x.tgt_new ? 0u : (uint32_t)q->col_of[a.b];
+            x.Bk = ch.Bp(*q, a.a);
+            x.rpk = ch.rpp(*q, a.a);
+            x.off = ec_off_of(q->ecjob[ci][0]);
+            cl.push_back(x);
+        }
+        j.nclose = (uint32_t)cl.size();
+        j.final_ = last ? 1u : 0u;
+        j.nowrite = (last && count_only) ? 1u : 0u;
+        if (last) {
+            for (uint32_t col = 0; col < w; col++) j.perm[col] = q->vert_of_col[col];
+            j.perm[w] = (uint8_t)st.nv;
+        }
+        JoinStep js{};
+        js.w = w;
+        js.wout = w + 1;
+        js.nj = 1;
+        js.cl = cl.empty() ? nullptr : upload(c, cl, ch.keep);
+        js.ec_val = ec_val;
+        js.ctl = PassCtl{blk, c->d_done, c->d_info};
+        DevPtr s0, poff;
+        auto segment = [&]() {   // s0 / pair offsets of the current local table
+            s0 = DevPtr(c, sizeof(uint32_t) * (R + 1));
+            poff = DevPtr(c, sizeof(uint64_t) * (R + 1));
+            j.M = M;
+            js.R = R;
+            js.jobs = upload(c, std::vector<JoinJob>{j}, ch.keep);
+            js.s0 = s0.as<uint32_t>();
+            js.poff = poff.as<uint64_t>();
+            if (R == 0) GPS_CK(cudaMemsetAsync(poff.p, 0, sizeof(uint64_t), c->stream));
+            else run_join_seg(c, js);
+        };
+        segment();
+        uint64_t lo = 0, hi = 0;
+        if (replicated) {
+            const uint64_t P = d2h_u64(c, js.poff + R, 1)[0];
+            pairs_range_host(P, (uint32_t)me, (uint32_t)N, lo, hi);
+        } else {
+            cm->allgather_u64(js.poff + R, d_all, 1, c->stream);
+            const std::vector<uint64_t> Pall = d2h_u64(c, d_all, N);
+            uint64_t PT = 0, S = 0, mx = 0;
+            for (int t = 0; t < N; t++) {
+                if (t < me) S += Pall[t];
+                PT += Pall[t];
+                mx = std::max(mx, Pall[t]);
+            }
+            const double mean = (double)PT / N;
+            if (PT > 0 && (double)mx > thr * mean) {
+                // ---- rebalance: rows of global pair range T_t go to rank t ----
+                std::vector<uint64_t> lohi(2 * N), T(2 * N);
+                for (int t = 0; t < N; t++) {
+                    pairs_range_host(PT, (uint32_t)t, (uint32_t)N, T[2 * t], T[2 * t + 1]);
+                    const uint64_t a = std::max(T[2 * t], S), b = std::min(T[2 * t + 1], S + Pall[me]);
+                    lohi[2 * t] = a < b ? a - S : 0;
+                    lohi[2 * t + 1] = a < b ? b - S : 0;
+                }
+                DevPtr drows(c, sizeof(uint64_t) * 3 * N);
+                run_rows_for_ranges(c, js.poff, R, upload(c, lohi, ch.keep), (uint32_t)N, drows.as<uint64_t>());
+                const std::vector<uint64_t> rows = d2h_u64(c, drows.as<uint64_t>(), 3 * N);
+                std::vector<uint64_t> sm(2 * N);
+                for (int t = 0; t < N; t++) {
+                    const bool any = lohi[2 * t] < lohi[2 * t + 1];
+                    sm[2 * t] = any ? rows[3 * t + 1] - rows[3 * t] : 0;
+                    sm[2 * t + 1] = any ? S + rows[3 * t + 2] : 0;
+                }
+                GPS_CK(cudaMemcpyAsync(d_send, upload(c, sm, ch.keep), sizeof(uint64_t) * 2 * N,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+                cm->allgather_u64(d_send, d_all, 2 * N, c->stream);
+                const std::vector<uint64_t> all = d2h_u64(c, d_all, 2 * (size_t)N * N);
+                uint64_t newR = 0, A = ~0ull;
+                std::vector<uint64_t> at(N);
+                for (int src = 0; src < N; src++) {
+                    at[src] = newR;
+                    const uint64_t n = all[(size_t)src * 2 * N + 2 * me];
+                    if (n && A == ~0ull) A = all[(size_t)src * 2 * N + 2 * me + 1];
+                    newR += n;
+                }
+                Block nb = make_block(c, sizeof(uint32_t) * (newR * w + 1));
+                uint32_t* NBp = static_cast<uint32_t*>(nb->p);
+                std::vector<P2POp> ops;
+                for (int t = 0; t < N; t++) {
+                    const uint64_t nsend = sm[2 * t];
+                    const uint64_t nrecv = all[(size_t)t * 2 * N + 2 * me];
+                    const uint32_t* src = M + rows[3 * t] * w;
+                    if (t == me) {
+                        if (nsend)
+                            GPS_CK(cudaMemcpyAsync(NBp + at[me] * w, src, nsend * w * 4, cudaMemcpyDeviceToDevice,
+                                                   c->stream));
+                        continue;
+                    }
+                    if (nsend || nrecv)
+                        ops.push_back(P2POp{t, src, nsend * w * 4, NBp + at[t] * w, nrecv * w * 4});
+                }
+                cm->exchange(ops, c->stream);
+                cur = nb;
+                M = NBp;
+                R = newR;
+                segment();
+                lo = newR ? T[2 * me] - A : 0;
+                hi = newR ? T[2 * me + 1] - A : 0;
+            } else {
+                lo = 0;
+                hi = Pall[me];
+            }
+        }
+        js.plo = lo;
+        js.phi = hi;
+        run_join_count(c, js, G);
+        const uint64_t local = d2h_u64(c, (const uint64_t*)j.total, 1)[0];
+        const uint64_t writes = d2h_u64(c, c->d_info + 1, 1)[0];
+        GPS_CK(cudaMemcpyAsync(d_send, j.total, sizeof(uint64_t), cudaMemcpyDeviceToDevice, c->stream));
+        cm->allgather_u64(d_send, d_all, 1, c->stream);
+        const std::vector<uint64_t> totals = d2h_u64(c, d_all, N);
+        uint64_t global = 0;
+        for (uint64_t t : totals) global += t;
+        c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)(hi - lo);
+        if (global == 0) {
+            r.rows = 0;
+            r.global_rows = 0;
+            return;
+        }
+        Block ob;
+        if (writes) {
+            ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
+            js.out = static_cast<uint32_t*>(ob->p);
+            run_join_write(c, js, G);
+            c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)(hi - lo) +
+                                                  4.0 * (w + 1) * (double)writes;
+        }
+        if (last) {
+            r.rows = local;
+            r.global_rows = global;
+            if (writes) {
+                r.block = ob;
+                r.data = static_cast<const uint32_t*>(ob->p);
+            }
+            return;
+        }
+        M = writes ? static_cast<const uint32_t*>(ob->p) : nullptr;
+        R = writes;
+        cur = ob;
+        replicated = false;
+        q->col_of[st.nv] = (int)w;
+        q->vert_of_col[w] = (uint8_t)st.nv;
+        c->stats.join_rows_max = std::max<uint64_t>(c->stats.join_rows_max, global);
+        c->stats.join_rows_total += local;
+    }
+}
+
+void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count_only, float thr,
+               std::vector<QueryResult>& out) {
     Chunk ch;
     ch.c = c;
     ch.g = g;
     ch.qs = qsv;
+    ch.rebalance = thr;
     const DevGraph& d = g->d;
     setup_chunk(ch);
     filter_phase(ch, 2);
@@ -252,6 +463,8 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         if (!q->live) continue;
         if (q->k == 1) {   // single-vertex query: the candidate set is the answer (reading R11)
             r.rows = q->C[0];
+            r.global_rows = r.rows;
+            if (c->comm && c->comm->world > 1 && c->comm->rank != 0) r.rows = 0;   // one shard holds it
             if (!count_only) {
                 r.block = make_block(c, (size_t)r.rows * 4);
                 GPS_CK(cudaMemcpyAsync(r.block->p, q->carr[0], (size_t)r.rows * 4, cudaMemcpyDeviceToDevice,
@@ -340,6 +553,14 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         q->vert_of_col[0] = (uint8_t)s0.key;
         q->M = q->carr[s0.key];
         q->R = q->C[s0.key];
+    }
+    if (c->comm && c->comm->world > 1) {
+        for (QS* q : ch.qs) {
+            if (!q->live) continue;
+            join_sharded(ch, q, val.as<uint32_t>(), ec_off_of, blk.as<uint64_t>(), count_only,
+                         ch.rebalance, out[q->idx]);
+        }
+        return;
     }
     Block cur;   // holds the previous step's output while its rows are read
     for (size_t s = 0;; s++) {
@@ -491,7 +712,8 @@ void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t n
         while (i < todo.size()) {
             QS* q = todo[i];
             size_t b = filter_bytes(*q, g->d.nws);
-            if (!chunk.empty() && (chunk.size() >= kMaxBatch || bytes + b > kChunkBytes ||
+            const size_t maxb = (c->comm && c->comm->world > 1) ? 1 : kMaxBatch;   // sharded: one query at a time
+            if (!chunk.empty() && (chunk.size() >= maxb || bytes + b > kChunkBytes ||
                                    ecj + 2 * (size_t)std::max(q->E, 1) > kMaxJobsPerLaunch || vtx + q->k > kMaxJobsPerLaunch))
                 break;
             chunk.push_back(q);
@@ -500,10 +722,12 @@ void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t n
             vtx += (size_t)q->k;
             i++;
         }
-        run_chunk(c, g, chunk, count_only, out);
+        run_chunk(c, g, chunk, count_only, o.rebalance_threshold, out);
     }
+    const bool sharded = c->comm && c->comm->world > 1;
     for (uint32_t j = 0; j < nq; j++)
         if (out[j].status == GPS_OK) {
+            if (!sharded) out[j].global_rows = out[j].rows;
             c->stats.queries++;
             c->stats.embeddings += out[j].rows;
         }

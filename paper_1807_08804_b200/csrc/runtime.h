@@ -37,6 +37,7 @@ struct QueryResult {
     uint32_t cols = 0;
     Block block;                 // device rows (match mode), row-major rows x cols at data
     const uint32_t* data = nullptr;
+    uint64_t global_rows = 0;    // over all ranks (row-sharded join)
 };
 
 // Run queries qs[0..nq) on ctx c (its stream), batch-synchronously: every phase

@@ -62,7 +62,8 @@ class QueryDesc(ctypes.Structure):
 
 class MatchOpts(ctypes.Structure):
     _fields_ = [("refine_rounds", ctypes.c_uint32), ("reverse_refine", ctypes.c_int32),
-                ("lowconn_threshold", ctypes.c_uint32), ("result_on_device", ctypes.c_int32)]
+                ("lowconn_threshold", ctypes.c_uint32), ("result_on_device", ctypes.c_int32),
+                ("rebalance_threshold", ctypes.c_float)]
 
 
 class Stats(ctypes.Structure):
@@ -103,6 +104,10 @@ def _load_lib():
         "gps_set_workers": (S, [P, ctypes.c_uint32]),
         "gps_set_slice": (S, [P, ctypes.c_uint32]),
         "gps_match_batch_host": (S, [P, P, P, ctypes.c_uint32, P, P, ctypes.c_uint64, P, P, P]),
+        "gps_result_global_rows": (S, [P, P]),
+        "gps_local_comm_create": (S, [ctypes.c_int, P]),
+        "gps_local_comm_destroy": (S, [P]),
+        "gps_create_local_rank": (S, [P, P, ctypes.c_int, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -116,7 +121,8 @@ EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_grap
             "gps_graph_info", "gps_match", "gps_match_host", "gps_count", "gps_result_info",
             "gps_result_free", "gps_last_error", "gps_get_stats", "gps_reset_stats",
             "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates", "gps_match_batch",
-            "gps_count_batch", "gps_set_workers", "gps_set_slice", "gps_match_batch_host"]
+            "gps_count_batch", "gps_set_workers", "gps_set_slice", "gps_match_batch_host",
+            "gps_result_global_rows", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
 
 
 def _check(st: int):
@@ -132,8 +138,13 @@ def default_opts(**kw) -> MatchOpts:
     o = MatchOpts()
     _check(lib.gps_default_opts(ctypes.byref(o)))
     for k_, v in kw.items():
-        setattr(o, k_, int(v))
+        setattr(o, k_, float(v) if k_ == "rebalance_threshold" else int(v))
     return o
+
+
+def _with_device(o: MatchOpts, on_device: bool) -> MatchOpts:
+    return MatchOpts(o.refine_rounds, o.reverse_refine, o.lowconn_threshold, 1 if on_device else 0,
+                     o.rebalance_threshold)
 
 
 class _QueryArrays:
@@ -254,15 +265,39 @@ class Graph:
             pass
 
 
-class Context:
-    """One gps_ctx: a device and a stream (default: a library-owned stream)."""
+class LocalComm:
+    """In-process ranks on one device (tests of the row-sharded join)."""
 
-    def __init__(self, device: int = 0, stream=None, workers: int = 0):
-        o = CtxOpts(device, None, None, 0, 1)
+    def __init__(self, world: int):
+        h = ctypes.c_void_p()
+        _check(lib.gps_local_comm_create(int(world), ctypes.byref(h)))
+        self._h, self.world = h, world
+
+    def __del__(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.gps_local_comm_destroy(self._h)
+            self._h = None
+
+
+class Context:
+    """One gps_ctx: a device and a stream (default: a library-owned stream).
+
+    nccl_comm/rank/world: row-sharded join across ranks (ProcessGroupNCCL._comm_ptr());
+    local_comm/rank: in-process ranks sharing one device (tests)."""
+
+    def __init__(self, device: int = 0, stream=None, workers: int = 0, nccl_comm=None, rank: int = 0,
+                 world: int = 1, local_comm: Optional[LocalComm] = None):
+        o = CtxOpts(device, None, None, int(rank), int(world))
         if stream is not None:
             o.stream = int(getattr(stream, "cuda_stream", stream))
+        if nccl_comm is not None:
+            o.nccl_comm = int(nccl_comm)
         h = ctypes.c_void_p()
-        _check(lib.gps_create(ctypes.byref(o), ctypes.byref(h)))
+        if local_comm is not None:
+            _check(lib.gps_create_local_rank(ctypes.byref(o), local_comm._h, int(rank), ctypes.byref(h)))
+            self._comm = local_comm
+        else:
+            _check(lib.gps_create(ctypes.byref(o), ctypes.byref(h)))
         self._h = h
         self.device = device
         if workers:
@@ -308,7 +343,7 @@ class Context:
         """All embeddings: torch uint32 (rows, k) CUDA tensor (device=True) or numpy array."""
         qa = _QueryArrays(q)
         o = opts if opts is not None else default_opts()
-        o = MatchOpts(o.refine_rounds, o.reverse_refine, o.lowconn_threshold, 1 if device else 0)
+        o = _with_device(o, device)
         res = ctypes.c_void_p()
         _check(lib.gps_match(self._h, graph.handle, ctypes.byref(qa.desc), ctypes.byref(o), ctypes.byref(res)))
         rows, cols, ptr, ondev = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_void_p(), ctypes.c_int()
@@ -329,6 +364,22 @@ class Context:
             return np.frombuffer(buf, dtype=np.uint32).reshape(rows.value, cols.value).copy()
         finally:
             lib.gps_result_free(res)
+
+    def match_shard(self, graph: Graph, q, opts: Optional[MatchOpts] = None):
+        """Row-sharded join: (this rank's rows as a numpy array, global row count)."""
+        qa = _QueryArrays(q)
+        o = _with_device(opts if opts is not None else default_opts(), False)
+        res = ctypes.c_void_p()
+        _check(lib.gps_match(self._h, graph.handle, ctypes.byref(qa.desc), ctypes.byref(o), ctypes.byref(res)))
+        rows, cols, ptr, ondev, glob = (ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_void_p(), ctypes.c_int(),
+                                        ctypes.c_uint64())
+        lib.gps_result_info(res, ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(ptr), ctypes.byref(ondev))
+        lib.gps_result_global_rows(res, ctypes.byref(glob))
+        a = np.zeros((rows.value, cols.value), np.uint32)
+        if rows.value:
+            ctypes.memmove(a.ctypes.data, ptr.value, rows.value * cols.value * 4)
+        lib.gps_result_free(res)
+        return a, int(glob.value)
 
     def match_host(self, graph: Graph, q, out=None, opts: Optional[MatchOpts] = None):
         """Rows into a caller-owned host buffer (numpy uint32 or pinned torch tensor).
@@ -367,7 +418,7 @@ class Context:
         res = (ctypes.c_void_p * max(n, 1))()
         st = np.zeros(max(n, 1), np.int32)
         o = opts if opts is not None else default_opts()
-        o = MatchOpts(o.refine_rounds, o.reverse_refine, o.lowconn_threshold, 1 if device else 0)
+        o = _with_device(o, device)
         rc = lib.gps_match_batch(self._h, graph.handle, arr, n, ctypes.byref(o), res,
                                  ctypes.c_void_p(st.ctypes.data))
         out = []
@@ -398,7 +449,7 @@ class Context:
         n = len(qas)
         res = (ctypes.c_void_p * max(n, 1))()
         o = opts if opts is not None else default_opts()
-        o = MatchOpts(o.refine_rounds, o.reverse_refine, o.lowconn_threshold, 1)
+        o = _with_device(o, True)
         rc = lib.gps_match_batch(self._h, graph.handle, arr, n, ctypes.byref(o), res, None)
         br = BatchResult(self, res, n)
         _check(rc)

@@ -46,13 +46,14 @@ def test_struct_layouts(gps):
     assert ctypes.sizeof(gps.CsrDesc) == 56
     assert ctypes.sizeof(gps.QEdge) == 12
     assert ctypes.sizeof(gps.QueryDesc) == 32
-    assert ctypes.sizeof(gps.MatchOpts) == 16
+    assert ctypes.sizeof(gps.MatchOpts) == 20
     assert ctypes.sizeof(gps.Stats) == 32 + 4 * 8 * gps.NK + 16
 
 
 def test_default_opts(gps):
     o = gps.default_opts()
     assert (o.refine_rounds, o.reverse_refine, o.lowconn_threshold, o.result_on_device) == (1, 1, 1, 1)
+    assert abs(o.rebalance_threshold - 1.10) < 1e-6
 
 
 def test_no_cpu_fallback_without_device(gps):
