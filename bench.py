@@ -145,6 +145,21 @@ def query_bytes(q):
     return 32 + q.k * 4 + q.k * 8 + len(q.edges) * 12
 
 
+def rank_batch(queries, counts, rank):
+    """Weak scaling: every rank runs a full batch (rotated per rank so ranks start on different queries)."""
+    rot = (rank * 37) % len(queries)
+    return queries[rot:] + queries[:rot], counts[rot:] + counts[:rot]
+
+
+def max_over_ranks(values, dist, device):
+    """Element-wise max over ranks (the timed region is the slowest rank's)."""
+    import torch
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -185,10 +200,7 @@ def main():
     g = config_graph(2)
     G = ctx.load_graph(g)
     queries, counts = load_queries()
-    # weak scaling: each rank runs a full batch of the queries, rotated per rank
-    rot = (rank * 37) % len(queries)
-    queries = queries[rot:] + queries[:rot]
-    counts = counts[rot:] + counts[:rot]
+    queries, counts = rank_batch(queries, counts, rank)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     if args.workers:
@@ -274,10 +286,7 @@ def main():
             e2e_ms += 1000 * (time.perf_counter() - t0)
         e2e_steps = max(1, args.steps // 2)
 
-    t = torch.tensor([total_ms, e2e_ms / e2e_steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms, e2e_step_ms = float(t[0]), float(t[1])
+    max_ms, e2e_step_ms = max_over_ranks([total_ms, e2e_ms / e2e_steps], dist, dev)
     nq = len(queries) * args.steps * world
     value = nq / (max_ms / 1000)
     emb_per_s = emb_total * world / (max_ms / 1000)
