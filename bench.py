@@ -33,6 +33,8 @@ WORKLOADS = {
     2: f"cfg2: {GRAPH}, 100 six-vertex BFS tree queries per step, gps_match with device-resident results",
     3: f"cfg3: {GRAPH}, 30 cyclic 8/10/12-vertex queries (dense hub core) per step, device-resident results",
     5: f"cfg5: {GRAPH}, QA batch of 10000 3-5-vertex queries with a bound concept vertex per step",
+    4: "cfg4: Chung-Lu graph n=20000000 m=100000000 labelled arcs (HBM-resident CSR); per step gps_match of "
+       "labelled out-star-2 / in-star-2 / 2-path (2.5e8 rows written) + gps_count of an out-star-3 (3.2e9)",
 }
 CONFIG = 2
 
@@ -40,6 +42,9 @@ CONFIG = 2
 def load_queries(cfg=None):
     from synth import Query
     cfg = CONFIG if cfg is None else cfg
+    if cfg == 4:   # closed-form-pinned large joins (tests/test_gpu_large.py); no stored oracle counts
+        from synth.large import CFG4
+        return [q for _, q, _ in CFG4], [None] * len(CFG4)
     data = json.load(open(os.path.join(ROOT, "synth", "data", f"cfg{cfg}_queries.json")))
     return [Query.from_json(d["query"]) for d in data["queries"]], [d["oracle_count"] for d in data["queries"]]
 
@@ -166,7 +171,7 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
                     help="BASELINE.json configs[N-1]; the driver's line is config 2")
     ap.add_argument("--ref-queries-per-step", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -197,9 +202,12 @@ def main():
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.Stream(device=dev)
     ctx = gpsense.Context(local, stream=stream)
-    g = config_graph(2)
+    g = config_graph(4 if CONFIG == 4 else 2)
     G = ctx.load_graph(g)
     queries, counts = load_queries()
+    if CONFIG == 4:
+        args.no_cpu_baseline = True   # the oracle on 10^8 arcs / 10^9 embeddings is far outside a bounded sample
+        from synth.large import CFG4
     queries, counts = rank_batch(queries, counts, rank)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -208,6 +216,16 @@ def main():
         ctx.set_slice(args.slice)
 
     def step():
+        if CONFIG == 4:
+            emb = 0
+            for (name, q, mode) in CFG4:
+                if mode == "count":
+                    emb += ctx.count(G, q)
+                else:
+                    br = ctx.match_batch_raw(G, [q])
+                    emb += int(br.rows().sum())
+                    br.free()
+            return emb
         if args.workers:
             br = ctx.match_batch_raw(G, queries)       # device-resident results, freed after the step
             emb = int(br.rows().sum())
@@ -268,7 +286,11 @@ def main():
         st = ctx.stats()
 
         # e2e: the same step through the C-ABI with a HOST result buffer (copies inside the region)
-        total_words = sum(c * q.k for c, q in zip(counts, queries))
+        if CONFIG == 4:   # sizes of the written results (untimed counts), for the pinned buffer
+            counts = [ctx.count(G, q) if mode == "match" else 0 for (_, q, mode) in CFG4]
+            total_words = max(c * q.k for c, q in zip(counts, queries))
+        else:
+            total_words = sum(c * q.k for c, q in zip(counts, queries))
         pinned = torch.empty(int(total_words * 1.05) + 1024, dtype=torch.int32, pin_memory=True)
         h2d = sum(query_bytes(q) for q in queries)
         d2h = sum(c * q.k * 4 for c, q in zip(counts, queries))
@@ -278,7 +300,13 @@ def main():
                 flush.fill_(s & 0xff)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            if args.workers:
+            if CONFIG == 4:
+                for (_, q, mode) in CFG4:
+                    if mode == "count":
+                        ctx.count(G, q)
+                    else:
+                        ctx.match_host(G, q, pinned)
+            elif args.workers:
                 ctx.match_batch_host(G, queries, pinned)    # library copies every result into `pinned`
             else:
                 for q in queries:

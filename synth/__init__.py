@@ -10,6 +10,7 @@ from .graphs import (  # noqa: F401
     DataGraph,
     gnm_undirected,
     chung_lu_directed,
+    chung_lu_directed_fast,
     random_multigraph,
     complete_graph,
     star_graph,

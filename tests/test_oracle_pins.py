@@ -22,6 +22,7 @@ import os
 import numpy as np
 import pytest
 
+import closed_forms  # noqa: F401  (tests/ on sys.path via conftest)
 from oracle import oracle
 from synth import (DataGraph, Query, complete_graph, complete_query, config_graph,
                    fixture_fig3_example, random_connected_query, random_multigraph,
@@ -289,3 +290,22 @@ def test_errors():
         oracle.count(og, Query(2, [-1] * 2, [-1] * 2, [(0, 0, -1), (0, 1, -1)]))
     with pytest.raises(ValueError):   # bound id out of range
         oracle.count(og, Query(2, [-1] * 2, [9, -1], [(0, 1, -1)]))
+
+
+# ------------------------------------------------------------------ closed forms of config 4
+@pytest.mark.parametrize("seed", range(6))
+def test_closed_forms_large_families_vs_oracle(seed):
+    """tests/closed_forms.py (used to pin config 4 at 10^8 scale) against the oracle on small graphs."""
+    import closed_forms as cf
+    from synth.large import in_star, out_star, path2
+    g = random_multigraph(60, 700, n_elabels=3, n_vlabels=3, seed=900 + seed, undirected=False,
+                          self_loops=False, dup_prob=0.3)
+    og = oracle.OracleGraph(g)
+    keys = cf.pair_keys(g)
+    rng = np.random.default_rng(seed)
+    for _ in range(4):
+        la, lb, lc = (int(x) for x in rng.integers(-1, 3, 3))
+        k = int(rng.integers(1, 4))
+        assert oracle.count(og, out_star(k, la, lb)) == cf.out_star(g, keys, k, la, lb)
+        assert oracle.count(og, in_star(k, la, lb)) == cf.in_star(g, keys, k, la, lb)
+        assert oracle.count(og, path2(la, lb, lc)) == cf.path2(g, keys, la, lb, lc)
