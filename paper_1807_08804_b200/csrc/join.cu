@@ -141,51 +141,119 @@ __device__ __forceinline__ uint32_t job_of_row(const JoinJob* __restrict__ jobs,
     return lo;
 }
 
+__device__ __forceinline__ bool seg_find(const uint32_t* __restrict__ val, uint32_t lo, uint32_t hi, uint32_t t,
+                                         uint32_t* pos) {
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        uint32_t v = __ldg(val + mid);
+        if (v == t) {
+            *pos = mid;
+            return true;
+        }
+        if (v < t) lo = mid + 1; else hi = mid;
+    }
+    return false;
+}
+
+template <bool FAST>
 __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
                                                   uint32_t epoch) {
-    __shared__ uint64_t s_pre;
+    __shared__ uint64_t s_pre[3];
     const uint32_t tile = lb_ticket(lb.ctr, ntiles);
     const uint64_t r0 = (uint64_t)tile * kSegTile + (uint64_t)threadIdx.x * kSegRows;
-    uint32_t len[kSegRows];
-    uint64_t tsum = 0;
+    uint32_t len[kSegRows], wc[kSegRows], ac[kSegRows];
+    uint64_t tsum = 0, wsum = 0, asum = 0;
     uint32_t jb = r0 < a.R ? job_of_row(a.jobs, a.nj, r0) : 0;
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {
         const uint64_t r = r0 + i;
-        len[i] = 0;
+        len[i] = wc[i] = ac[i] = 0;
         if (r < a.R) {
             while (jb + 1 < a.nj && a.jobs[jb + 1].row0 <= r) jb++;
             const JoinJob& J = a.jobs[jb];
-            const uint32_t key = __ldg(J.M + (r - J.row0) * a.w + J.x_col);
+            const uint32_t* row = J.M + (r - J.row0) * a.w;
+            const uint32_t key = __ldg(row + J.x_col);
             const uint32_t rk = bit_rank(J.Bx, J.rpx, key);
             const uint32_t s = __ldg(J.ec_off + rk);
             len[i] = __ldg(J.ec_off + rk + 1) - s;
             a.s0[r] = s;
+            if (FAST) {
+                uint32_t excl = 0, pos;
+                for (uint32_t c = 0; c < a.w; c++) excl += seg_find(a.ec_val, s, s + len[i], __ldg(row + c), &pos);
+                ac[i] = len[i] - excl;
+                wc[i] = J.nowrite ? 0u : ac[i];
+            }
         }
         tsum += len[i];
+        wsum += wc[i];
+        asum += ac[i];
     }
-    uint64_t tot;
+    uint64_t tot, wtot = 0, atot = 0;
     const uint64_t pre = block_excl_scan(tsum, &tot);
+    uint64_t wpre = 0, apre = 0;
+    if (FAST) {
+        wpre = block_excl_scan(wsum, &wtot);
+        apre = block_excl_scan(asum, &atot);
+    }
     if (threadIdx.x < 32) {
         uint64_t p = lb_warp_lookback(lb.status, tile, tot, epoch);
-        if (threadIdx.x == 0) s_pre = p;
+        uint64_t pw = 0, pa = 0;
+        if (FAST) {
+            pw = lb_warp_lookback(lb.status + lb.max_tiles, tile, wtot, epoch);
+            pa = lb_warp_lookback(lb.status + 2 * (size_t)lb.max_tiles, tile, atot, epoch);
+        }
+        if (threadIdx.x == 0) {
+            s_pre[0] = p;
+            s_pre[1] = pw;
+            s_pre[2] = pa;
+        }
     }
     __syncthreads();
-    uint64_t run = s_pre + pre;
+    uint64_t run = s_pre[0] + pre, wrun = s_pre[1] + wpre, arun = s_pre[2] + apre;
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {
         const uint64_t r = r0 + i;
-        if (r < a.R) a.poff[r] = run;
+        if (r < a.R) {
+            a.poff[r] = run;
+            if (FAST) {
+                a.woff[r] = wrun;
+                a.aoff[r] = arun;
+            }
+        }
         run += len[i];
+        wrun += wc[i];
+        arun += ac[i];
     }
-    if (tile == ntiles - 1 && threadIdx.x == 0) a.poff[a.R] = s_pre + tot;
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        a.poff[a.R] = s_pre[0] + tot;
+        if (FAST) {
+            a.woff[a.R] = s_pre[1] + wtot;
+            a.aoff[a.R] = s_pre[2] + atot;
+        }
+    }
+}
+
+__global__ void k_join_job_totals(const __grid_constant__ JoinStep a) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= a.nj) return;
+    const uint64_t lo = a.jobs[j].row0, hi = j + 1 < a.nj ? a.jobs[j + 1].row0 : a.R;
+    *a.jobs[j].total = a.aoff[hi] - a.aoff[lo];
+}
+
+void run_join_job_totals(gps_ctx* c, const JoinStep& s) {
+    launch(c, GPS_K_JOIN_LEN, dim3((s.nj + 127) / 128), dim3(128), 0, k_join_job_totals, s);
 }
 
 void run_join_seg(gps_ctx* c, const JoinStep& s) {
     const uint64_t nt = (s.R + kSegTile - 1) / kSegTile;
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join table too large");
-    LbScratch lb = lb_scratch(c, 1, (uint32_t)nt);
-    launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg, s, lb, (uint32_t)nt, lb_next_epoch(c));
+    LbScratch lb = lb_scratch(c, 3, (uint32_t)nt);
+    if (s.fast)
+        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg<true>, s, lb, (uint32_t)nt,
+               lb_next_epoch(c));
+    else
+        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg<false>, s, lb, (uint32_t)nt,
+               lb_next_epoch(c));
     c->stats.k_bytes[GPS_K_JOIN_LEN] += 4.0 * s.R + 12.0 * s.R;
 }
 
@@ -216,6 +284,7 @@ __device__ __forceinline__ bool pair_ok(const JoinStep& a, const JoinJob& J, con
 
 struct JMeta {              // one input row of a join step
     const uint32_t* rowp;   // its w values
+    uint64_t r;             // its index in the step's row space
     uint32_t s0;            // start of its EC segment in ec_val
     uint32_t job;
 };
@@ -238,6 +307,7 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
         m.job = pairs_find_smem(s_jr, a.nj, r);
         const JoinJob& J = a.jobs[m.job];
         m.rowp = J.M + (r - J.row0) * a.w;
+        m.r = r;
         m.s0 = __ldg(a.s0 + r);
         return m;
     };
@@ -265,7 +335,34 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
                 writes[it] = valid[it] && !J.nowrite;
             }
         }
-        if (WRITE) {
+        if (WRITE && a.fast) {
+            // closing-free step: output position = woff[row] + valid pairs before j in the row
+            // (j - #row values found in the segment prefix); no count pass, no block scan
+            uint64_t cur = ~0ull, pos = 0;
+#pragma unroll
+            for (int it = 0; it < kPI; it++) {
+                if (!v[it]) continue;
+                if (m[it].r != cur) {
+                    cur = m[it].r;
+                    uint32_t excl = 0, fp;
+                    if (j[it] > 0)
+                        for (uint32_t c = 0; c < a.w; c++)
+                            excl += seg_find(a.ec_val, m[it].s0, m[it].s0 + (uint32_t)j[it], __ldg(m[it].rowp + c), &fp);
+                    pos = __ldg(a.woff + cur) + j[it] - excl;
+                }
+                if (!writes[it]) continue;
+                const JoinJob& J = a.jobs[m[it].job];
+                const uint32_t* row = m[it].rowp;
+                uint32_t* dst = a.out + (pos++) * a.wout;
+                if (J.final_) {
+                    for (uint32_t c = 0; c < a.w; c++) dst[J.perm[c]] = __ldg(row + c);
+                    dst[J.perm[a.w]] = cand[it];
+                } else {
+                    for (uint32_t c = 0; c < a.w; c++) dst[c] = __ldg(row + c);
+                    dst[a.w] = cand[it];
+                }
+            }
+        } else if (WRITE) {
             uint32_t mine = 0;
 #pragma unroll
             for (int it = 0; it < kPI; it++) mine += writes[it] ? 1u : 0u;

@@ -144,7 +144,16 @@ struct JoinStep {
     PassCtl ctl;
     uint32_t* out;         // output rows of the writing jobs, job order
     uint64_t plo = 0, phi = ~0ull;   // pair sub-range to process (row-sharded join); phi == ~0: all pairs
+    // closing-free fast path (no job of the step has a fused closing arc): validity is
+    // injectivity only, so a row's output count is len - #(row values in its sorted
+    // segment) and the count pass disappears; woff / aoff are exclusive scans of the
+    // written / all per-row output counts (R+1 entries).
+    int fast = 0;
+    uint64_t* woff = nullptr;
+    uint64_t* aoff = nullptr;
 };
+// per-job output totals of a fast step: total[j] = aoff[row0(j+1)] - aoff[row0(j)]
+void run_join_job_totals(gps_ctx* c, const JoinStep& s);
 // Row-sharded join: for each target pair range [lo[t], hi[t]) of the local pair
 // space (poff[0..R]), the local row range [i0, i1) covering it and poff[i0]
 // (rows[3t .. 3t+2]).

@@ -610,8 +610,10 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             R += q->R;
         }
         if (jj.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: join job list too long");
+        const bool fast = cl.empty();   // no fused closing arc in any job of this step
         DevPtr s0(c, sizeof(uint32_t) * (R + 1));
         DevPtr poff(c, sizeof(uint64_t) * (R + 1));
+        DevPtr woff, aoff;
         JoinStep js{};
         js.w = w;
         js.wout = w + 1;
@@ -623,8 +625,21 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         js.s0 = s0.as<uint32_t>();
         js.poff = poff.as<uint64_t>();
         js.ctl = PassCtl{blk.as<uint64_t>(), c->d_done, c->d_info};
+        if (fast) {
+            woff = DevPtr(c, sizeof(uint64_t) * (R + 1));
+            aoff = DevPtr(c, sizeof(uint64_t) * (R + 1));
+            js.fast = 1;
+            js.woff = woff.as<uint64_t>();
+            js.aoff = aoff.as<uint64_t>();
+        }
         run_join_seg(c, js);
-        run_join_count(c, js, G);
+        if (fast) {
+            run_join_job_totals(c, js);
+            GPS_CK(cudaMemcpyAsync(c->d_info, js.poff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
+            GPS_CK(cudaMemcpyAsync(c->d_info + 1, js.woff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            run_join_count(c, js, G);
+        }
         std::vector<uint64_t> tot(act.size());
         uint64_t P = 0, writes = 0;
         {
@@ -638,7 +653,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             writes = h[act.size() + 1];
             pinned_release(c, h, got);
         }
-        c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)P;
+        if (!fast) c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)P;
         Block ob;
         if (writes) {
             if (writes > (~0ull) / (4ull * (w + 1))) fail(GPS_EOVERFLOW, "result size overflows");
