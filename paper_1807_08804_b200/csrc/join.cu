@@ -336,33 +336,21 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
             }
         }
         if (WRITE && a.fast) {
-            // closing-free step: output position = woff[row] + valid pairs before j in the row
-            // (j - #row values found in the segment prefix); no count pass, no block scan
-            uint64_t cur = ~0ull, pos = 0;
-#pragma unroll
-            for (int it = 0; it < kPI; it++) {
-                if (!v[it]) continue;
-                if (m[it].r != cur) {
-                    cur = m[it].r;
-                    uint32_t excl = 0, fp;
-                    if (j[it] > 0)
-                        for (uint32_t c = 0; c < a.w; c++)
-                            excl += seg_find(a.ec_val, m[it].s0, m[it].s0 + (uint32_t)j[it], __ldg(m[it].rowp + c), &fp);
-                    pos = __ldg(a.woff + cur) + j[it] - excl;
-                }
-                if (!writes[it]) continue;
-                const JoinJob& J = a.jobs[m[it].job];
-                const uint32_t* row = m[it].rowp;
-                uint32_t* dst = a.out + (pos++) * a.wout;
-                if (J.final_) {
-                    for (uint32_t c = 0; c < a.w; c++) dst[J.perm[c]] = __ldg(row + c);
-                    dst[J.perm[a.w]] = cand[it];
-                } else {
-                    for (uint32_t c = 0; c < a.w; c++) dst[c] = __ldg(row + c);
-                    dst[a.w] = cand[it];
-                }
+            // closing-free step (no count pass): the chunk's first output row is
+            // woff[row] + (j - #row values in the segment prefix) of its first pair;
+            // thread 0 computes it, the staged path below does the rest
+            __shared__ uint64_t s_base;
+            if (threadIdx.x == 0 && v[0]) {
+                uint32_t excl = 0, fp;
+                if (j[0] > 0)
+                    for (uint32_t c = 0; c < a.w; c++)
+                        excl += seg_find(a.ec_val, m[0].s0, m[0].s0 + (uint32_t)j[0], __ldg(m[0].rowp + c), &fp);
+                s_base = __ldg(a.woff + m[0].r) + j[0] - excl;
             }
-        } else if (WRITE) {
+            __syncthreads();
+            running = s_base;
+        }
+        if (WRITE) {
             uint32_t mine = 0;
 #pragma unroll
             for (int it = 0; it < kPI; it++) mine += writes[it] ? 1u : 0u;

@@ -610,7 +610,16 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             R += q->R;
         }
         if (jj.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: join job list too long");
-        const bool fast = cl.empty();   // no fused closing arc in any job of this step
+        // closing-free fast path when segments are long enough that w binary searches per row
+        // beat a count pass over every pair (mean EC segment length of the extension arcs)
+        double segw = 0, roww = 0;
+        for (size_t i = 0; i < act.size(); i++) {
+            const JoinStepPlan& st = act[i]->steps[s];
+            const uint32_t ck = act[i]->C[st.key];
+            segw += (double)act[i]->R * (double)ectot[act[i]->ecjob[st.arc][st.key_dir]] / std::max<uint32_t>(ck, 1);
+            roww += (double)act[i]->R;
+        }
+        const bool fast = cl.empty() && roww > 0 && segw / roww > 2.0 * (w + 1);
         DevPtr s0(c, sizeof(uint32_t) * (R + 1));
         DevPtr poff(c, sizeof(uint64_t) * (R + 1));
         DevPtr woff, aoff;
