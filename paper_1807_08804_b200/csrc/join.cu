@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
     pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
     p0 += plo;
     p1 += plo;
-    uint64_t running = WRITE ? a.ctl.blk[blockIdx.x] : 0ull;
+    uint64_t running = (WRITE && !a.fast) ? a.ctl.blk[blockIdx.x] : 0ull;
+    bool have_base = false;
     uint64_t count = 0;
     pair_chunks<JMeta, kPT, kPI, kJW, 1>(p0, p1, a.R, offs, load, s_meta, s_off,
                                          [&](const bool (&v)[kPI], const JMeta (&m)[kPI], const uint64_t (&j)[kPI]) {
@@ -340,15 +341,18 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
             // woff[row] + (j - #row values in the segment prefix) of its first pair;
             // thread 0 computes it, the staged path below does the rest
             __shared__ uint64_t s_base;
-            if (threadIdx.x == 0 && v[0]) {
+            if (!have_base && threadIdx.x == 0 && v[0]) {
                 uint32_t excl = 0, fp;
                 if (j[0] > 0)
                     for (uint32_t c = 0; c < a.w; c++)
                         excl += seg_find(a.ec_val, m[0].s0, m[0].s0 + (uint32_t)j[0], __ldg(m[0].rowp + c), &fp);
                 s_base = __ldg(a.woff + m[0].r) + j[0] - excl;
             }
-            __syncthreads();
-            running = s_base;
+            if (!have_base) {   // later chunks of the block continue from `running`
+                __syncthreads();
+                running = s_base;
+                have_base = true;
+            }
         }
         if (WRITE) {
             uint32_t mine = 0;
