@@ -619,7 +619,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             segw += (double)act[i]->R * (double)ectot[act[i]->ecjob[st.arc][st.key_dir]] / std::max<uint32_t>(ck, 1);
             roww += (double)act[i]->R;
         }
-        const bool fast = cl.empty() && roww > 0 && segw / roww > 2.0 * (w + 1);
+        const bool fast = cl.empty() && roww > 0 && segw / roww > 32.0 * (w + 1);
         DevPtr s0(c, sizeof(uint32_t) * (R + 1));
         DevPtr poff(c, sizeof(uint64_t) * (R + 1));
         DevPtr woff, aoff;
