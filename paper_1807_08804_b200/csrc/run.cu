@@ -610,16 +610,6 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             R += q->R;
         }
         if (jj.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: join job list too long");
-        // closing-free fast path when segments are long enough that w binary searches per row
-        // beat a count pass over every pair (mean EC segment length of the extension arcs)
-        double segw = 0, roww = 0;
-        for (size_t i = 0; i < act.size(); i++) {
-            const JoinStepPlan& st = act[i]->steps[s];
-            const uint32_t ck = act[i]->C[st.key];
-            segw += (double)act[i]->R * (double)ectot[act[i]->ecjob[st.arc][st.key_dir]] / std::max<uint32_t>(ck, 1);
-            roww += (double)act[i]->R;
-        }
-        const bool fast = cl.empty() && roww > 0 && segw / roww > 32.0 * (w + 1);
         DevPtr s0(c, sizeof(uint32_t) * (R + 1));
         DevPtr poff(c, sizeof(uint64_t) * (R + 1));
         DevPtr woff, aoff;
@@ -634,15 +624,21 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         js.s0 = s0.as<uint32_t>();
         js.poff = poff.as<uint64_t>();
         js.ctl = PassCtl{blk.as<uint64_t>(), c->d_done, c->d_info};
+        run_join_seg(c, js);
+        // closing-free fast path when rows are long (pairs per row >> w): w binary searches per
+        // row then replace a count pass over every pair
+        bool fast = false;
+        if (cl.empty()) {
+            const uint64_t P0 = d2h_u64(c, js.poff + R, 1)[0];
+            fast = (double)P0 > 8.0 * (w + 1) * (double)R;
+        }
         if (fast) {
             woff = DevPtr(c, sizeof(uint64_t) * (R + 1));
             aoff = DevPtr(c, sizeof(uint64_t) * (R + 1));
             js.fast = 1;
             js.woff = woff.as<uint64_t>();
             js.aoff = aoff.as<uint64_t>();
-        }
-        run_join_seg(c, js);
-        if (fast) {
+            run_join_seg(c, js);
             run_join_job_totals(c, js);
             GPS_CK(cudaMemcpyAsync(c->d_info, js.poff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
             GPS_CK(cudaMemcpyAsync(c->d_info + 1, js.woff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
