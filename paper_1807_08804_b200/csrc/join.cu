@@ -343,10 +343,11 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
             __shared__ uint64_t s_base;
             if (!have_base && threadIdx.x == 0 && v[0]) {
                 uint32_t excl = 0, fp;
-                if (j[0] > 0)
+                const bool nw = a.jobs[m[0].job].nowrite;   // count-only rows contribute no output rows
+                if (j[0] > 0 && !nw)
                     for (uint32_t c = 0; c < a.w; c++)
                         excl += seg_find(a.ec_val, m[0].s0, m[0].s0 + (uint32_t)j[0], __ldg(m[0].rowp + c), &fp);
-                s_base = __ldg(a.woff + m[0].r) + j[0] - excl;
+                s_base = __ldg(a.woff + m[0].r) + (nw ? 0 : j[0] - excl);
             }
             if (!have_base) {   // later chunks of the block continue from `running`
                 __syncthreads();
