@@ -45,7 +45,6 @@ void ctx_harvest(gps_ctx* c) {
 void ctx_sync(gps_ctx* c) {
     GPS_CK(cudaStreamSynchronize(c->stream));
     c->stats.host_syncs++;
-    c->h_arena_off = 0;   // every staged upload has completed
     ctx_harvest(c);
 }
 
@@ -72,25 +71,50 @@ Block make_block(gps_ctx* c, size_t bytes) {
     return b;
 }
 
+// Job arrays go through a pinned arena and its device twin (same offsets, bump
+// allocated): no device allocation per upload, and all the arrays staged for one
+// launch travel in ONE H2D copy (flush_uploads, called by launch()).  The arena
+// grows by whole segments and is rewound only at the start of a run.
 void* upload_bytes(gps_ctx* c, const void* src, size_t bytes, std::vector<DevPtr>& keep) {
+    (void)keep;
     const size_t need = (bytes + 255) & ~size_t(255);
-    if (c->h_arena_off + need > c->h_arena_cap) {
-        if (c->h_arena_off) ctx_sync(c);   // staged copies done: the arena can be reused
-        if (need > c->h_arena_cap) {
-            if (c->h_arena) cudaFreeHost(c->h_arena);
-            c->h_arena = nullptr;
-            size_t cap = std::max<size_t>(need, std::max<size_t>(c->h_arena_cap * 2, 4u << 20));
-            GPS_CK(cudaMallocHost(&c->h_arena, cap));
-            c->h_arena_cap = cap;
+    if (c->arena.empty() || c->h_arena_off + need > c->arena[c->arena_seg].cap) {
+        if (!c->arena.empty()) {
+            flush_uploads(c);
+            c->arena_seg++;
         }
+        if (c->arena_seg >= c->arena.size() || c->arena[c->arena_seg].cap < need) {
+            const size_t prev = c->arena.empty() ? 0 : c->arena.back().cap;
+            gps_ctx::ArenaSeg sg{nullptr, nullptr, std::max<size_t>(need, std::max<size_t>(2 * prev, 4u << 20))};
+            GPS_CK(cudaMallocHost(&sg.h, sg.cap));
+            GPS_CK(cudaMalloc(&sg.d, sg.cap));
+            c->arena.insert(c->arena.begin() + c->arena_seg, sg);
+        }
+        c->h_arena_off = 0;
+        c->h_flushed = 0;
     }
-    char* h = c->h_arena + c->h_arena_off;
+    gps_ctx::ArenaSeg& sg = c->arena[c->arena_seg];
+    char* h = sg.h + c->h_arena_off;
+    void* d = sg.d + c->h_arena_off;
     c->h_arena_off += need;
     if (bytes) std::memcpy(h, src, bytes);
-    keep.emplace_back(c, need ? need : 16);
-    void* d = keep.back().p;
-    if (bytes) GPS_CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream));
     return d;
+}
+
+void flush_uploads(gps_ctx* c) {
+    if (c->arena.empty()) return;
+    gps_ctx::ArenaSeg& sg = c->arena[c->arena_seg];
+    const size_t a = c->h_flushed, b = c->h_arena_off;
+    if (b > a) GPS_CK(cudaMemcpyAsync(sg.d + a, sg.h + a, b - a, cudaMemcpyHostToDevice, c->stream));
+    c->h_flushed = b;
+}
+
+void arena_reset(gps_ctx* c) {
+    flush_uploads(c);
+    GPS_CK(cudaStreamSynchronize(c->stream));   // earlier staged copies / kernels are done with the arena
+    c->arena_seg = 0;
+    c->h_arena_off = 0;
+    c->h_flushed = 0;
 }
 
 void* pinned_alloc(gps_ctx* c, size_t bytes, size_t* got) {
@@ -188,8 +212,11 @@ void ctx_release(gps_ctx* c) {
     c->event_pool.clear();
     for (auto& kv : c->pinned_free) cudaFreeHost(kv.second);
     c->pinned_free.clear();
-    if (c->h_arena) cudaFreeHost(c->h_arena);
-    c->h_arena = nullptr;
+    for (auto& sg : c->arena) {
+        cudaFreeHost(sg.h);
+        cudaFree(sg.d);
+    }
+    c->arena.clear();
     cudaFree(c->d_bytes);
     cudaFree(c->d_info);
     cudaFreeHost(c->h_info);

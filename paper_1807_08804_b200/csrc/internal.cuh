@@ -86,8 +86,16 @@ struct gps_ctx {
     uint32_t lb_tiles = 0;                   // tiles per slot currently allocated
     uint32_t lb_slots = 0;                   // slots currently allocated
     uint32_t lb_epoch = 0;                   // launch epoch (never 0 once used)
-    char* h_arena = nullptr;                 // pinned staging for job uploads (bump, reset at every sync)
-    size_t h_arena_cap = 0, h_arena_off = 0;
+    // job-array staging: pinned segments with device twins (same offsets), bump allocated,
+    // rewound only by arena_reset() at the start of a run (never while arrays are in use)
+    struct ArenaSeg {
+        char* h;
+        char* d;
+        size_t cap;
+    };
+    std::vector<ArenaSeg> arena;
+    size_t arena_seg = 0, h_arena_off = 0;
+    size_t h_flushed = 0;                    // [h_flushed, h_arena_off) of the current segment not yet copied
     std::multimap<size_t, void*> pinned_free;  // pinned host buffers for host results (reused)
     std::vector<gps_result*> results;        // live device results (freed at destroy)
     // batch execution: worker sub-contexts (own stream + scratch) driven by a host thread pool
@@ -137,9 +145,13 @@ cudaEvent_t ctx_event(gps_ctx* c);
 void ctx_harvest(gps_ctx* c);          // after a stream sync: fold finished event pairs into stats
 void ctx_sync(gps_ctx* c);             // stream sync + harvest
 
+void flush_uploads(gps_ctx* c);         // one H2D copy of every job array staged since the last launch
+void arena_reset(gps_ctx* c);           // rewind the staging arena (no staged array may still be in use)
+
 template <typename Kernel, typename... Args>
 inline void launch(gps_ctx* c, int cls, dim3 grid, dim3 block, size_t smem, Kernel k, Args... args) {
     if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
+    if (c->h_arena_off > c->h_flushed) flush_uploads(c);
     bool timed = (c->prof_mask >> cls) & 1u;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timed) {

@@ -342,8 +342,9 @@ void join_sharded(Chunk& ch, QS* q, const uint32_t* ec_val, const std::function<
                     sm[2 * t] = any ? rows[3 * t + 1] - rows[3 * t] : 0;
                     sm[2 * t + 1] = any ? S + rows[3 * t + 2] : 0;
                 }
-                GPS_CK(cudaMemcpyAsync(d_send, upload(c, sm, ch.keep), sizeof(uint64_t) * 2 * N,
-                                       cudaMemcpyDeviceToDevice, c->stream));
+                const uint64_t* dsm = upload(c, sm, ch.keep);
+                flush_uploads(c);   // a plain copy (not a launch) reads the staged array
+                GPS_CK(cudaMemcpyAsync(d_send, dsm, sizeof(uint64_t) * 2 * N, cudaMemcpyDeviceToDevice, c->stream));
                 cm->allgather_u64(d_send, d_all, 2 * N, c->stream);
                 const std::vector<uint64_t> all = d2h_u64(c, d_all, 2 * (size_t)N * N);
                 uint64_t newR = 0, A = ~0ull;
@@ -428,6 +429,7 @@ void join_sharded(Chunk& ch, QS* q, const uint32_t* ec_val, const std::function<
 
 void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count_only, float thr,
                std::vector<QueryResult>& out) {
+    arena_reset(c);   // previous chunks' kernels are complete (their last step synced)
     Chunk ch;
     ch.c = c;
     ch.g = g;
@@ -760,6 +762,7 @@ void run_filter_debug(gps_ctx* c, const gps_graph* g, const gps_query* q, const 
     one.k = one.plan.k;
     one.E = (int)one.plan.arcs.size();
     for (int u = 0; u < one.k; u++) one.cap[u] = (uint32_t)std::min<uint64_t>(g->d.n, std::max<uint64_t>(1, one.plan.freq[u]));
+    arena_reset(c);
     Chunk ch;
     ch.c = c;
     ch.g = g;
