@@ -12,7 +12,12 @@
 //
 // Every query's outputs of a phase are concatenated in job order, so one global
 // scan / compaction serves the whole batch (two-step output scheme).
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -47,6 +52,30 @@ void pairs_range_host(uint64_t P, uint32_t b, uint32_t G, uint64_t& p0, uint64_t
     p0 = q * b + (b < rem ? b : rem);
     p1 = p0 + q + (b < rem ? 1 : 0);
 }
+
+// Phase tracing: NVTX ranges (visible in any CUDA profiler) and, with GPS_TRACE=1,
+// host timestamps of every phase boundary on stderr.
+struct Trace {
+    bool on = false;
+    std::chrono::steady_clock::time_point t0, last;
+    explicit Trace(const char* what, size_t nq) {
+        const char* e = std::getenv("GPS_TRACE");
+        on = e && *e == '1';
+        t0 = last = std::chrono::steady_clock::now();
+        nvtxRangePushA(what);
+        if (on) std::fprintf(stderr, "[gps] %s: %zu queries\n", what, nq);
+    }
+    void mark(const char* phase) {
+        nvtxMarkA(phase);
+        if (!on) return;
+        auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[gps]   %-28s +%8.1f us  (t=%9.1f us)\n", phase,
+                     std::chrono::duration<double, std::micro>(t - last).count(),
+                     std::chrono::duration<double, std::micro>(t - t0).count());
+        last = t;
+    }
+    ~Trace() { nvtxRangePop(); }
+};
 
 struct QS {                       // one query of a chunk
     uint32_t idx = 0;             // position in the caller's array
@@ -429,6 +458,7 @@ void join_sharded(Chunk& ch, QS* q, const uint32_t* ec_val, const std::function<
 
 void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count_only, float thr,
                std::vector<QueryResult>& out) {
+    Trace tr("gps chunk", qsv.size());
     arena_reset(c);   // previous chunks' kernels are complete (their last step synced)
     Chunk ch;
     ch.c = c;
@@ -437,7 +467,9 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
     ch.rebalance = thr;
     const DevGraph& d = g->d;
     setup_chunk(ch);
+    tr.mark("setup (arena)");
     filter_phase(ch, 2);
+    tr.mark("filter enqueued");
 
     // ---- final collect of every query vertex, sync #1 ----
     {
@@ -457,6 +489,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         }
         pinned_release(c, h, got);
     }
+    tr.mark("sync1 (|C(u)|)");
     for (QS* q : ch.qs) {
         QueryResult& r = out[q->idx];
         r.cols = (uint32_t)q->k;
@@ -530,6 +563,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         ec_values = h[nj + 1];
         pinned_release(c, h, got);
     }
+    tr.mark("sync2 (#EC)");
     if (ec_values >= (1ull << 32)) fail(GPS_EOVERFLOW, "more than 2^32 candidate edges in one batch");
     for (QS* q : ch.qs) {
         if (!q->live) continue;
@@ -545,6 +579,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
     run_ec(c, d, dej, nj, true, ctl, val.as<uint32_t>(), G);
     c->stats.k_bytes[GPS_K_EC_WRITE] += 4.0 * (double)ec_values;
     auto ec_off_of = [&](int job) { return ecoff.as<uint32_t>() + kc_off[job]; };
+    tr.mark("join order + EC write enqueued");
 
     // ---- combine_edge_candidates: one join step for all queries at a time ----
     for (QS* q : ch.qs) {
@@ -660,6 +695,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             writes = h[act.size() + 1];
             pinned_release(c, h, got);
         }
+        tr.mark(fast ? "join step synced (fast)" : "join step synced");
         if (!fast) c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)P;
         Block ob;
         if (writes) {
