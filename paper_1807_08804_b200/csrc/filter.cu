@@ -155,10 +155,10 @@ template <int MODE>   // 0: prune (mark satisfied constraints), 1: propagate
 __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
                                                  unsigned long long* bytes_acc) {
     extern __shared__ __align__(16) char s_dyn[];
-    using SM = PairSmem<ExMeta, kEW, 2>;
+    using SM = PairSmem<ExMeta, kET, kEI, kEW, 2>;
     uint64_t* s_jp = reinterpret_cast<uint64_t*>(s_dyn);          // [nj+1] job pair prefix
-    uint64_t* s_off = reinterpret_cast<uint64_t*>(s_dyn + SM::off_off(nj));
-    ExMeta* s_meta = reinterpret_cast<ExMeta*>(s_dyn + SM::meta_off(nj));
+    char* s_bufs = s_dyn + SM::buf_off(nj);
+    SM::init(s_bufs);
     job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].cnt); }, s_jp);
     uint64_t p0, p1;
     pairs_range(s_jp[nj], blockIdx.x, gridDim.x, p0, p1);
@@ -181,29 +181,29 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
             m.skip = MODE == 0 ? ((mk & bitm) != 0) : (mk != full);
             return m;
         };
-        pair_chunks<ExMeta, kET, kEI, kEW, 2>(lo, hi, (uint64_t)C, offs, load, s_meta, s_off,
-                                           [&](const bool (&v)[kEI], const ExMeta (&m)[kEI], const uint64_t (&j)[kEI]) {
+        pair_chunks<ExMeta, kET, kEI, kEW, 2>(lo, hi, (uint64_t)C, offs, load, s_bufs,
+                                           [&](const bool (&v)[kEI], const uint32_t (&wi)[kEI],
+                                               const uint32_t (&j)[kEI], const ExMeta* sm) {
             uint32_t arc[kEI];
             bool live[kEI];
 #pragma unroll
             for (int it = 0; it < kEI; it++) {
-                live[it] = v[it] && !m[it].skip;
-                arc[it] = live[it] ? __ldg(arcs + m[it].base + (uint32_t)j[it]) : 0u;
+                const ExMeta& m = sm[wi[it]];
+                live[it] = v[it] && !m.skip;
+                arc[it] = live[it] ? __ldg(arcs + m.base + j[it]) : 0u;
             }
             bool fits[kEI];
 #pragma unroll
             for (int it = 0; it < kEI; it++) {
                 const uint32_t d = arc[it] >> g.lbits;
-                fits[it] = live[it] && lab_ok(arc[it], g.lmask, J.lab) && d != m[it].key && bit_test(J.Bv, d);
+                fits[it] = live[it] && lab_ok(arc[it], g.lmask, J.lab) && d != sm[wi[it]].key && bit_test(J.Bv, d);
             }
             if (MODE == 0) {
-                uint32_t key[kEI], one[kEI];
+                uint32_t one[kEI];
 #pragma unroll
-                for (int it = 0; it < kEI; it++) {
-                    key[it] = m[it].row;
-                    one[it] = fits[it] ? 1u : 0u;
-                }
-                run_sum<kEI>(v, key, one, [&](uint32_t row, uint32_t) {
+                for (int it = 0; it < kEI; it++) one[it] = fits[it] ? 1u : 0u;
+                run_sum<kEI>(v, wi, one, [&](uint32_t w, uint32_t) {
+                    const uint32_t row = sm[w].row;
                     if (!(__ldcg(J.mask + row) & bitm)) atomicOr(J.mask + row, bitm);
                 });
             } else {
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(256) k_clear(const ClearJob* __restrict__ jobs
     }
 }
 
-static size_t ex_smem(uint32_t nj) { return PairSmem<ExMeta, kEW, 2>::bytes(nj, 0); }
+static size_t ex_smem(uint32_t nj) { return PairSmem<ExMeta, kET, kEI, kEW, 2>::bytes(nj, 0); }
 
 void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, const ClearJob* d_clear,
                uint32_t nclear) {

@@ -39,10 +39,10 @@ template <bool WRITE>
 __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict__ jobs, uint32_t nj, PassCtl ctl,
                                            uint32_t* __restrict__ val, unsigned long long* bytes_acc) {
     extern __shared__ __align__(16) char s_dyn[];
-    using SM = PairSmem<EcMeta, kPW, 2>;
+    using SM = PairSmem<EcMeta, kPT, kPI, kPW, 2>;
     uint64_t* s_jp = reinterpret_cast<uint64_t*>(s_dyn);
-    uint64_t* s_off = reinterpret_cast<uint64_t*>(s_dyn + SM::off_off(nj));
-    EcMeta* s_meta = reinterpret_cast<EcMeta*>(s_dyn + SM::meta_off(nj));
+    char* s_bufs = s_dyn + SM::buf_off(nj);
+    SM::init(s_bufs);
     job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].nkeys); }, s_jp);
     const uint64_t P = s_jp[nj];
     uint64_t p0, p1;
@@ -63,35 +63,36 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
             return m;
         };
         uint32_t jcount = 0;
-        pair_chunks<EcMeta, kPT, kPI, kPW, 2>(lo, hi, (uint64_t)*J.nkeys, offs, load, s_meta, s_off,
-                                           [&](const bool (&v)[kPI], const EcMeta (&m)[kPI], const uint64_t (&j)[kPI]) {
+        pair_chunks<EcMeta, kPT, kPI, kPW, 2>(lo, hi, (uint64_t)*J.nkeys, offs, load, s_bufs,
+                                           [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
+                                               const uint32_t (&j)[kPI], const EcMeta* sm) {
             uint32_t x[kPI], xp[kPI];
 #pragma unroll
             for (int it = 0; it < kPI; it++) {
-                x[it] = v[it] ? __ldg(arcs + m[it].base + j[it]) : 0u;
-                xp[it] = (v[it] && j[it] > 0) ? __ldg(arcs + m[it].base + j[it] - 1) : 0xffffffffu;
+                const uint32_t base = sm[wi[it]].base;
+                x[it] = v[it] ? __ldg(arcs + base + j[it]) : 0u;
+                xp[it] = (v[it] && j[it] > 0) ? __ldg(arcs + base + j[it] - 1) : 0xffffffffu;
             }
             bool pred[kPI];
 #pragma unroll
             for (int it = 0; it < kPI; it++) {
                 const uint32_t d = x[it] >> g.lbits;
                 pred[it] = false;
-                if (v[it] && lab_ok(x[it], g.lmask, J.lab) && d != m[it].key && bit_test(J.Bq, d)) {
+                if (v[it] && lab_ok(x[it], g.lmask, J.lab) && d != sm[wi[it]].key && bit_test(J.Bq, d)) {
                     // parallel arcs to the same v' (reading R5): count v' once
                     const bool dup = j[it] > 0 && (xp[it] >> g.lbits) == d && lab_ok(xp[it], g.lmask, J.lab);
                     pred[it] = !dup;
                 }
             }
             if (!WRITE) {
-                uint32_t key[kPI], one[kPI];
+                uint32_t one[kPI];
 #pragma unroll
                 for (int it = 0; it < kPI; it++) {
-                    key[it] = m[it].row;
                     one[it] = pred[it] ? 1u : 0u;
                     count += one[it];
                     jcount += one[it];
                 }
-                run_sum<kPI>(v, key, one, [&](uint32_t row, uint32_t n) { atomicAdd(J.kcnt + row, n); });
+                run_sum<kPI>(v, wi, one, [&](uint32_t w, uint32_t n) { atomicAdd(J.kcnt + sm[w].row, n); });
             } else {
                 uint32_t mine = 0;
 #pragma unroll
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
     if (bytes_acc && threadIdx.x == 0 && p1 > p0) atomicAdd(bytes_acc, (unsigned long long)(p1 - p0) * 4ull);
 }
 
-static size_t ec_smem_n(uint32_t nj) { return PairSmem<EcMeta, kPW, 2>::bytes(nj, 0); }
+static size_t ec_smem_n(uint32_t nj) { return PairSmem<EcMeta, kPT, kPI, kPW, 2>::bytes(nj, 0); }
 
 void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, bool write, PassCtl ctl,
             uint32_t* val, uint32_t G) {
@@ -292,12 +293,12 @@ struct JMeta {              // one input row of a join step
 template <bool WRITE>
 __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a) {
     extern __shared__ __align__(16) char s_dyn[];
-    using SM = PairSmem<JMeta, kJW, 1>;
+    using SM = PairSmem<JMeta, kPT, kPI, kJW, 1>;
     uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);      // [nj+1] first row of every job
-    uint64_t* s_off = reinterpret_cast<uint64_t*>(s_dyn + SM::off_off(a.nj));
-    JMeta* s_meta = reinterpret_cast<JMeta*>(s_dyn + SM::meta_off(a.nj));
+    char* s_bufs = s_dyn + SM::buf_off(a.nj);
     uint32_t* s_out = reinterpret_cast<uint32_t*>(s_dyn + SM::extra_off(a.nj));   // staged output tile
     const bool stage = WRITE && a.wout <= kStageW;
+    SM::init(s_bufs);
     for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
     if (threadIdx.x == 0) s_jr[a.nj] = a.R;
     __syncthreads();
@@ -320,8 +321,12 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
     uint64_t running = (WRITE && !a.fast) ? a.ctl.blk[blockIdx.x] : 0ull;
     bool have_base = false;
     uint64_t count = 0;
-    pair_chunks<JMeta, kPT, kPI, kJW, 1>(p0, p1, a.R, offs, load, s_meta, s_off,
-                                         [&](const bool (&v)[kPI], const JMeta (&m)[kPI], const uint64_t (&j)[kPI]) {
+    pair_chunks<JMeta, kPT, kPI, kJW, 1>(p0, p1, a.R, offs, load, s_bufs,
+                                         [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
+                                             const uint32_t (&j)[kPI], const JMeta* sm) {
+        JMeta m[kPI];
+#pragma unroll
+        for (int it = 0; it < kPI; it++) m[it] = sm[wi[it]];
         uint32_t cand[kPI];
 #pragma unroll
         for (int it = 0; it < kPI; it++) cand[it] = v[it] ? __ldg(a.ec_val + m[it].s0 + j[it]) : 0u;
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
 }
 
 static size_t join_smem(uint32_t nj, bool write) {
-    return PairSmem<JMeta, kJW, 1>::bytes(nj, write ? sizeof(uint32_t) * kPT * kPI * kStageW : 0);
+    return PairSmem<JMeta, kPT, kPI, kJW, 1>::bytes(nj, write ? sizeof(uint32_t) * kPT * kPI * kStageW : 0);
 }
 
 // Opt the join kernels in to their largest dynamic shared memory ONCE (the

@@ -39,51 +39,6 @@ __device__ __forceinline__ void pairs_range(uint64_t P, uint32_t b, uint32_t G, 
     p1 = p0 + q + (b < rem ? 1 : 0);
 }
 
-// Calls body(valid, p, row, j) for every item slot of the block's range, T*IPT
-// slots per chunk, all threads together (body may use block-wide barriers).
-// s_off must hold W+1 uint64 in shared memory.
-template <int T, int IPT, int W, typename OffF, typename Body>
-__device__ __forceinline__ void for_pairs(uint64_t p0, uint64_t p1, uint64_t nrows, OffF offs, uint64_t* s_off,
-                                          uint64_t* s_row, Body&& body) {
-    if (p0 >= p1) return;
-    const uint32_t tid = threadIdx.x;
-    if (tid == 0) *s_row = pairs_find_global(offs, 0, nrows, p0);
-    __syncthreads();
-    uint64_t r0 = *s_row;
-    for (uint64_t cp = p0; cp < p1; cp += (uint64_t)T * IPT) {
-        const uint64_t cend = cp + (uint64_t)T * IPT < p1 ? cp + (uint64_t)T * IPT : p1;
-        const uint32_t wn = (uint32_t)((nrows - r0) < (uint64_t)W ? (nrows - r0) : (uint64_t)W);
-        for (uint32_t i = tid; i <= wn; i += T) s_off[i] = offs(r0 + i);
-        __syncthreads();
-        const uint64_t wend = s_off[wn];
-#pragma unroll 1
-        for (int it = 0; it < IPT; it++) {
-            const uint64_t p = cp + (uint64_t)it * T + tid;
-            const bool v = p < cend;
-            uint64_t row = 0, base = 0;
-            if (v) {
-                if (p < wend) {
-                    const uint32_t i = pairs_find_smem(s_off, wn, p);
-                    row = r0 + i;
-                    base = s_off[i];
-                } else {
-                    row = pairs_find_global(offs, r0 + wn, nrows, p);
-                    base = offs(row);
-                }
-            }
-            body(v, p, row, p - base);
-        }
-        __syncthreads();
-        if (cend < p1) {
-            if (tid == 0)
-                *s_row = (cend < wend) ? r0 + pairs_find_smem(s_off, wn, cend)
-                                       : pairs_find_global(offs, r0 + wn, nrows, cend);
-            __syncthreads();
-            r0 = *s_row;
-        }
-    }
-}
-
 // Warp-segmented reduction for lanes holding consecutive pairs: lanes with the
 // same key form one group (keys are non-decreasing across lanes).  Returns the
 // group's OR / sum in the group's lowest lane (is_leader), 0 elsewhere.
@@ -170,80 +125,143 @@ namespace gps {
 
 // Chunked pair iteration with per-row metadata staged in shared memory.
 //
-// Per chunk of T*IPT consecutive pairs: the offsets of a window of W rows are
-// staged (coalesced), then load_meta(row) -> Meta is evaluated ONCE per row that
-// meets the chunk (in parallel) and kept in s_meta.  Thread t owns the IPT
-// CONSECUTIVE pairs cp + t*IPT + [0, IPT): one shared-memory binary search finds
-// the row of its first pair, the rest walk forward.  body(v[], m[], j[])
-// receives all IPT items at once (rows non-decreasing across the items and
-// across the threads of the block), so it can issue their global loads back to
-// back and aggregate per row.  Rows outside the window (runs of empty rows) fall
-// back to load_meta from global.  body may use block-wide barriers.
+// Per chunk of CH = T*IPT consecutive pairs [cp, cend), one pass over a window
+// of W rows starting at r0 (the row containing cp) stages, for every row that
+// meets the chunk: its start relative to cp (s_start), load_meta(row) (s_meta,
+// evaluated ONCE per row), a row-start mark at its first in-chunk pair (s_mark,
+// window index as u16), the row covering each warp's first pair (s_wrow) and the
+// row containing cend (s_next, the next chunk's r0).  After ONE block barrier,
+// thread t owns the IPT consecutive pairs cp + t*IPT + [0, IPT): the window row
+// of each is a running max over the marks, seeded by a warp max-scan and the
+// warp's s_wrow -- no per-thread search and no walk over row boundaries.  If
+// the window ends before cend the chunk is cut at the window end (every chunk
+// covers at least row r0's remainder, so no global fallback exists).
+//
+// body(v[], wi[], j[], sm) receives all IPT items at once: wi = window index of
+// the item's row (its metadata is sm[wi]; rows non-decreasing across items and
+// across the threads of the block), j = the pair's index within its row.  body
+// may use block-wide barriers.  NB = 2 double-buffers the window so a chunk
+// needs a single barrier.  Marks are cleared by the thread that read them, so
+// the buffers are clean whenever pair_chunks returns.
+template <typename Meta, int T, int IPT, int W, int NB>
+struct PairSmem {
+    static constexpr int CH = T * IPT;
+    static_assert(IPT % 4 == 0, "marks are read as 4 x u16 vectors");
+    static_assert(W <= 65535, "marks are u16 window indices");
+    static __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+    // one buffer: [start W u32][meta W][mark CH u16][wrow T/32 u32][next u32]
+    static constexpr size_t START = 0;
+    static constexpr size_t META = a16(sizeof(uint32_t) * W);
+    static constexpr size_t MARK = META + a16(sizeof(Meta) * W);
+    static constexpr size_t WROW = MARK + a16(sizeof(uint16_t) * CH);
+    static constexpr size_t NEXT = WROW + sizeof(uint32_t) * (T / 32);
+    static constexpr size_t BUF = a16(NEXT + sizeof(uint32_t));
+    static __host__ __device__ size_t buf_off(uint32_t nj) { return a16(sizeof(uint64_t) * (nj + 1)); }
+    static __host__ __device__ size_t extra_off(uint32_t nj) { return buf_off(nj) + NB * BUF; }
+    static __host__ __device__ size_t bytes(uint32_t nj, size_t extra) { return extra_off(nj) + extra; }
+    // zero the marks of every buffer (once per kernel, before the first chunk; needs a barrier after)
+    static __device__ void init(char* bufs) {
+        for (int b = 0; b < NB; b++) {
+            uint2* m = reinterpret_cast<uint2*>(bufs + b * BUF + MARK);
+            for (int i = threadIdx.x; i < CH / 4; i += blockDim.x) m[i] = make_uint2(0u, 0u);
+        }
+    }
+};
+
+// Largest r in [lo, hi) with offs(r) <= p (offs(lo) <= p): one warp, 32-ary
+// search (about log32 of the range dependent global loads instead of log2).
+template <typename OffF>
+__device__ __forceinline__ uint64_t pairs_find_warp(OffF offs, uint64_t lo, uint64_t hi, uint64_t p) {
+    const uint32_t lane = lane_id();
+    while (hi - lo > 32) {
+        const uint64_t step = (hi - lo + 31) / 32;   // probes lo + lane*step
+        const uint64_t x = lo + lane * step;
+        const bool le = x < hi && offs(x) <= p;
+        const uint32_t b = __ballot_sync(kFull, le);   // lane 0 always set (offs(lo) <= p)
+        const uint32_t last = 31 - __clz(b);
+        const uint64_t nlo = lo + last * step;
+        hi = (nlo + step < hi) ? nlo + step : hi;
+        lo = nlo;
+    }
+    const uint64_t x = lo + lane;
+    const bool le = x < hi && offs(x) <= p;
+    return lo + (31 - __clz(__ballot_sync(kFull, le)));
+}
+
 template <typename Meta, int T, int IPT, int W, int NB, typename OffF, typename LoadMeta, typename Body>
 __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t nrows, OffF offs, LoadMeta load_meta,
-                                            Meta* s_meta, uint64_t* s_off, Body&& body) {
-    // s_off holds NB*(W+1) and s_meta NB*W entries.  NB = 2 double-buffers the
-    // window, so a chunk needs ONE block barrier (between staging and use); the row
-    // of the next chunk is recomputed by every thread from the current window.
+                                            char* bufs, Body&& body) {
+    using SM = PairSmem<Meta, T, IPT, W, NB>;
+    constexpr uint32_t CH = SM::CH, WSPAN = 32 * IPT;
     if (p0 >= p1) return;
-    const uint32_t tid = threadIdx.x;
-    uint64_t r0 = pairs_find_global(offs, 0, nrows, p0);
+    const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    uint64_t r0 = pairs_find_warp(offs, 0, nrows, p0);
     int buf = 0;
-    for (uint64_t cp = p0; cp < p1; cp += (uint64_t)T * IPT, buf = (NB == 2) ? buf ^ 1 : 0) {
-        uint64_t* so = s_off + buf * (W + 1);
-        Meta* sm = s_meta + buf * W;
-        const uint64_t cend = cp + (uint64_t)T * IPT < p1 ? cp + (uint64_t)T * IPT : p1;
+    for (uint64_t cp = p0; cp < p1; buf = (NB == 2) ? buf ^ 1 : 0) {
+        char* B = bufs + buf * SM::BUF;
+        uint32_t* s_start = reinterpret_cast<uint32_t*>(B + SM::START);
+        Meta* s_meta = reinterpret_cast<Meta*>(B + SM::META);
+        uint16_t* s_mark = reinterpret_cast<uint16_t*>(B + SM::MARK);
+        uint32_t* s_wrow = reinterpret_cast<uint32_t*>(B + SM::WROW);
+        uint32_t* s_next = reinterpret_cast<uint32_t*>(B + SM::NEXT);
         const uint32_t wn = (uint32_t)((nrows - r0) < (uint64_t)W ? (nrows - r0) : (uint64_t)W);
-        for (uint32_t i = tid; i <= wn; i += T) {
-            const uint64_t a = offs(r0 + i);
-            so[i] = a;
-            if (i < wn && a < cend) {
-                const uint64_t b = offs(r0 + i + 1);
-                if (b > a) sm[i] = load_meta(r0 + i);
+        const uint64_t wend = offs(r0 + wn);
+        uint64_t cend = cp + CH < p1 ? cp + CH : p1;
+        if (cend > wend) cend = wend;   // window exhausted: cut the chunk (wend > cp: row r0 contains cp)
+        const uint32_t n = (uint32_t)(cend - cp);
+        for (uint32_t i = tid; i < wn; i += T) {
+            const uint64_t a = offs(r0 + i), b = offs(r0 + i + 1);
+            if (a < cend && b > cp && b > a) {   // a non-empty row meeting the chunk
+                const uint32_t rs = a > cp ? (uint32_t)(a - cp) : 0u;
+                const uint32_t re = (uint32_t)((b < cend ? b : cend) - cp);
+                s_start[i] = (uint32_t)(a - cp);   // mod 2^32: j = pair - start
+                if (rs) s_mark[rs] = (uint16_t)i;
+                for (uint32_t wb = (rs + WSPAN - 1) / WSPAN * WSPAN; wb < re; wb += WSPAN) s_wrow[wb / WSPAN] = i;
+                s_meta[i] = load_meta(r0 + i);
             }
+            if (a <= cend && cend < b) *s_next = i;   // the row containing cend (if inside the window)
         }
         __syncthreads();
-        const uint64_t wend = so[wn];
+        const uint32_t q0 = tid * IPT;
+        uint32_t mk[IPT];
+#pragma unroll
+        for (int x = 0; x < IPT; x += 4) {
+            uint2* mp = reinterpret_cast<uint2*>(s_mark + q0 + x);
+            const uint2 u = *mp;
+            *mp = make_uint2(0u, 0u);   // clean for this buffer's next chunk (after >= 1 barrier)
+            mk[x] = u.x & 0xffffu;
+            mk[x + 1] = u.x >> 16;
+            mk[x + 2] = u.y & 0xffffu;
+            mk[x + 3] = u.y >> 16;
+        }
+        uint32_t tmax = 0;
+#pragma unroll
+        for (int it = 0; it < IPT; it++) tmax = mk[it] > tmax ? mk[it] : tmax;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {   // inclusive warp max-scan
+            const uint32_t o = __shfl_up_sync(kFull, tmax, d);
+            if (lane >= (uint32_t)d) tmax = o > tmax ? o : tmax;
+        }
+        uint32_t run = __shfl_up_sync(kFull, tmax, 1);
+        if (lane == 0) run = 0;
+        const uint32_t ws = warp * WSPAN < n ? s_wrow[warp] : 0u;
+        run = run > ws ? run : ws;
         bool v[IPT];
-        Meta m[IPT];
-        uint64_t j[IPT];
-        const uint64_t pt = cp + (uint64_t)tid * IPT;
-        uint32_t i = (pt < cend && pt < wend) ? pairs_find_smem(so, wn, pt) : 0;
+        uint32_t wi[IPT], j[IPT];
 #pragma unroll
         for (int it = 0; it < IPT; it++) {
-            const uint64_t p = pt + it;
-            v[it] = p < cend;
-            j[it] = 0;
-            if (v[it]) {
-                if (p < wend) {
-                    while (so[i + 1] <= p) i++;
-                    m[it] = sm[i];
-                    j[it] = p - so[i];
-                } else {
-                    const uint64_t row = pairs_find_global(offs, r0 + wn, nrows, p);
-                    m[it] = load_meta(row);
-                    j[it] = p - offs(row);
-                }
-            }
+            run = mk[it] > run ? mk[it] : run;
+            v[it] = q0 + it < n;
+            wi[it] = v[it] ? run : 0u;
+            j[it] = v[it] ? q0 + it - s_start[run] : 0u;
         }
-        body(v, m, j);
-        if (cend < p1)
-            r0 = (cend < wend) ? r0 + pairs_find_smem(so, wn, cend) : pairs_find_global(offs, r0 + wn, nrows, cend);
+        body(v, wi, j, (const Meta*)s_meta);
+        if (cend < p1) r0 = (cend < wend) ? r0 + *s_next : pairs_find_warp(offs, r0 + wn - 1, nrows, cend);
+        cp = cend;
         if (NB == 1) __syncthreads();   // the single window is restaged next
     }
     if (NB == 2) __syncthreads();   // the caller may reuse the shared buffers
 }
-
-// Dynamic shared memory of a pair kernel: [job prefix (nj+1)] [offset window
-// NB*(W+1)] [row metadata NB*W] [extra].
-template <typename Meta, int W, int NB>
-struct PairSmem {
-    static __host__ __device__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
-    static __host__ __device__ size_t off_off(uint32_t nj) { return a16(sizeof(uint64_t) * (nj + 1)); }
-    static __host__ __device__ size_t meta_off(uint32_t nj) { return off_off(nj) + a16(sizeof(uint64_t) * NB * (W + 1)); }
-    static __host__ __device__ size_t extra_off(uint32_t nj) { return meta_off(nj) + a16(sizeof(Meta) * NB * W); }
-    static __host__ __device__ size_t bytes(uint32_t nj, size_t extra) { return extra_off(nj) + extra; }
-};
 
 // Per-key aggregation of a thread's IPT consecutive items (keys non-decreasing
 // across items and lanes): runs wholly inside the thread are emitted directly;
