@@ -16,8 +16,8 @@
 //                  neighbours of surviving candidates in per-neighbour scratch bitmaps
 //                  (lines 19-22).  Equal contiguous pair ranges per block replace the
 //                  paper's warp-per-candidate + block-per-hub split.
-//   k_clear        prune candidates that missed a constraint (atomicAnd on B[u]).
-//   k_bitand       reading R15: B[v] &= propagated set, scratch reset.
+//   k_post         end of a step, word-parallel: candidates that missed a constraint
+//                  leave B[u]; reading R15: B[v] &= propagated set, scratch reset.
 #include "kernels.cuh"
 #include "lookback.cuh"
 #include "pairs.cuh"
@@ -67,23 +67,34 @@ void run_check(gps_ctx* c, const DevGraph& g, const QDesc* d_q, uint32_t nq, uin
 }
 
 // -------------------------------------------------------------- a3 collect
-constexpr int kColThreads = 256;   // one bitmap word (32 vertices) per thread
+constexpr int kColThreads = 256;
+constexpr int kColWords = 4;                          // bitmap words (128 vertices) per thread
+constexpr int kColTile = kColThreads * kColWords;     // words per tile
 
 __global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const CollectJob* __restrict__ jobs,
                                                          LbScratch lb, uint32_t ntiles, uint32_t epoch) {
     const uint32_t y = blockIdx.y;
     const CollectJob& J = jobs[y];
     const uint32_t tile = lb_ticket(lb.ctr + 3 * y, ntiles);
-    const uint32_t w = tile * kColThreads + threadIdx.x;
-    const uint32_t word = w < g.nw ? J.B[w] : 0u;
-    uint32_t c = __popc(word), so = 0, si = 0;
-    if (word) {
-        const uint32_t v0 = w * 32;
-        uint32_t bits = word;
+    const uint32_t w0 = tile * kColTile + threadIdx.x * kColWords;
+    uint32_t word[kColWords];
+    if (w0 < g.nw) {   // nws >= nw rounded up to 64 words: the vector load stays in bounds
+        const uint4 b4 = *reinterpret_cast<const uint4*>(J.B + w0);
+        word[0] = b4.x;
+        word[1] = w0 + 1 < g.nw ? b4.y : 0u;
+        word[2] = w0 + 2 < g.nw ? b4.z : 0u;
+        word[3] = w0 + 3 < g.nw ? b4.w : 0u;
+    } else {
+        word[0] = word[1] = word[2] = word[3] = 0u;
+    }
+    uint32_t c = 0, so = 0, si = 0;
+#pragma unroll
+    for (int i = 0; i < kColWords; i++) {
+        c += __popc(word[i]);
+        uint32_t bits = word[i];
         while (bits) {
-            const uint32_t b = __ffs(bits) - 1;
+            const uint32_t v = (w0 + i) * 32 + __ffs(bits) - 1;
             bits &= bits - 1;
-            const uint32_t v = v0 + b;
             so += __ldg(g.off_out + v + 1) - __ldg(g.off_out + v);
             si += __ldg(g.off_in + v + 1) - __ldg(g.off_in + v);
         }
@@ -92,35 +103,42 @@ __global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const Colle
     const uint32_t ec = block_excl_scan(c, &tc);
     const uint32_t eso = block_excl_scan(so, &tso);
     const uint32_t esi = block_excl_scan(si, &tsi);
+    // the three look-backs (count, out-degree, in-degree prefixes) run in warps 0..2 concurrently
     __shared__ uint64_t s_pre[3];
-    if (threadIdx.x < 32) {
-        const size_t base = (size_t)(3 * y) * lb.max_tiles;
-        uint64_t p0 = lb_warp_lookback(lb.status + base, tile, tc, epoch);
-        uint64_t p1 = lb_warp_lookback(lb.status + base + lb.max_tiles, tile, tso, epoch);
-        uint64_t p2 = lb_warp_lookback(lb.status + base + 2 * (size_t)lb.max_tiles, tile, tsi, epoch);
-        if (threadIdx.x == 0) {
-            s_pre[0] = p0;
-            s_pre[1] = p1;
-            s_pre[2] = p2;
-        }
+    const uint32_t wid = threadIdx.x >> 5;
+    if (wid < 3) {
+        const uint64_t agg = wid == 0 ? tc : (wid == 1 ? tso : tsi);
+        const size_t base = (size_t)(3 * y + wid) * lb.max_tiles;
+        const uint64_t p = lb_warp_lookback(lb.status + base, tile, agg, epoch);
+        if ((threadIdx.x & 31u) == 0) s_pre[wid] = p;
     }
     __syncthreads();
     uint32_t rank = (uint32_t)s_pre[0] + ec;
     uint32_t ro = (uint32_t)s_pre[1] + eso;
     uint32_t ri = (uint32_t)s_pre[2] + esi;
-    if (w < g.nw) J.rp[w] = rank;
-    uint32_t bits = word;
-    while (bits) {
-        const uint32_t b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const uint32_t v = w * 32 + b;
-        J.carr[rank] = v;
-        J.seg_out[rank] = ro;
-        J.seg_in[rank] = ri;
-        if (J.mask) J.mask[rank] = 0ull;
-        ro += __ldg(g.off_out + v + 1) - __ldg(g.off_out + v);
-        ri += __ldg(g.off_in + v + 1) - __ldg(g.off_in + v);
-        rank++;
+    if (w0 < g.nw) {
+        uint32_t r[kColWords], x = rank;
+#pragma unroll
+        for (int i = 0; i < kColWords; i++) {
+            r[i] = x;
+            x += __popc(word[i]);
+        }
+        *reinterpret_cast<uint4*>(J.rp + w0) = make_uint4(r[0], r[1], r[2], r[3]);
+    }
+#pragma unroll
+    for (int i = 0; i < kColWords; i++) {
+        uint32_t bits = word[i];
+        while (bits) {
+            const uint32_t v = (w0 + i) * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            J.carr[rank] = v;
+            J.seg_out[rank] = ro;
+            J.seg_in[rank] = ri;
+            if (J.mask) J.mask[rank] = 0ull;
+            ro += __ldg(g.off_out + v + 1) - __ldg(g.off_out + v);
+            ri += __ldg(g.off_in + v + 1) - __ldg(g.off_in + v);
+            rank++;
+        }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
         const uint32_t C = (uint32_t)s_pre[0] + tc;
@@ -133,7 +151,7 @@ __global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const Colle
 
 void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32_t nj) {
     if (nj == 0) return;
-    const uint32_t ntiles = (g.nw + kColThreads - 1) / kColThreads;
+    const uint32_t ntiles = (g.nw + kColTile - 1) / kColTile;
     LbScratch lb = lb_scratch(c, 3 * nj, ntiles);
     launch(c, GPS_K_COLLECT, dim3(ntiles, nj), dim3(kColThreads), 0, k_collect, g, d_jobs, lb, ntiles,
            lb_next_epoch(c));
@@ -219,29 +237,14 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
     if (bytes_acc && threadIdx.x == 0 && p1 > p0) atomicAdd(bytes_acc, (unsigned long long)(p1 - p0) * 4ull);
 }
 
-__global__ void __launch_bounds__(256) k_clear(const ClearJob* __restrict__ jobs) {
-    const ClearJob J = jobs[blockIdx.y];
-    const uint32_t C = *J.cnt;
-    const unsigned long long full = J.nc >= 64 ? ~0ull : ((1ull << J.nc) - 1ull);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < C; i += gridDim.x * blockDim.x) {
-        if (J.mask[i] != full) {
-            const uint32_t key = J.cands[i];
-            atomicAnd(J.Bu + (key >> 5), ~(1u << (key & 31)));
-        }
-    }
-}
-
 static size_t ex_smem(uint32_t nj) { return PairSmem<ExMeta, kET, kEI, kEW, 2>::bytes(nj, 0); }
 
-void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, const ClearJob* d_clear,
-               uint32_t nclear) {
+void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj) {
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
     const uint32_t G = (uint32_t)c->nsm * 6;
     launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), ex_smem(nj), k_explore<0>, g, d_jobs, nj,
            c->d_bytes + GPS_K_EXPLORE);
-    launch(c, GPS_K_CLEAR, dim3(std::max<uint32_t>(1, (uint32_t)c->nsm * 2 / nclear + 1), nclear), dim3(256), 0,
-           k_clear, d_clear);
 }
 
 void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj) {
@@ -252,25 +255,48 @@ void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint
            c->d_bytes + GPS_K_PROPAGATE);
 }
 
-// --------------------------------------------------------------- bit-and
-__global__ void __launch_bounds__(256) k_bitand(DevGraph g, const AndJob* __restrict__ jobs,
-                                                uint32_t* const* __restrict__ xs) {
-    const AndJob& J = jobs[blockIdx.y];
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < g.nw; w += gridDim.x * blockDim.x) {
-        uint32_t v = J.B[w];
-        for (uint32_t x = J.x0; x < J.x1; x++) {
-            v &= xs[x][w];
-            xs[x][w] = 0u;
+// ------------------------------------------------------------ step end
+// One thread per 4 bitmap words of one job: the clear needs the candidates' ranks
+// (rp + popcount below the bit) to read their masks; the AND streams the scratch.
+constexpr int kPostWords = 4;
+
+__global__ void __launch_bounds__(256) k_post(DevGraph g, const PostJob* __restrict__ jobs,
+                                              uint32_t* const* __restrict__ xs) {
+    const PostJob J = jobs[blockIdx.y];
+    const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) * kPostWords;
+    if (w0 >= g.nw) return;   // nws >= nw rounded up to 64 words: the 4-word vector stays in bounds
+    uint4 b4 = *reinterpret_cast<const uint4*>(J.B + w0);
+    uint32_t b[kPostWords] = {b4.x, b4.y, b4.z, b4.w};
+    if (J.mask) {
+#pragma unroll
+        for (int i = 0; i < kPostWords; i++) {
+            if (!b[i]) continue;
+            uint32_t rank = __ldg(J.rp + w0 + i), bits = b[i], fails = 0;
+            while (bits) {
+                const uint32_t bit = bits & (0u - bits);
+                bits ^= bit;
+                if (J.mask[rank++] != J.full) fails |= bit;
+            }
+            b[i] &= ~fails;
         }
-        J.B[w] = v;
     }
+    for (uint32_t x = J.x0; x < J.x1; x++) {
+        uint4* xp = reinterpret_cast<uint4*>(xs[x] + w0);
+        const uint4 v = *xp;
+        b[0] &= v.x;
+        b[1] &= v.y;
+        b[2] &= v.z;
+        b[3] &= v.w;
+        *xp = make_uint4(0u, 0u, 0u, 0u);
+    }
+    *reinterpret_cast<uint4*>(J.B + w0) = make_uint4(b[0], b[1], b[2], b[3]);
 }
 
-void run_bitand(gps_ctx* c, const DevGraph& g, const AndJob* d_jobs, uint32_t* const* d_xs, uint32_t nj) {
+void run_post(gps_ctx* c, const DevGraph& g, const PostJob* d_jobs, uint32_t* const* d_xs, uint32_t nj) {
     if (nj == 0) return;
-    uint32_t blocks = std::min<uint32_t>((g.nw + 255) / 256, std::max<uint32_t>(1, (uint32_t)c->nsm * 4 / nj + 1));
-    launch(c, GPS_K_BITAND, dim3(blocks, nj), dim3(256), 0, k_bitand, g, d_jobs, d_xs);
-    c->stats.k_bytes[GPS_K_BITAND] += (double)g.nw * 4.0 * 4.0 * nj;
+    const uint32_t bx = (g.nw + 256 * kPostWords - 1) / (256 * kPostWords);
+    launch(c, GPS_K_BITAND, dim3(bx, nj), dim3(256), 0, k_post, g, d_jobs, d_xs);
+    c->stats.k_bytes[GPS_K_BITAND] += (double)g.nw * 4.0 * 2.0 * nj;
 }
 
 }  // namespace gps

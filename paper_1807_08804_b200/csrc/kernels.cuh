@@ -67,25 +67,23 @@ struct ExploreJob {
     uint32_t bit;           // constraint index (bit in mask)
     uint32_t nc;            // constraints of this (query, u) step (full mask = 2^nc - 1)
 };
-// prune over all (u, constraint) jobs; clear over the (u) jobs; propagate over the
-// constraints of initialisation steps
-struct ClearJob {
-    const uint32_t* cands;
-    const uint32_t* cnt;
-    const unsigned long long* mask;
-    uint32_t* Bu;
-    uint32_t nc, pad;
-};
-void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, const ClearJob* d_clear,
-               uint32_t nclear);
+// prune over all (u, constraint) jobs; propagate over the constraints of
+// initialisation steps
+void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj);
 void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj);
 
-// B &= X[x0] & ... & X[x1-1], then the scratch is zeroed.
-struct AndJob {
+// End of an explore step, one job per bitmap the step changes (word-parallel, no
+// atomics): if mask != null, the candidates (ranks from rp, taken at this step's
+// collect) that missed a constraint leave B (Alg. 2 line 18); then
+// B &= X[x0] & ... & X[x1-1] (reading R15) and that scratch is zeroed.
+struct PostJob {
     uint32_t* B;
+    const uint32_t* rp;
+    const unsigned long long* mask;
+    unsigned long long full;
     uint32_t x0, x1;
 };
-void run_bitand(gps_ctx* c, const DevGraph& g, const AndJob* d_jobs, uint32_t* const* d_xs, uint32_t nj);
+void run_post(gps_ctx* c, const DevGraph& g, const PostJob* d_jobs, uint32_t* const* d_xs, uint32_t nj);
 
 // ---- a6 collect_edge_candidates, two-step -----------------------
 // Job = (query, arc, direction).  Pass 1 counts per key (kcnt, concatenated over

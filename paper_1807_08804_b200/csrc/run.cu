@@ -181,8 +181,7 @@ void filter_phase(Chunk& ch, int stage) {
     for (size_t s = 0; s < S; s++) {
         std::vector<CollectJob> cj;
         std::vector<ExploreJob> ej, pj;
-        std::vector<ClearJob> clj;
-        std::vector<AndJob> aj;
+        std::vector<PostJob> post;
         std::vector<uint32_t*> xs;
         for (QS* q : ch.qs) {
             const Plan& p = q->plan;
@@ -211,28 +210,33 @@ void filter_phase(Chunk& ch, int stage) {
                 ej.push_back(e);
                 if (st.propagate) pj.push_back(e);
             }
-            clj.push_back(ClearJob{q->carr[u], q->cnt + u, q->mask, ch.Bp(*q, u), nc, 0});
+            const size_t pu = post.size();
+            post.push_back(PostJob{ch.Bp(*q, u), ch.rpp(*q, u), q->mask, nc >= 64 ? ~0ull : ((1ull << nc) - 1ull), 0, 0});
             if (st.propagate) {
                 std::vector<int> targets;
                 for (const Constraint& cs : st.cons)
                     if (std::find(targets.begin(), targets.end(), cs.v) == targets.end()) targets.push_back(cs.v);
                 for (int v : targets) {
-                    AndJob a{ch.Bp(*q, v), (uint32_t)xs.size(), 0};
+                    // one job per bitmap: a target equal to u (never for simple queries) shares u's job
+                    PostJob a{ch.Bp(*q, v), nullptr, nullptr, 0ull, (uint32_t)xs.size(), 0};
                     for (uint32_t i = 0; i < nc; i++)
                         if (st.cons[i].v == v) xs.push_back(ch.Xp(*q, (int)i));
                     a.x1 = (uint32_t)xs.size();
-                    aj.push_back(a);
+                    if (v == u) {
+                        post[pu].x0 = a.x0;
+                        post[pu].x1 = a.x1;
+                    } else {
+                        post.push_back(a);
+                    }
                 }
             }
         }
         if (cj.empty()) continue;
         run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
         if (ej.empty()) continue;
-        run_prune(c, d, upload(c, ej, ch.keep), (uint32_t)ej.size(), upload(c, clj, ch.keep), (uint32_t)clj.size());
-        if (!pj.empty()) {
-            run_propagate(c, d, upload(c, pj, ch.keep), (uint32_t)pj.size());
-            run_bitand(c, d, upload(c, aj, ch.keep), upload(c, xs, ch.keep), (uint32_t)aj.size());
-        }
+        run_prune(c, d, upload(c, ej, ch.keep), (uint32_t)ej.size());
+        if (!pj.empty()) run_propagate(c, d, upload(c, pj, ch.keep), (uint32_t)pj.size());
+        run_post(c, d, upload(c, post, ch.keep), xs.empty() ? nullptr : upload(c, xs, ch.keep), (uint32_t)post.size());
     }
 }
 
