@@ -146,6 +146,10 @@ __global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const Colle
         *J.cnt = C;
         J.seg_out[C] = (uint32_t)s_pre[1] + tso;
         J.seg_in[C] = (uint32_t)s_pre[2] + tsi;
+        if (J.segtot) {
+            J.segtot[0] = (uint32_t)s_pre[1] + tso;
+            J.segtot[1] = (uint32_t)s_pre[2] + tsi;
+        }
     }
 }
 

@@ -1,13 +1,11 @@
 // join.cu -- joining phase kernels (PAPER.md §"Joining Phase"), batched.
 //
-//   k_ec<W>      a6 collect_edge_candidates with the two-step output scheme (P:809,
-//                citing Mars) over the pair space (job, key u' in C(p), arc of
-//                adj_dir(u')): pass 1 (W=false) counts, per key, the distinct v' with a
-//                fitting label, v' in B[q], v' != u' (warp-aggregated atomics), per job
-//                and per block (last block scans the block counts); the per-key counts
-//                are scanned into the address of each key's first v' (the "hash table"
-//                of fig3:hashtable); pass 2 (W=true) re-examines and writes with
-//                block-scan ranks in pair order, so every key's values come out sorted.
+//   k_ec         a6 collect_edge_candidates over the pair space (job, key u' in C(p),
+//                arc of adj_dir(u')): the distinct v' with a fitting label, v' in B[q],
+//                v' != u', in pair order, with the address of each key's first v' (the
+//                "hash table" of fig3:hashtable).  The paper's two-step output
+//                scheme (citing Mars) becomes ONE pass: tiles compact in shared
+//                memory and take their output offset from a decoupled look-back.
 //   k_join_seg   a8 per input row: O(1) key lookup (bitmap rank, instead of the paper's
 //                logarithmic search P:820) -> EC segment start, and the exclusive scan of
 //                segment lengths (pair offsets) in the same single pass.
@@ -25,107 +23,141 @@ namespace gps {
 
 constexpr int kPT = 256;    // threads per block
 constexpr int kPI = 4;      // pairs per thread per chunk
-constexpr int kPW = 512;    // EC: rows of offsets staged in shared memory (double-buffered)
+constexpr int kPW = 1024;   // EC: rows staged per chunk (keys are never empty: a chunk always fits)
 constexpr int kJW = 1024;   // join: rows staged (single buffer; fan-out can be 1)
 constexpr uint32_t kStageW = 8;   // join write: stage output rows of width <= 8 in shared memory
 
 
 // ------------------------------------------------------------ a6 EC build
+// Single pass over TILES of kTile consecutive pairs of one job (tiles of all jobs
+// numbered in job order, taken in ticket order): the tile's passing values are
+// compacted in shared memory in pair order, the tile's count goes through a
+// decoupled look-back, and the tile then writes its values and the offsets of
+// the keys whose first pair it holds.  Values of a key therefore come out sorted
+// and contiguous, and the count pass + scan of the two-step scheme disappear.
+constexpr uint32_t kTile = kPT * kPI;      // pairs per chunk (and per join tile)
+constexpr uint32_t kEcTile = 4 * kTile;     // pairs per EC tile: a few chunks amortise the tile's set-up latency
+static_assert(kEcTile == kEcPairTile, "host and device EC tiling differ");
+
 struct EcMeta {             // one key row of an EC job
     uint32_t row, key, base, pad;
 };
+using EcSmem = PairSmem<EcMeta, kPT, kPI, kPW, 2>;
 
-template <bool WRITE>
-__global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict__ jobs, uint32_t nj, PassCtl ctl,
-                                           uint32_t* __restrict__ val, unsigned long long* bytes_acc) {
-    extern __shared__ __align__(16) char s_dyn[];
-    using SM = PairSmem<EcMeta, kPT, kPI, kPW, 2>;
-    uint64_t* s_jp = reinterpret_cast<uint64_t*>(s_dyn);
-    char* s_bufs = s_dyn + SM::buf_off(nj);
-    SM::init(s_bufs);
-    job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].nkeys); }, s_jp);
-    const uint64_t P = s_jp[nj];
-    uint64_t p0, p1;
-    pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
-    uint64_t running = WRITE ? ctl.blk[blockIdx.x] : 0ull;
-    uint64_t count = 0;
-    for_job_ranges(s_jp, nj, p0, p1, [&](uint32_t jj, uint64_t lo, uint64_t hi) {
-        const ECJob& J = jobs[jj];
-        const uint32_t* off = J.dir ? g.off_in : g.off_out;
-        const uint32_t* arcs = J.dir ? g.arc_in : g.arc_out;
-        auto offs = [&](uint64_t i) -> uint64_t { return (uint64_t)__ldg(J.seg + i); };
-        auto load = [&](uint64_t r) -> EcMeta {
-            EcMeta m;
-            m.row = (uint32_t)r;
-            m.key = __ldg(J.keys + r);
-            m.base = __ldg(off + m.key);
-            m.pad = 0;
-            return m;
-        };
-        uint32_t jcount = 0;
-        pair_chunks<EcMeta, kPT, kPI, kPW, 2>(lo, hi, (uint64_t)*J.nkeys, offs, load, s_bufs,
-                                           [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
-                                               const uint32_t (&j)[kPI], const EcMeta* sm) {
-            uint32_t x[kPI], xp[kPI];
-#pragma unroll
-            for (int it = 0; it < kPI; it++) {
-                const uint32_t base = sm[wi[it]].base;
-                x[it] = v[it] ? __ldg(arcs + base + j[it]) : 0u;
-                xp[it] = (v[it] && j[it] > 0) ? __ldg(arcs + base + j[it] - 1) : 0xffffffffu;
-            }
-            bool pred[kPI];
-#pragma unroll
-            for (int it = 0; it < kPI; it++) {
-                const uint32_t d = x[it] >> g.lbits;
-                pred[it] = false;
-                if (v[it] && lab_ok(x[it], g.lmask, J.lab) && d != sm[wi[it]].key && bit_test(J.Bq, d)) {
-                    // parallel arcs to the same v' (reading R5): count v' once
-                    const bool dup = j[it] > 0 && (xp[it] >> g.lbits) == d && lab_ok(xp[it], g.lmask, J.lab);
-                    pred[it] = !dup;
-                }
-            }
-            if (!WRITE) {
-                uint32_t one[kPI];
-#pragma unroll
-                for (int it = 0; it < kPI; it++) {
-                    one[it] = pred[it] ? 1u : 0u;
-                    count += one[it];
-                    jcount += one[it];
-                }
-                run_sum<kPI>(v, wi, one, [&](uint32_t w, uint32_t n) { atomicAdd(J.kcnt + sm[w].row, n); });
-            } else {
-                uint32_t mine = 0;
-#pragma unroll
-                for (int it = 0; it < kPI; it++) mine += pred[it] ? 1u : 0u;
-                uint32_t tot;
-                uint64_t pos = running + block_excl_scan(mine, &tot);
-#pragma unroll
-                for (int it = 0; it < kPI; it++)
-                    if (pred[it]) val[pos++] = x[it] >> g.lbits;
-                running += tot;
-            }
-        });
-        if (!WRITE) {
-            const uint32_t s = block_sum(jcount);
-            if (threadIdx.x == 0 && s) atomicAdd(J.total, (unsigned long long)s);
-        }
-    });
-    if (!WRITE) last_block_scan(ctl.blk, gridDim.x, ctl.done, ctl.info, P, count);
-    if (bytes_acc && threadIdx.x == 0 && p1 > p0) atomicAdd(bytes_acc, (unsigned long long)(p1 - p0) * 4ull);
+__host__ __device__ inline size_t ec_smem_n(uint32_t nj) {
+    // [tile0 of every job (nj+1) u32 -> rounded][pair buffers][values kEcTile u32][first/last key started]
+    return EcSmem::bytes(nj, sizeof(uint32_t) * kEcTile + 16);
 }
 
-static size_t ec_smem_n(uint32_t nj) { return PairSmem<EcMeta, kPT, kPI, kPW, 2>::bytes(nj, 0); }
+__global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict__ jobs, uint32_t nj, LbScratch lb,
+                                           uint32_t ntiles, uint32_t epoch, uint32_t* __restrict__ val,
+                                           unsigned long long* bytes_acc) {
+    extern __shared__ __align__(16) char s_dyn[];
+    uint32_t* s_t0 = reinterpret_cast<uint32_t*>(s_dyn);   // first tile of every job, s_t0[nj] = ntiles
+    char* s_bufs = s_dyn + EcSmem::buf_off(nj);
+    uint32_t* s_val = reinterpret_cast<uint32_t*>(s_dyn + EcSmem::extra_off(nj));
+    uint32_t* s_rows = s_val + kEcTile;   // [0] = first, [1] = last key whose first pair is in the tile
+    __shared__ uint64_t s_prefix;
+    const uint32_t t = lb_ticket(lb.ctr, ntiles);
+    for (uint32_t i = threadIdx.x; i < nj; i += blockDim.x) s_t0[i] = jobs[i].tile0;
+    if (threadIdx.x == 0) {
+        s_t0[nj] = ntiles;
+        s_rows[0] = 0xffffffffu;
+        s_rows[1] = 0u;
+    }
+    EcSmem::init(s_bufs);
+    __syncthreads();
+    uint32_t lo = 0, hi = nj;   // job of tile t: largest j with tile0 <= t
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_t0[mid] <= t) lo = mid; else hi = mid;
+    }
+    const ECJob& J = jobs[lo];
+    const uint32_t kt = t - s_t0[lo];
+    const uint32_t C = *J.nkeys;
+    const uint64_t P = __ldg(J.seg + C);
+    const uint64_t p0 = (uint64_t)kt * kEcTile, p1 = p0 + kEcTile < P ? p0 + kEcTile : P;
+    const uint32_t* off = J.dir ? g.off_in : g.off_out;
+    const uint32_t* arcs = J.dir ? g.arc_in : g.arc_out;
+    auto offs = [&](uint64_t i) -> uint64_t { return (uint64_t)__ldg(J.seg + i); };
+    auto load = [&](uint64_t r) -> EcMeta {
+        EcMeta m;
+        m.row = (uint32_t)r;
+        m.key = __ldg(J.keys + r);
+        m.base = __ldg(off + m.key);
+        m.pad = 0;
+        return m;
+    };
+    uint32_t lc = 0;   // values of the tile so far (uniform)
+    pair_chunks<EcMeta, kPT, kPI, kPW, 2>(p0, p1, (uint64_t)C, offs, load, s_bufs,
+                                       [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
+                                           const uint32_t (&j)[kPI], const EcMeta* sm) {
+        uint32_t x[kPI], xp[kPI];
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            const uint32_t base = sm[wi[it]].base;
+            x[it] = v[it] ? __ldg(arcs + base + j[it]) : 0u;
+            xp[it] = (v[it] && j[it] > 0) ? __ldg(arcs + base + j[it] - 1) : 0xffffffffu;
+        }
+        bool pred[kPI];
+        uint32_t mine = 0;
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            const uint32_t d = x[it] >> g.lbits;
+            pred[it] = false;
+            if (v[it] && lab_ok(x[it], g.lmask, J.lab) && d != sm[wi[it]].key && bit_test(J.Bq, d)) {
+                // parallel arcs to the same v' (reading R5): count v' once
+                const bool dup = j[it] > 0 && (xp[it] >> g.lbits) == d && lab_ok(xp[it], g.lmask, J.lab);
+                pred[it] = !dup;
+            }
+            mine += pred[it] ? 1u : 0u;
+        }
+        uint32_t tot;
+        uint32_t pos = lc + block_excl_scan(mine, &tot);
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            if (v[it] && j[it] == 0) {   // key starts here: tile-relative offset now, + prefix after the look-back
+                const uint32_t row = sm[wi[it]].row;
+                J.off[row] = pos;
+                atomicMin(s_rows, row);
+                atomicMax(s_rows + 1, row);
+            }
+            if (pred[it]) s_val[pos++] = x[it] >> g.lbits;
+        }
+        lc += tot;
+    });
+    if (threadIdx.x < 32) {   // pair_chunks ended with a barrier: s_val / s_rows / J.off writes are visible
+        const uint64_t pre = lb_warp_lookback(lb.status, t, lc, epoch);
+        if (threadIdx.x == 0) s_prefix = pre;
+    }
+    __syncthreads();
+    const uint64_t pre = s_prefix;
+    for (uint32_t i = threadIdx.x; i < lc; i += blockDim.x) val[pre + i] = s_val[i];
+    // every key has >= 1 pair (a candidate passed the degree check), so the keys starting in
+    // this tile are exactly [first, last]
+    const uint32_t r0 = s_rows[0], r1 = s_rows[1];
+    for (uint32_t r = r0 + threadIdx.x; r0 <= r1 && r <= r1; r += blockDim.x) J.off[r] += (uint32_t)pre;
+    if (threadIdx.x == 0) {
+        if (kt == 0) J.span[0] = pre;
+        if (p1 == P) {
+            J.span[1] = pre + lc;
+            J.off[C] = (uint32_t)(pre + lc);
+        }
+        if (bytes_acc) atomicAdd(bytes_acc, (unsigned long long)(p1 - p0) * 4ull + lc * 4ull);
+    }
+}
 
-void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, bool write, PassCtl ctl,
-            uint32_t* val, uint32_t G) {
-    if (nj == 0) return;
+void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uint32_t ntiles, uint32_t* val) {
+    if (nj == 0 || ntiles == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many EC jobs per launch");
-    if (write)
-        launch(c, GPS_K_EC_WRITE, dim3(G), dim3(kPT), ec_smem_n(nj), k_ec<true>, g, d_jobs, nj, ctl, val,
-               c->d_bytes + GPS_K_EC_WRITE);
-    else
-        launch(c, GPS_K_EC_COUNT, dim3(G), dim3(kPT), ec_smem_n(nj), k_ec<false>, g, d_jobs, nj, ctl, val,
-               c->d_bytes + GPS_K_EC_COUNT);
+    static std::once_flag once;
+    std::call_once(once, [] {
+        GPS_CK(cudaFuncSetAttribute(k_ec, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ec_smem_n(kMaxJobsPerLaunch)));
+    });
+    LbScratch lb = lb_scratch(c, 1, ntiles);
+    launch(c, GPS_K_EC_WRITE, dim3(ntiles), dim3(kPT), ec_smem_n(nj), k_ec, g, d_jobs, nj, lb, ntiles,
+           lb_next_epoch(c), val, c->d_bytes + GPS_K_EC_WRITE);
 }
 
 // ------------------------------------------------------------ a8 join step
@@ -142,119 +174,53 @@ __device__ __forceinline__ uint32_t job_of_row(const JoinJob* __restrict__ jobs,
     return lo;
 }
 
-__device__ __forceinline__ bool seg_find(const uint32_t* __restrict__ val, uint32_t lo, uint32_t hi, uint32_t t,
-                                         uint32_t* pos) {
-    while (lo < hi) {
-        uint32_t mid = (lo + hi) >> 1;
-        uint32_t v = __ldg(val + mid);
-        if (v == t) {
-            *pos = mid;
-            return true;
-        }
-        if (v < t) lo = mid + 1; else hi = mid;
-    }
-    return false;
-}
-
-template <bool FAST>
+// Per input row: O(1) key lookup -> EC segment start (s0) and the exclusive scan of
+// the segment lengths (poff, the step's pair space), one look-back pass.
 __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
                                                   uint32_t epoch) {
-    __shared__ uint64_t s_pre[3];
+    __shared__ uint64_t s_pre;
     const uint32_t tile = lb_ticket(lb.ctr, ntiles);
     const uint64_t r0 = (uint64_t)tile * kSegTile + (uint64_t)threadIdx.x * kSegRows;
-    uint32_t len[kSegRows], wc[kSegRows], ac[kSegRows];
-    uint64_t tsum = 0, wsum = 0, asum = 0;
+    uint32_t len[kSegRows];
+    uint64_t tsum = 0;
     uint32_t jb = r0 < a.R ? job_of_row(a.jobs, a.nj, r0) : 0;
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {
         const uint64_t r = r0 + i;
-        len[i] = wc[i] = ac[i] = 0;
+        len[i] = 0;
         if (r < a.R) {
             while (jb + 1 < a.nj && a.jobs[jb + 1].row0 <= r) jb++;
             const JoinJob& J = a.jobs[jb];
-            const uint32_t* row = J.M + (r - J.row0) * a.w;
-            const uint32_t key = __ldg(row + J.x_col);
+            const uint32_t key = __ldg(J.M + (r - J.row0) * a.w + J.x_col);
             const uint32_t rk = bit_rank(J.Bx, J.rpx, key);
             const uint32_t s = __ldg(J.ec_off + rk);
             len[i] = __ldg(J.ec_off + rk + 1) - s;
             a.s0[r] = s;
-            if (FAST) {
-                uint32_t excl = 0, pos;
-                for (uint32_t c = 0; c < a.w; c++) excl += seg_find(a.ec_val, s, s + len[i], __ldg(row + c), &pos);
-                ac[i] = len[i] - excl;
-                wc[i] = J.nowrite ? 0u : ac[i];
-            }
         }
         tsum += len[i];
-        wsum += wc[i];
-        asum += ac[i];
     }
-    uint64_t tot, wtot = 0, atot = 0;
+    uint64_t tot;
     const uint64_t pre = block_excl_scan(tsum, &tot);
-    uint64_t wpre = 0, apre = 0;
-    if (FAST) {
-        wpre = block_excl_scan(wsum, &wtot);
-        apre = block_excl_scan(asum, &atot);
-    }
     if (threadIdx.x < 32) {
-        uint64_t p = lb_warp_lookback(lb.status, tile, tot, epoch);
-        uint64_t pw = 0, pa = 0;
-        if (FAST) {
-            pw = lb_warp_lookback(lb.status + lb.max_tiles, tile, wtot, epoch);
-            pa = lb_warp_lookback(lb.status + 2 * (size_t)lb.max_tiles, tile, atot, epoch);
-        }
-        if (threadIdx.x == 0) {
-            s_pre[0] = p;
-            s_pre[1] = pw;
-            s_pre[2] = pa;
-        }
+        const uint64_t p = lb_warp_lookback(lb.status, tile, tot, epoch);
+        if (threadIdx.x == 0) s_pre = p;
     }
     __syncthreads();
-    uint64_t run = s_pre[0] + pre, wrun = s_pre[1] + wpre, arun = s_pre[2] + apre;
+    uint64_t run = s_pre + pre;
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {
         const uint64_t r = r0 + i;
-        if (r < a.R) {
-            a.poff[r] = run;
-            if (FAST) {
-                a.woff[r] = wrun;
-                a.aoff[r] = arun;
-            }
-        }
+        if (r < a.R) a.poff[r] = run;
         run += len[i];
-        wrun += wc[i];
-        arun += ac[i];
     }
-    if (tile == ntiles - 1 && threadIdx.x == 0) {
-        a.poff[a.R] = s_pre[0] + tot;
-        if (FAST) {
-            a.woff[a.R] = s_pre[1] + wtot;
-            a.aoff[a.R] = s_pre[2] + atot;
-        }
-    }
-}
-
-__global__ void k_join_job_totals(const __grid_constant__ JoinStep a) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= a.nj) return;
-    const uint64_t lo = a.jobs[j].row0, hi = j + 1 < a.nj ? a.jobs[j + 1].row0 : a.R;
-    *a.jobs[j].total = a.aoff[hi] - a.aoff[lo];
-}
-
-void run_join_job_totals(gps_ctx* c, const JoinStep& s) {
-    launch(c, GPS_K_JOIN_LEN, dim3((s.nj + 127) / 128), dim3(128), 0, k_join_job_totals, s);
+    if (tile == ntiles - 1 && threadIdx.x == 0) a.poff[a.R] = s_pre + tot;
 }
 
 void run_join_seg(gps_ctx* c, const JoinStep& s) {
     const uint64_t nt = (s.R + kSegTile - 1) / kSegTile;
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join table too large");
-    LbScratch lb = lb_scratch(c, 3, (uint32_t)nt);
-    if (s.fast)
-        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg<true>, s, lb, (uint32_t)nt,
-               lb_next_epoch(c));
-    else
-        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg<false>, s, lb, (uint32_t)nt,
-               lb_next_epoch(c));
+    LbScratch lb = lb_scratch(c, 1, (uint32_t)nt);
+    launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg, s, lb, (uint32_t)nt, lb_next_epoch(c));
     c->stats.k_bytes[GPS_K_JOIN_LEN] += 4.0 * s.R + 12.0 * s.R;
 }
 
@@ -285,20 +251,41 @@ __device__ __forceinline__ bool pair_ok(const JoinStep& a, const JoinJob& J, con
 
 struct JMeta {              // one input row of a join step
     const uint32_t* rowp;   // its w values
-    uint64_t r;             // its index in the step's row space
     uint32_t s0;            // start of its EC segment in ec_val
     uint32_t job;
 };
+using JoinSmem = PairSmem<JMeta, kPT, kPI, kJW, 1>;
 
-template <bool WRITE>
-__global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a) {
+// Block-wide copy of `words` staged u32 to global memory, 16-byte stores where the
+// destination allows.
+__device__ __forceinline__ void copy_out(uint32_t* __restrict__ g, const uint32_t* __restrict__ s, uint32_t words) {
+    const uint32_t head = min(words, (uint32_t)((16u - ((uintptr_t)g & 15u)) & 15u) >> 2);
+    if (threadIdx.x < head) g[threadIdx.x] = s[threadIdx.x];
+    const uint32_t body = (words - head) & ~3u;
+    uint4* g4 = reinterpret_cast<uint4*>(g + head);
+    for (uint32_t x = threadIdx.x; x < body / 4; x += blockDim.x) {
+        const uint32_t* q = s + head + 4 * x;
+        g4[x] = make_uint4(q[0], q[1], q[2], q[3]);
+    }
+    for (uint32_t x = head + body + threadIdx.x; x < words; x += blockDim.x) g[x] = s[x];
+}
+
+// MODE 0: count pass (per-job totals + per-block counts -> last-block scan);
+// MODE 1: write pass at the block offsets of the count pass;
+// MODE 2: single pass over tiles of kTile pairs in ticket order: outputs staged in
+//         shared memory, the tile's output offset from a decoupled look-back.
+template <int MODE>
+__global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
+                                              uint32_t epoch) {
     extern __shared__ __align__(16) char s_dyn[];
-    using SM = PairSmem<JMeta, kPT, kPI, kJW, 1>;
+    constexpr bool WRITE = MODE != 0;
     uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);      // [nj+1] first row of every job
-    char* s_bufs = s_dyn + SM::buf_off(a.nj);
-    uint32_t* s_out = reinterpret_cast<uint32_t*>(s_dyn + SM::extra_off(a.nj));   // staged output tile
-    const bool stage = WRITE && a.wout <= kStageW;
-    SM::init(s_bufs);
+    char* s_bufs = s_dyn + JoinSmem::buf_off(a.nj);
+    uint32_t* s_out = reinterpret_cast<uint32_t*>(s_dyn + JoinSmem::extra_off(a.nj));   // staged output rows
+    __shared__ uint64_t s_prefix;
+    const bool stage = MODE == 2 || (MODE == 1 && a.wout <= kStageW);
+    const uint32_t t = MODE == 2 ? lb_ticket(lb.ctr, ntiles) : 0u;
+    JoinSmem::init(s_bufs);
     for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
     if (threadIdx.x == 0) s_jr[a.nj] = a.R;
     __syncthreads();
@@ -308,18 +295,22 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
         m.job = pairs_find_smem(s_jr, a.nj, r);
         const JoinJob& J = a.jobs[m.job];
         m.rowp = J.M + (r - J.row0) * a.w;
-        m.r = r;
         m.s0 = __ldg(a.s0 + r);
         return m;
     };
     const uint64_t plo = a.plo, phi = a.phi == ~0ull ? offs(a.R) : a.phi;
     const uint64_t P = phi > plo ? phi - plo : 0;
     uint64_t p0, p1;
-    pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
-    p0 += plo;
-    p1 += plo;
-    uint64_t running = (WRITE && !a.fast) ? a.ctl.blk[blockIdx.x] : 0ull;
-    bool have_base = false;
+    if (MODE == 2) {
+        p0 = plo + (uint64_t)t * kTile;
+        p1 = p0 + kTile < phi ? p0 + kTile : phi;
+    } else {
+        pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
+        p0 += plo;
+        p1 += plo;
+    }
+    uint64_t running = MODE == 1 ? a.ctl.blk[blockIdx.x] : 0ull;
+    uint32_t lc = 0;        // MODE 2: output rows staged by the tile so far
     uint64_t count = 0;
     pair_chunks<JMeta, kPT, kPI, kJW, 1>(p0, p1, a.R, offs, load, s_bufs,
                                          [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
@@ -341,24 +332,17 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
                 writes[it] = valid[it] && !J.nowrite;
             }
         }
-        if (WRITE && a.fast) {
-            // closing-free step (no count pass): the chunk's first output row is
-            // woff[row] + (j - #row values in the segment prefix) of its first pair;
-            // thread 0 computes it, the staged path below does the rest
-            __shared__ uint64_t s_base;
-            if (!have_base && threadIdx.x == 0 && v[0]) {
-                uint32_t excl = 0, fp;
-                const bool nw = a.jobs[m[0].job].nowrite;   // count-only rows contribute no output rows
-                if (j[0] > 0 && !nw)
-                    for (uint32_t c = 0; c < a.w; c++)
-                        excl += seg_find(a.ec_val, m[0].s0, m[0].s0 + (uint32_t)j[0], __ldg(m[0].rowp + c), &fp);
-                s_base = __ldg(a.woff + m[0].r) + (nw ? 0 : j[0] - excl);
+        if (MODE != 1) {   // per-job output totals
+            uint32_t key[kPI], one[kPI];
+#pragma unroll
+            for (int it = 0; it < kPI; it++) {
+                key[it] = m[it].job;
+                one[it] = valid[it] ? 1u : 0u;
+                count += writes[it] ? 1u : 0u;
             }
-            if (!have_base) {   // later chunks of the block continue from `running`
-                __syncthreads();
-                running = s_base;
-                have_base = true;
-            }
+            run_sum<kPI>(v, key, one, [&](uint32_t job, uint32_t n) {
+                atomicAdd(a.jobs[job].total, (unsigned long long)n);
+            });
         }
         if (WRITE) {
             uint32_t mine = 0;
@@ -366,8 +350,8 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
             for (int it = 0; it < kPI; it++) mine += writes[it] ? 1u : 0u;
             uint32_t tot;
             const uint32_t ex = block_excl_scan(mine, &tot);
-            uint64_t pos = running + ex;   // global output row
-            uint32_t lpos = ex;            // row within the block's tile
+            uint64_t pos = running + ex;                 // MODE 1 unstaged: global output row
+            uint32_t lpos = (MODE == 2 ? lc : 0u) + ex;  // staged: row within the tile
 #pragma unroll
             for (int it = 0; it < kPI; it++) {
                 if (!writes[it]) continue;
@@ -382,32 +366,35 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
                     dst[a.w] = cand[it];
                 }
             }
-            if (stage) {
-                // the block's rows are contiguous in the output: coalesced copy of the tile
+            if (MODE == 1 && stage) {   // the block's rows are contiguous in the output
                 __syncthreads();
-                uint32_t* g = a.out + running * a.wout;
-                const uint32_t words = tot * a.wout;
-                for (uint32_t x = threadIdx.x; x < words; x += blockDim.x) g[x] = s_out[x];
+                copy_out(a.out + running * a.wout, s_out, tot * a.wout);
             }
             running += tot;
-        } else {
-            uint32_t key[kPI], one[kPI];
-#pragma unroll
-            for (int it = 0; it < kPI; it++) {
-                key[it] = m[it].job;
-                one[it] = valid[it] ? 1u : 0u;
-                count += writes[it] ? 1u : 0u;
-            }
-            run_sum<kPI>(v, key, one, [&](uint32_t job, uint32_t n) {
-                atomicAdd(a.jobs[job].total, (unsigned long long)n);
-            });
+            lc += tot;
         }
     });
-    if (!WRITE) last_block_scan(a.ctl.blk, gridDim.x, a.ctl.done, a.ctl.info, P, count);
+    if (MODE == 0) last_block_scan(a.ctl.blk, gridDim.x, a.ctl.done, a.ctl.info, P, count);
+    if (MODE == 2) {
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const uint64_t pre = lb_warp_lookback(lb.status, t, lc, epoch);
+            if (threadIdx.x == 0) s_prefix = pre;
+        }
+        __syncthreads();
+        const uint64_t pre = s_prefix;
+        copy_out(a.out + pre * a.wout, s_out, lc * a.wout);
+        if (t == ntiles - 1 && threadIdx.x == 0) {
+            a.ctl.info[0] = P;
+            a.ctl.info[1] = pre + lc;
+        }
+    }
 }
 
-static size_t join_smem(uint32_t nj, bool write) {
-    return PairSmem<JMeta, kPT, kPI, kJW, 1>::bytes(nj, write ? sizeof(uint32_t) * kPT * kPI * kStageW : 0);
+static size_t join_smem(uint32_t nj, int mode, uint32_t wout) {
+    const size_t out = mode == 2 ? sizeof(uint32_t) * kTile * wout
+                                 : (mode == 1 ? sizeof(uint32_t) * kTile * kStageW : 0);
+    return JoinSmem::bytes(nj, out);
 }
 
 // Opt the join kernels in to their largest dynamic shared memory ONCE (the
@@ -416,10 +403,12 @@ static size_t join_smem(uint32_t nj, bool write) {
 static void allow_join_smem() {
     static std::once_flag once;
     std::call_once(once, [] {
-        GPS_CK(cudaFuncSetAttribute(k_join<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)join_smem(kMaxJobsPerLaunch, false)));
-        GPS_CK(cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)join_smem(kMaxJobsPerLaunch, true)));
+        GPS_CK(cudaFuncSetAttribute(k_join<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)join_smem(kMaxJobsPerLaunch, 0, 0)));
+        GPS_CK(cudaFuncSetAttribute(k_join<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)join_smem(kMaxJobsPerLaunch, 1, 0)));
+        GPS_CK(cudaFuncSetAttribute(k_join<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)join_smem(kMaxJobsPerLaunch, 2, GPS_MAX_QV)));
     });
 }
 
@@ -454,11 +443,21 @@ void run_rows_for_ranges(gps_ctx* c, const uint64_t* poff, uint64_t R, const uin
 
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G) {
     allow_join_smem();
-    launch(c, GPS_K_JOIN_COUNT, dim3(G), dim3(kPT), join_smem(s.nj, false), k_join<false>, s);
+    launch(c, GPS_K_JOIN_COUNT, dim3(G), dim3(kPT), join_smem(s.nj, 0, s.wout), k_join<0>, s, LbScratch{}, 0u, 0u);
 }
 void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G) {
     allow_join_smem();
-    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), join_smem(s.nj, true), k_join<true>, s);
+    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), join_smem(s.nj, 1, s.wout), k_join<1>, s, LbScratch{}, 0u, 0u);
+}
+void run_join_tiles(gps_ctx* c, const JoinStep& s, uint64_t P) {
+    if (P == 0) return;
+    const uint64_t nt = (P + kTile - 1) / kTile;
+    if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join pair space too large");
+    if (s.wout > GPS_MAX_QV) fail(GPS_EINVAL, "internal: join row too wide");
+    allow_join_smem();
+    LbScratch lb = lb_scratch(c, 1, (uint32_t)nt);
+    launch(c, GPS_K_JOIN_WRITE, dim3((uint32_t)nt), dim3(kPT), join_smem(s.nj, 2, s.wout), k_join<2>, s, lb,
+           (uint32_t)nt, lb_next_epoch(c));
 }
 
 }  // namespace gps

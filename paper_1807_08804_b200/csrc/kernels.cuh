@@ -47,6 +47,7 @@ struct CollectJob {
     uint32_t* seg_out;
     uint32_t* seg_in;
     unsigned long long* mask;
+    uint32_t* segtot;       // optional [2]: seg_out[C], seg_in[C] (pair-space sizes for the host)
 };
 void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32_t nj);
 
@@ -85,27 +86,29 @@ struct PostJob {
 };
 void run_post(gps_ctx* c, const DevGraph& g, const PostJob* d_jobs, uint32_t* const* d_xs, uint32_t nj);
 
-// ---- a6 collect_edge_candidates, two-step -----------------------
-// Job = (query, arc, direction).  Pass 1 counts per key (kcnt, concatenated over
-// jobs; scanned into the key offsets) and per job (total); pass 2 writes the
-// values into one array shared by all jobs (positions = global pair order).
+// ---- a6 collect_edge_candidates, single pass -------------------
+// Job = (query, arc, direction).  The job's pair space is cut into tiles of
+// kPT*kPI pairs; tile0 = the job's first tile in the launch-wide numbering (job
+// order).  Values of all jobs go to one array in global pair order.
 struct ECJob {
     const uint32_t* keys;   // c_array of the key endpoint p
     const uint32_t* nkeys;  // device |C(p)|
     const uint32_t* seg;    // degree prefix of the keys in direction dir
     const uint32_t* Bq;     // bitmap of the value endpoint q
-    uint32_t* kcnt;         // [|C(p)|] per-key counts (zeroed by the host)
-    unsigned long long* total;  // per-job count
+    uint32_t* off;          // [|C(p)|+1] written: position of each key's first value, off[C] = end
+    unsigned long long* span;  // [2] written: first / one-past-last value position of the job
+    uint32_t tile0;
     int32_t lab;
     uint32_t dir;           // 0: values are out-neighbours of the key, 1: in-neighbours
 };
+void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uint32_t ntiles, uint32_t* val);
+constexpr uint32_t kEcPairTile = 4096;   // pairs per tile of the single-pass EC kernel
+
 struct PassCtl {             // two-step bookkeeping of one pair-space launch
     uint64_t* blk;           // [G+1] per-block counts -> exclusive offsets
     unsigned int* done;      // last-block counter
     uint64_t* info;          // [0] = pairs, [1] = written rows
 };
-void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, bool write, PassCtl ctl,
-            uint32_t* val, uint32_t G);
 
 // ---- a8 join step: count -> scan -> write ----------------
 struct CloseChk {          // fused closing arc p -> q: value(q) must be in EC(p->q)[value(p)]
@@ -142,16 +145,7 @@ struct JoinStep {
     PassCtl ctl;
     uint32_t* out;         // output rows of the writing jobs, job order
     uint64_t plo = 0, phi = ~0ull;   // pair sub-range to process (row-sharded join); phi == ~0: all pairs
-    // closing-free fast path (no job of the step has a fused closing arc): validity is
-    // injectivity only, so a row's output count is len - #(row values in its sorted
-    // segment) and the count pass disappears; woff / aoff are exclusive scans of the
-    // written / all per-row output counts (R+1 entries).
-    int fast = 0;
-    uint64_t* woff = nullptr;
-    uint64_t* aoff = nullptr;
 };
-// per-job output totals of a fast step: total[j] = aoff[row0(j+1)] - aoff[row0(j)]
-void run_join_job_totals(gps_ctx* c, const JoinStep& s);
 // Row-sharded join: for each target pair range [lo[t], hi[t]) of the local pair
 // space (poff[0..R]), the local row range [i0, i1) covering it and poff[i0]
 // (rows[3t .. 3t+2]).
@@ -160,5 +154,8 @@ void run_rows_for_ranges(gps_ctx* c, const uint64_t* poff, uint64_t R, const uin
 void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (one look-back pass)
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G);
 void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G);
+// Single pass (no count pass): P = pairs of the step (poff[R]); out must hold P rows
+// (an upper bound); per-job totals via jobs[].total, info[0] = P, info[1] = rows written.
+void run_join_tiles(gps_ctx* c, const JoinStep& s, uint64_t P);
 
 }  // namespace gps

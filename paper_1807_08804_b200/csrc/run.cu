@@ -33,6 +33,12 @@ namespace {
 constexpr size_t kAlign = 256;
 constexpr uint32_t kMaxBatch = 512;            // queries per chunk
 constexpr size_t kChunkBytes = size_t(6) << 30;  // filter arena budget per chunk
+// Largest upper-bound output block (P rows) a join step may allocate to run as one
+// pass; GPS_SINGLE_PASS_BYTES overrides (0 forces count -> write everywhere).
+double single_pass_bytes() {
+    const char* e = std::getenv("GPS_SINGLE_PASS_BYTES");
+    return e && *e ? std::atof(e) : 24.0 * (1ull << 30);
+}
 
 struct Carve {
     char* base = nullptr;
@@ -90,6 +96,7 @@ struct QS {                       // one query of a chunk
     uint32_t* cnt = nullptr;      // k counters, inside the chunk-wide counter array
     unsigned long long* mask = nullptr;
     uint32_t C[GPS_MAX_QV];
+    uint32_t P[GPS_MAX_QV][2];    // out / in pair-space size of C(u) (sum of degrees)
     bool live = true;
     int ecjob[GPS_MAX_QE][2];
     std::vector<JoinStepPlan> steps;
@@ -104,7 +111,8 @@ struct Chunk {
     const gps_graph* g;
     std::vector<QS*> qs;
     Block arena;                  // filter state of every query
-    uint32_t* cnt_all = nullptr;  // [Σ k] candidate counts, contiguous
+    uint32_t* cnt_all = nullptr;  // [Σ k] candidate counts, then [2 Σ k] out/in pair-space sizes
+    size_t ncnt = 0;
     std::vector<uint32_t> cnt_base;
     std::vector<DevPtr> keep;     // uploaded job arrays
     float rebalance = 1.10f;      // row-sharded join threshold
@@ -136,7 +144,8 @@ void carve_all(Chunk& ch, Carve& cv) {
         ch.cnt_base.push_back((uint32_t)nc);
         nc += (size_t)q->k;
     }
-    ch.cnt_all = cv.take<uint32_t>(nc);
+    ch.cnt_all = cv.take<uint32_t>(3 * nc);   // [counts (nc)][pair-space sizes out/in (2 nc)]
+    ch.ncnt = nc;
     for (size_t i = 0; i < ch.qs.size(); i++) ch.qs[i]->cnt = ch.cnt_all + ch.cnt_base[i];
     for (QS* q : ch.qs) {
         q->B = cv.take<uint32_t>((size_t)q->k * nws);
@@ -191,7 +200,7 @@ void filter_phase(Chunk& ch, int stage) {
             const FilterStep& st = s < ni ? p.init_steps[s] : p.refine_steps[s - ni];
             const int u = st.u;
             cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0], q->seg[u][1],
-                                    q->mask});
+                                    q->mask, nullptr});
             const uint32_t nc = (uint32_t)st.cons.size();
             if (nc == 0) continue;
             for (uint32_t i = 0; i < nc; i++) {
@@ -478,18 +487,26 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
     // ---- final collect of every query vertex, sync #1 ----
     {
         std::vector<CollectJob> cj;
-        for (QS* q : ch.qs)
+        for (size_t i = 0; i < ch.qs.size(); i++) {
+            QS* q = ch.qs[i];
             for (int u = 0; u < q->k; u++)
                 cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0],
-                                        q->seg[u][1], nullptr});
+                                        q->seg[u][1], nullptr, ch.cnt_all + ch.ncnt + 2 * (ch.cnt_base[i] + u)});
+        }
         run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
-        size_t nc = cj.size(), got = 0;
-        uint32_t* h = static_cast<uint32_t*>(pinned_alloc(c, nc * 4, &got));
-        GPS_CK(cudaMemcpyAsync(h, ch.cnt_all, nc * 4, cudaMemcpyDeviceToHost, c->stream));
+        const size_t nc = ch.ncnt;
+        size_t got = 0;
+        uint32_t* h = static_cast<uint32_t*>(pinned_alloc(c, nc * 12, &got));
+        GPS_CK(cudaMemcpyAsync(h, ch.cnt_all, nc * 12, cudaMemcpyDeviceToHost, c->stream));
         ctx_sync(c);
         for (size_t i = 0; i < ch.qs.size(); i++) {
             QS* q = ch.qs[i];
-            for (int u = 0; u < q->k; u++) q->C[u] = h[ch.cnt_base[i] + u];
+            for (int u = 0; u < q->k; u++) {
+                const size_t x = ch.cnt_base[i] + u;
+                q->C[u] = h[x];
+                q->P[u][0] = h[nc + 2 * x];
+                q->P[u][1] = h[nc + 2 * x + 1];
+            }
         }
         pinned_release(c, h, got);
     }
@@ -517,7 +534,8 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
     // ---- collect_edge_candidates (both directions of every arc), sync #2 ----
     std::vector<ECJob> ej;
     std::vector<uint64_t> kc_off;
-    uint64_t kc_total = 0;
+    uint64_t kc_total = 0, ec_pairs = 0;
+    uint32_t ntiles = 0;
     for (QS* q : ch.qs) {
         if (!q->live) continue;
         for (int e = 0; e < q->E; e++)
@@ -532,6 +550,12 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
                 j.Bq = ch.Bp(*q, other);
                 j.lab = a.lab;
                 j.dir = (uint32_t)dir;
+                j.tile0 = ntiles;
+                const uint64_t P = q->P[key][dir];
+                ec_pairs += P;
+                const uint64_t nt = (P + kEcPairTile - 1) / kEcPairTile;
+                if ((uint64_t)ntiles + nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "EC pair space too large");
+                ntiles += (uint32_t)nt;
                 ej.push_back(j);
                 kc_off.push_back(kc_total);
                 kc_total += (uint64_t)q->C[key] + 1;
@@ -539,36 +563,32 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
     }
     if (ej.empty()) return;
     if (ej.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: EC job list too long");
+    if (ec_pairs >= (1ull << 32)) fail(GPS_EOVERFLOW, "more than 2^32 candidate-edge pairs in one batch");
     const uint32_t nj = (uint32_t)ej.size();
     const uint32_t G = (uint32_t)c->nsm * 4;
-    DevPtr kcnt(c, sizeof(uint32_t) * (kc_total + 1));
     DevPtr ecoff(c, sizeof(uint32_t) * (kc_total + 2));
-    DevPtr jtot(c, sizeof(unsigned long long) * nj);
+    DevPtr span(c, sizeof(unsigned long long) * 2 * nj);
     DevPtr blk(c, sizeof(uint64_t) * (G + 1));
-    GPS_CK(cudaMemsetAsync(kcnt.p, 0, sizeof(uint32_t) * (kc_total + 1), c->stream));
-    GPS_CK(cudaMemsetAsync(jtot.p, 0, sizeof(unsigned long long) * nj, c->stream));
+    DevPtr val(c, sizeof(uint32_t) * (ec_pairs + 1));   // upper bound: every pair passes
     for (uint32_t j = 0; j < nj; j++) {
-        ej[j].kcnt = kcnt.as<uint32_t>() + kc_off[j];
-        ej[j].total = jtot.as<unsigned long long>() + j;
+        ej[j].off = ecoff.as<uint32_t>() + kc_off[j];
+        ej[j].span = span.as<unsigned long long>() + 2 * j;
     }
-    const ECJob* dej = upload(c, ej, ch.keep);
-    PassCtl ctl{blk.as<uint64_t>(), c->d_done + 1, c->d_info};
-    run_ec(c, d, dej, nj, false, ctl, nullptr, G);
-    scan_exclusive1<uint32_t, uint32_t>(c, kcnt.as<uint32_t>(), ecoff.as<uint32_t>(), kc_total);
+    run_ec(c, d, upload(c, ej, ch.keep), nj, ntiles, val.as<uint32_t>());
     uint64_t ec_values = 0;
     std::vector<uint64_t> ectot(nj);
     {
         size_t got = 0;
-        uint64_t* h = static_cast<uint64_t*>(pinned_alloc(c, (nj + 2) * 8, &got));
-        GPS_CK(cudaMemcpyAsync(h, jtot.p, nj * 8, cudaMemcpyDeviceToHost, c->stream));
-        GPS_CK(cudaMemcpyAsync(h + nj, c->d_info, 16, cudaMemcpyDeviceToHost, c->stream));
+        uint64_t* h = static_cast<uint64_t*>(pinned_alloc(c, 2 * nj * 8, &got));
+        GPS_CK(cudaMemcpyAsync(h, span.p, 2 * nj * 8, cudaMemcpyDeviceToHost, c->stream));
         ctx_sync(c);
-        for (uint32_t j = 0; j < nj; j++) ectot[j] = h[j];
-        ec_values = h[nj + 1];
+        for (uint32_t j = 0; j < nj; j++) {
+            ectot[j] = h[2 * j + 1] - h[2 * j];
+            ec_values = std::max<uint64_t>(ec_values, h[2 * j + 1]);
+        }
         pinned_release(c, h, got);
     }
     tr.mark("sync2 (#EC)");
-    if (ec_values >= (1ull << 32)) fail(GPS_EOVERFLOW, "more than 2^32 candidate edges in one batch");
     for (QS* q : ch.qs) {
         if (!q->live) continue;
         std::vector<uint64_t> cnts(q->E);
@@ -579,11 +599,8 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         if (!q->live) continue;
         q->steps = make_join_order(q->plan, cnts);
     }
-    DevPtr val(c, sizeof(uint32_t) * (ec_values + 1));
-    run_ec(c, d, dej, nj, true, ctl, val.as<uint32_t>(), G);
-    c->stats.k_bytes[GPS_K_EC_WRITE] += 4.0 * (double)ec_values;
     auto ec_off_of = [&](int job) { return ecoff.as<uint32_t>() + kc_off[job]; };
-    tr.mark("join order + EC write enqueued");
+    tr.mark("join order");
 
     // ---- combine_edge_candidates: one join step for all queries at a time ----
     for (QS* q : ch.qs) {
@@ -653,7 +670,6 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         if (jj.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: join job list too long");
         DevPtr s0(c, sizeof(uint32_t) * (R + 1));
         DevPtr poff(c, sizeof(uint64_t) * (R + 1));
-        DevPtr woff, aoff;
         JoinStep js{};
         js.w = w;
         js.wout = w + 1;
@@ -666,23 +682,20 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         js.poff = poff.as<uint64_t>();
         js.ctl = PassCtl{blk.as<uint64_t>(), c->d_done, c->d_info};
         run_join_seg(c, js);
-        // closing-free fast path when rows are long (pairs per row >> w): w binary searches per
-        // row then replace a count pass over every pair
-        bool fast = false;
-        if (cl.empty()) {
-            const uint64_t P0 = d2h_u64(c, js.poff + R, 1)[0];
-            fast = (double)P0 > 8.0 * (w + 1) * (double)R;
-        }
-        if (fast) {
-            woff = DevPtr(c, sizeof(uint64_t) * (R + 1));
-            aoff = DevPtr(c, sizeof(uint64_t) * (R + 1));
-            js.fast = 1;
-            js.woff = woff.as<uint64_t>();
-            js.aoff = aoff.as<uint64_t>();
-            run_join_seg(c, js);
-            run_join_job_totals(c, js);
-            GPS_CK(cudaMemcpyAsync(c->d_info, js.poff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
-            GPS_CK(cudaMemcpyAsync(c->d_info + 1, js.woff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
+        const uint64_t P0 = d2h_u64(c, js.poff + R, 1)[0];
+        bool any_write = false;
+        for (const JoinJob& x : jj) any_write |= !x.nowrite;
+        // single pass when an output block of P0 rows (an upper bound) is affordable: no
+        // count pass; else count -> exact allocation -> write
+        const bool single = !any_write || (double)P0 * 4.0 * (w + 1) <= single_pass_bytes();
+        Block ob;
+        if (single) {
+            if (any_write && P0) {
+                ob = make_block(c, sizeof(uint32_t) * P0 * (w + 1));
+                js.out = static_cast<uint32_t*>(ob->p);
+            }
+            if (P0) run_join_tiles(c, js, P0);
+            else GPS_CK(cudaMemsetAsync(c->d_info, 0, 16, c->stream));
         } else {
             run_join_count(c, js, G);
         }
@@ -699,15 +712,19 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             writes = h[act.size() + 1];
             pinned_release(c, h, got);
         }
-        tr.mark(fast ? "join step synced (fast)" : "join step synced");
-        if (!fast) c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)P;
-        Block ob;
-        if (writes) {
-            if (writes > (~0ull) / (4ull * (w + 1))) fail(GPS_EOVERFLOW, "result size overflows");
-            ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
-            js.out = static_cast<uint32_t*>(ob->p);
-            run_join_write(c, js, G);
+        tr.mark(single ? "join step synced (single pass)" : "join step synced");
+        if (single) {
             c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)P + 4.0 * (w + 1) * (double)writes;
+        } else {
+            c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)P;
+            if (writes) {
+                if (writes > (~0ull) / (4ull * (w + 1))) fail(GPS_EOVERFLOW, "result size overflows");
+                ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
+                js.out = static_cast<uint32_t*>(ob->p);
+                run_join_write(c, js, G);
+                c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)P +
+                                                      4.0 * (w + 1) * (double)writes;
+            }
         }
         uint64_t off = 0;
         for (size_t i = 0; i < act.size(); i++) {

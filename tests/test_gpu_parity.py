@@ -103,6 +103,21 @@ def test_random_corpus(ctx, seed):
     _check(ctx, ctx.load_graph(g), og, q)
 
 
+@pytest.mark.parametrize("seed", range(0, 200, 5))
+def test_random_corpus_two_pass_join(ctx, seed, monkeypatch):
+    """Same corpus with every join step forced onto count -> exact allocation -> write."""
+    monkeypatch.setenv("GPS_SINGLE_PASS_BYTES", "0")
+    g, q = _instance(seed)
+    og = oracle.OracleGraph(g)
+    try:
+        if oracle.count(og, q, limit=2_000_000) == oracle.ELIMIT:
+            pytest.skip("too many embeddings for the oracle")
+    except ValueError:
+        pytest.skip("oracle rejects the instance")
+    ctx.reset_stats()
+    _check(ctx, ctx.load_graph(g), og, q)
+
+
 @pytest.mark.parametrize("seed", range(0, 200, 7))
 def test_filter_soundness_and_monotone(ctx, seed):
     """No oracle-embedding image is ever pruned; stages only shrink the sets."""
@@ -182,6 +197,16 @@ def test_cfg2_counts_all_queries(ctx, cfg2):
     for item in data["queries"]:
         q = Query.from_json(item["query"])
         assert ctx.count(G, q) == item["oracle_count"], item["seed"]
+
+
+def test_cfg2_two_pass_join(ctx, cfg2, monkeypatch):
+    """Full-size config 2 with the count -> write join: same counts as the single-pass join."""
+    monkeypatch.setenv("GPS_SINGLE_PASS_BYTES", "0")
+    g, G, data = cfg2
+    for item in data["queries"][:20]:
+        assert ctx.count(G, Query.from_json(item["query"])) == item["oracle_count"], item["seed"]
+    item = min(data["queries"], key=lambda d: d["oracle_count"])
+    assert ctx.match(G, Query.from_json(item["query"])).shape[0] == item["oracle_count"]
 
 
 def test_cfg2_match_sets(ctx, cfg2):
@@ -290,7 +315,7 @@ def test_stats_count_launches(ctx, cfg1):
     ctx.count(G, triangle_tail())
     st = ctx.stats()
     assert st["queries"] == 1 and st["launches"] > 5
-    assert st["kernels"]["join_count"]["launches"] >= 1
+    assert st["kernels"]["join_write"]["launches"] >= 1   # single-pass join steps count and write
 
 
 # ------------------------------------------------------------ batched execution
