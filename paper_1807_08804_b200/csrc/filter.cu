@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
         };
         pair_chunks<ExMeta, kET, kEI, kEW, 2>(lo, hi, (uint64_t)C, offs, load, s_bufs,
                                            [&](const bool (&v)[kEI], const uint32_t (&wi)[kEI],
-                                               const uint32_t (&j)[kEI], const ExMeta* sm) {
+                                               const uint32_t (&j)[kEI], const ExMeta* sm, uint64_t) {
             uint32_t arc[kEI];
             bool live[kEI];
 #pragma unroll

@@ -39,10 +39,10 @@ constexpr uint32_t kTile = kPT * kPI;      // pairs per chunk (and per join tile
 constexpr uint32_t kEcTile = 4 * kTile;     // pairs per EC tile: a few chunks amortise the tile's set-up latency
 static_assert(kEcTile == kEcPairTile, "host and device EC tiling differ");
 
-struct EcMeta {             // one key row of an EC job
-    uint32_t row, key, base, pad;
+struct EcMeta {             // one key row of an EC job (row = window base + window index)
+    uint32_t key, base;
 };
-using EcSmem = PairSmem<EcMeta, kPT, kPI, kPW, 2>;
+using EcSmem = PairSmem<EcMeta, kPT, kPI, kPW, 1>;
 
 __host__ __device__ inline size_t ec_smem_n(uint32_t nj) {
     // [tile0 of every job (nj+1) u32 -> rounded][pair buffers][values kEcTile u32][first/last key started]
@@ -51,7 +51,7 @@ __host__ __device__ inline size_t ec_smem_n(uint32_t nj) {
 
 __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict__ jobs, uint32_t nj, LbScratch lb,
                                            uint32_t ntiles, uint32_t epoch, uint32_t* __restrict__ val,
-                                           unsigned long long* bytes_acc) {
+                                           uint64_t base, unsigned long long* bytes_acc) {
     extern __shared__ __align__(16) char s_dyn[];
     uint32_t* s_t0 = reinterpret_cast<uint32_t*>(s_dyn);   // first tile of every job, s_t0[nj] = ntiles
     char* s_bufs = s_dyn + EcSmem::buf_off(nj);
@@ -74,24 +74,22 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
     }
     const ECJob& J = jobs[lo];
     const uint32_t kt = t - s_t0[lo];
-    const uint32_t C = *J.nkeys;
-    const uint64_t P = __ldg(J.seg + C);
+    const uint32_t C = J.C;
+    const uint64_t P = J.P;
     const uint64_t p0 = (uint64_t)kt * kEcTile, p1 = p0 + kEcTile < P ? p0 + kEcTile : P;
     const uint32_t* off = J.dir ? g.off_in : g.off_out;
     const uint32_t* arcs = J.dir ? g.arc_in : g.arc_out;
     auto offs = [&](uint64_t i) -> uint64_t { return (uint64_t)__ldg(J.seg + i); };
     auto load = [&](uint64_t r) -> EcMeta {
         EcMeta m;
-        m.row = (uint32_t)r;
         m.key = __ldg(J.keys + r);
         m.base = __ldg(off + m.key);
-        m.pad = 0;
         return m;
     };
     uint32_t lc = 0;   // values of the tile so far (uniform)
-    pair_chunks<EcMeta, kPT, kPI, kPW, 2>(p0, p1, (uint64_t)C, offs, load, s_bufs,
+    pair_chunks<EcMeta, kPT, kPI, kPW, 1>(p0, p1, (uint64_t)C, offs, load, s_bufs,
                                        [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
-                                           const uint32_t (&j)[kPI], const EcMeta* sm) {
+                                           const uint32_t (&j)[kPI], const EcMeta* sm, uint64_t wr0) {
         uint32_t x[kPI], xp[kPI];
 #pragma unroll
         for (int it = 0; it < kPI; it++) {
@@ -117,7 +115,7 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
 #pragma unroll
         for (int it = 0; it < kPI; it++) {
             if (v[it] && j[it] == 0) {   // key starts here: tile-relative offset now, + prefix after the look-back
-                const uint32_t row = sm[wi[it]].row;
+                const uint32_t row = (uint32_t)wr0 + wi[it];
                 J.off[row] = pos;
                 atomicMin(s_rows, row);
                 atomicMax(s_rows + 1, row);
@@ -126,12 +124,13 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
         }
         lc += tot;
     });
-    if (threadIdx.x < 32) {   // pair_chunks ended with a barrier: s_val / s_rows / J.off writes are visible
+    __syncthreads();   // s_val / s_rows / J.off writes of the last chunk
+    if (threadIdx.x < 32) {
         const uint64_t pre = lb_warp_lookback(lb.status, t, lc, epoch);
         if (threadIdx.x == 0) s_prefix = pre;
     }
     __syncthreads();
-    const uint64_t pre = s_prefix;
+    const uint64_t pre = s_prefix + base;
     for (uint32_t i = threadIdx.x; i < lc; i += blockDim.x) val[pre + i] = s_val[i];
     // every key has >= 1 pair (a candidate passed the degree check), so the keys starting in
     // this tile are exactly [first, last]
@@ -147,7 +146,8 @@ __global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict_
     }
 }
 
-void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uint32_t ntiles, uint32_t* val) {
+void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uint32_t ntiles, uint32_t* val,
+            uint64_t base) {
     if (nj == 0 || ntiles == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many EC jobs per launch");
     static std::once_flag once;
@@ -157,7 +157,7 @@ void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uin
     });
     LbScratch lb = lb_scratch(c, 1, ntiles);
     launch(c, GPS_K_EC_WRITE, dim3(ntiles), dim3(kPT), ec_smem_n(nj), k_ec, g, d_jobs, nj, lb, ntiles,
-           lb_next_epoch(c), val, c->d_bytes + GPS_K_EC_WRITE);
+           lb_next_epoch(c), val, base, c->d_bytes + GPS_K_EC_WRITE);
 }
 
 // ------------------------------------------------------------ a8 join step
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
     uint64_t count = 0;
     pair_chunks<JMeta, kPT, kPI, kJW, 1>(p0, p1, a.R, offs, load, s_bufs,
                                          [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
-                                             const uint32_t (&j)[kPI], const JMeta* sm) {
+                                             const uint32_t (&j)[kPI], const JMeta* sm, uint64_t) {
         JMeta m[kPI];
 #pragma unroll
         for (int it = 0; it < kPI; it++) m[it] = sm[wi[it]];

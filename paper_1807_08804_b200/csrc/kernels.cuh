@@ -97,11 +97,15 @@ struct ECJob {
     const uint32_t* Bq;     // bitmap of the value endpoint q
     uint32_t* off;          // [|C(p)|+1] written: position of each key's first value, off[C] = end
     unsigned long long* span;  // [2] written: first / one-past-last value position of the job
+    uint64_t P;             // pair-space size (host copy of seg[C])
+    uint32_t C;             // host copy of |C(p)|
     uint32_t tile0;
     int32_t lab;
     uint32_t dir;           // 0: values are out-neighbours of the key, 1: in-neighbours
 };
-void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uint32_t ntiles, uint32_t* val);
+// values are written at val[base + launch-wide position]; off / span hold absolute positions
+void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uint32_t ntiles, uint32_t* val,
+            uint64_t base);
 constexpr uint32_t kEcPairTile = 4096;   // pairs per tile of the single-pass EC kernel
 
 struct PassCtl {             // two-step bookkeeping of one pair-space launch

@@ -137,9 +137,9 @@ namespace gps {
 // the window ends before cend the chunk is cut at the window end (every chunk
 // covers at least row r0's remainder, so no global fallback exists).
 //
-// body(v[], wi[], j[], sm) receives all IPT items at once: wi = window index of
-// the item's row (its metadata is sm[wi]; rows non-decreasing across items and
-// across the threads of the block), j = the pair's index within its row.  body
+// body(v[], wi[], j[], sm, r0) receives all IPT items at once: wi = window index
+// of the item's row (row r0 + wi, metadata sm[wi]; rows non-decreasing across
+// items and across the threads of the block), j = the pair's index within its row.  body
 // may use block-wide barriers.  NB = 2 double-buffers the window so a chunk
 // needs a single barrier.  Marks are cleared by the thread that read them, so
 // the buffers are clean whenever pair_chunks returns.
@@ -255,7 +255,7 @@ __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t n
             wi[it] = v[it] ? run : 0u;
             j[it] = v[it] ? q0 + it - s_start[run] : 0u;
         }
-        body(v, wi, j, (const Meta*)s_meta);
+        body(v, wi, j, (const Meta*)s_meta, r0);
         if (cend < p1) r0 = (cend < wend) ? r0 + *s_next : pairs_find_warp(offs, r0 + wn - 1, nrows, cend);
         cp = cend;
         if (NB == 1) __syncthreads();   // the single window is restaged next

@@ -172,7 +172,8 @@ Plan make_plan(const gps_query* q, uint32_t n, bool undirected, const std::vecto
     return p;
 }
 
-std::vector<JoinStepPlan> make_join_order(const Plan& p, const std::vector<uint64_t>& ec) {
+std::vector<JoinStepPlan> make_join_order(const Plan& p, const std::vector<uint64_t>& ec,
+                                          const std::vector<int>& seed_dir) {
     std::vector<JoinStepPlan> steps;
     const int E = (int)p.arcs.size();
     if (E == 0) return steps;
@@ -191,9 +192,9 @@ std::vector<JoinStepPlan> make_join_order(const Plan& p, const std::vector<uint6
     {
         JoinStepPlan st;
         st.arc = seed;
-        st.key = p.arcs[seed].a;
-        st.nv = p.arcs[seed].b;
-        st.key_dir = 0;
+        st.key_dir = seed_dir.empty() ? 0 : seed_dir[seed];
+        st.key = st.key_dir ? p.arcs[seed].b : p.arcs[seed].a;
+        st.nv = st.key_dir ? p.arcs[seed].a : p.arcs[seed].b;
         used[seed] = 1;
         vis |= 1u << p.arcs[seed].a;
         vis |= 1u << p.arcs[seed].b;

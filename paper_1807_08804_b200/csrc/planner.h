@@ -64,7 +64,9 @@ struct JoinStepPlan {
     std::vector<int> closing;  // arcs fused into this step (both endpoints visited after it)
 };
 
-// Join order from per-arc candidate-edge counts.
-std::vector<JoinStepPlan> make_join_order(const Plan& p, const std::vector<uint64_t>& ec_count);
+// Join order from per-arc candidate-edge counts.  seed_dir[e]: the
+// direction the seed arc is keyed by if e becomes the seed (the one already built).
+std::vector<JoinStepPlan> make_join_order(const Plan& p, const std::vector<uint64_t>& ec_count,
+                                          const std::vector<int>& seed_dir);
 
 }  // namespace gps

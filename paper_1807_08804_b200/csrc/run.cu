@@ -279,6 +279,24 @@ std::vector<uint64_t> d2h_u64(gps_ctx* c, const uint64_t* d, size_t n) {
     return v;
 }
 
+// A fused closing arc a -> b checks value(tgt) in EC[value(key)] through whichever
+// direction of the arc was materialised (dir 0: keyed by a, dir 1: keyed by b).
+CloseChk make_close(const Chunk& ch, const QS& q, int ci, int nv,
+                    const std::function<const uint32_t*(int)>& ec_off_of) {
+    const QArc& a = q.plan.arcs[ci];
+    const int dir = q.ecjob[ci][0] >= 0 ? 0 : 1;
+    const int key = dir ? a.b : a.a, tgt = dir ? a.a : a.b;
+    CloseChk x{};
+    x.key_new = key == nv;
+    x.key_col = x.key_new ? 0u : (uint32_t)q.col_of[key];
+    x.tgt_new = tgt == nv;
+    x.tgt_col = x.tgt_new ? 0u : (uint32_t)q.col_of[tgt];
+    x.Bk = ch.Bp(q, key);
+    x.rpk = ch.rpp(q, key);
+    x.off = ec_off_of(q.ecjob[ci][dir]);
+    return x;
+}
+
 // Row-sharded join of ONE query across the ranks of c->comm.  The
 // seed table is replicated, so its pair space is split evenly by pair index.  From
 // then on every rank extends its own rows; each step all-gathers the per-rank pair
@@ -313,18 +331,7 @@ void join_sharded(Chunk& ch, QS* q, const uint32_t* ec_val, const std::function<
         j.total = jt.as<unsigned long long>();
         j.x_col = (uint32_t)q->col_of[st.key];
         std::vector<CloseChk> cl;
-        for (int ci : st.closing) {
-            const QArc& a = q->plan.arcs[ci];
-            CloseChk x{};
-            x.key_new = a.a == st.nv;
-            x.key_col = x.key_new ? 0u : (uint32_t)q->col_of[a.a];
-            x.tgt_new = a.b == st.nv;
-            x.tgt_col = x.tgt_new ? 0u : (uint32_t)q->col_of[a.b];
-            x.Bk = ch.Bp(*q, a.a);
-            x.rpk = ch.rpp(*q, a.a);
-            x.off = ec_off_of(q->ecjob[ci][0]);
-            cl.push_back(x);
-        }
+        for (int ci : st.closing) cl.push_back(make_close(ch, *q, ci, st.nv, ec_off_of));
         j.nclose = (uint32_t)cl.size();
         j.final_ = last ? 1u : 0u;
         j.nowrite = (last && count_only) ? 1u : 0u;
@@ -531,74 +538,100 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         }
     }
 
-    // ---- collect_edge_candidates (both directions of every arc), sync #2 ----
+    // ---- collect_edge_candidates, sync #2 ----
+    // Pass 1 materialises every arc in its cheaper direction (smaller pair space); the
+    // count is the same in both, so the join order can be planned from it.  Pass 2
+    // adds the other direction only for arcs the join extends from their target.
     std::vector<ECJob> ej;
     std::vector<uint64_t> kc_off;
     uint64_t kc_total = 0, ec_pairs = 0;
     uint32_t ntiles = 0;
+    auto add_ec = [&](QS* q, int e, int dir) {
+        const QArc& a = q->plan.arcs[e];
+        const int key = dir ? a.b : a.a, other = dir ? a.a : a.b;
+        q->ecjob[e][dir] = (int)ej.size();
+        ECJob j{};
+        j.keys = q->carr[key];
+        j.nkeys = q->cnt + key;
+        j.seg = q->seg[key][dir];
+        j.Bq = ch.Bp(*q, other);
+        j.lab = a.lab;
+        j.dir = (uint32_t)dir;
+        j.tile0 = ntiles;
+        j.P = q->P[key][dir];
+        j.C = q->C[key];
+        ec_pairs += j.P;
+        const uint64_t nt = (j.P + kEcPairTile - 1) / kEcPairTile;
+        if ((uint64_t)ntiles + nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "EC pair space too large");
+        ntiles += (uint32_t)nt;
+        ej.push_back(j);
+        kc_off.push_back(kc_total);
+        kc_total += (uint64_t)q->C[key] + 1;
+    };
+    uint64_t both_dirs = 0;   // value capacity: every pair of both directions (upper bound)
     for (QS* q : ch.qs) {
         if (!q->live) continue;
-        for (int e = 0; e < q->E; e++)
-            for (int dir = 0; dir < 2; dir++) {
-                const QArc& a = q->plan.arcs[e];
-                const int key = dir ? a.b : a.a, other = dir ? a.a : a.b;
-                q->ecjob[e][dir] = (int)ej.size();
-                ECJob j{};
-                j.keys = q->carr[key];
-                j.nkeys = q->cnt + key;
-                j.seg = q->seg[key][dir];
-                j.Bq = ch.Bp(*q, other);
-                j.lab = a.lab;
-                j.dir = (uint32_t)dir;
-                j.tile0 = ntiles;
-                const uint64_t P = q->P[key][dir];
-                ec_pairs += P;
-                const uint64_t nt = (P + kEcPairTile - 1) / kEcPairTile;
-                if ((uint64_t)ntiles + nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "EC pair space too large");
-                ntiles += (uint32_t)nt;
-                ej.push_back(j);
-                kc_off.push_back(kc_total);
-                kc_total += (uint64_t)q->C[key] + 1;
-            }
+        for (int e = 0; e < q->E; e++) {
+            const QArc& a = q->plan.arcs[e];
+            q->ecjob[e][0] = q->ecjob[e][1] = -1;
+            add_ec(q, e, q->P[a.b][1] < q->P[a.a][0] ? 1 : 0);
+            both_dirs += (uint64_t)q->P[a.a][0] + q->P[a.b][1];
+        }
     }
     if (ej.empty()) return;
-    if (ej.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: EC job list too long");
-    if (ec_pairs >= (1ull << 32)) fail(GPS_EOVERFLOW, "more than 2^32 candidate-edge pairs in one batch");
-    const uint32_t nj = (uint32_t)ej.size();
+    if (both_dirs >= (1ull << 32)) fail(GPS_EOVERFLOW, "more than 2^32 candidate-edge pairs in one batch");
     const uint32_t G = (uint32_t)c->nsm * 4;
-    DevPtr ecoff(c, sizeof(uint32_t) * (kc_total + 2));
-    DevPtr span(c, sizeof(unsigned long long) * 2 * nj);
+    // key offsets: capacity for both directions of every arc
+    uint64_t kc_cap = 0;
+    for (QS* q : ch.qs)
+        if (q->live)
+            for (int e = 0; e < q->E; e++) kc_cap += (uint64_t)q->C[q->plan.arcs[e].a] + q->C[q->plan.arcs[e].b] + 2;
+    DevPtr ecoff(c, sizeof(uint32_t) * (kc_cap + 2));
+    DevPtr span(c, sizeof(unsigned long long) * 2 * (2 * ej.size()));
     DevPtr blk(c, sizeof(uint64_t) * (G + 1));
-    DevPtr val(c, sizeof(uint32_t) * (ec_pairs + 1));   // upper bound: every pair passes
-    for (uint32_t j = 0; j < nj; j++) {
-        ej[j].off = ecoff.as<uint32_t>() + kc_off[j];
-        ej[j].span = span.as<unsigned long long>() + 2 * j;
-    }
-    run_ec(c, d, upload(c, ej, ch.keep), nj, ntiles, val.as<uint32_t>());
+    DevPtr val(c, sizeof(uint32_t) * (both_dirs + 1));
+    auto launch_ec = [&](size_t j0, uint64_t base) {
+        const uint32_t nj = (uint32_t)(ej.size() - j0);
+        if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: EC job list too long");
+        for (size_t j = j0; j < ej.size(); j++) {
+            ej[j].off = ecoff.as<uint32_t>() + kc_off[j];
+            ej[j].span = span.as<unsigned long long>() + 2 * j;
+        }
+        std::vector<ECJob> part(ej.begin() + j0, ej.end());
+        run_ec(c, d, upload(c, part, ch.keep), nj, ntiles, val.as<uint32_t>(), base);
+    };
+    launch_ec(0, 0);
+    const size_t nj1 = ej.size();
     uint64_t ec_values = 0;
-    std::vector<uint64_t> ectot(nj);
+    std::vector<uint64_t> ectot(nj1);
     {
         size_t got = 0;
-        uint64_t* h = static_cast<uint64_t*>(pinned_alloc(c, 2 * nj * 8, &got));
-        GPS_CK(cudaMemcpyAsync(h, span.p, 2 * nj * 8, cudaMemcpyDeviceToHost, c->stream));
+        uint64_t* h = static_cast<uint64_t*>(pinned_alloc(c, 2 * nj1 * 8, &got));
+        GPS_CK(cudaMemcpyAsync(h, span.p, 2 * nj1 * 8, cudaMemcpyDeviceToHost, c->stream));
         ctx_sync(c);
-        for (uint32_t j = 0; j < nj; j++) {
+        for (size_t j = 0; j < nj1; j++) {
             ectot[j] = h[2 * j + 1] - h[2 * j];
             ec_values = std::max<uint64_t>(ec_values, h[2 * j + 1]);
         }
         pinned_release(c, h, got);
     }
     tr.mark("sync2 (#EC)");
+    ntiles = 0;
     for (QS* q : ch.qs) {
         if (!q->live) continue;
         std::vector<uint64_t> cnts(q->E);
+        std::vector<int> mdir(q->E);
         for (int e = 0; e < q->E; e++) {
-            cnts[e] = ectot[q->ecjob[e][0]];
+            mdir[e] = q->ecjob[e][0] >= 0 ? 0 : 1;
+            cnts[e] = ectot[q->ecjob[e][mdir[e]]];
             if (cnts[e] == 0) q->live = false;   // an edge with no candidate edge: no match
         }
         if (!q->live) continue;
-        q->steps = make_join_order(q->plan, cnts);
+        q->steps = make_join_order(q->plan, cnts, mdir);
+        for (const JoinStepPlan& st : q->steps)
+            if (q->ecjob[st.arc][st.key_dir] < 0) add_ec(q, st.arc, st.key_dir);
     }
+    if (ej.size() > nj1) launch_ec(nj1, ec_values);
     auto ec_off_of = [&](int job) { return ecoff.as<uint32_t>() + kc_off[job]; };
     tr.mark("join order");
 
@@ -644,18 +677,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             j.total = jt.as<unsigned long long>() + i;
             j.x_col = (uint32_t)q->col_of[st.key];
             j.close0 = (uint32_t)cl.size();
-            for (int ci : st.closing) {
-                const QArc& a = q->plan.arcs[ci];   // closing arcs use their source-keyed table
-                CloseChk x{};
-                x.key_new = a.a == st.nv;
-                x.key_col = x.key_new ? 0u : (uint32_t)q->col_of[a.a];
-                x.tgt_new = a.b == st.nv;
-                x.tgt_col = x.tgt_new ? 0u : (uint32_t)q->col_of[a.b];
-                x.Bk = ch.Bp(*q, a.a);
-                x.rpk = ch.rpp(*q, a.a);
-                x.off = ec_off_of(q->ecjob[ci][0]);
-                cl.push_back(x);
-            }
+            for (int ci : st.closing) cl.push_back(make_close(ch, *q, ci, st.nv, ec_off_of));
             j.nclose = (uint32_t)st.closing.size();
             const bool last = s + 1 == q->steps.size();
             j.final_ = last ? 1u : 0u;
