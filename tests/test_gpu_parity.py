@@ -11,6 +11,8 @@ import os
 import numpy as np
 import pytest
 
+import corpus
+import filter_ref
 from oracle import oracle
 from synth import (DataGraph, Query, bfs_query, config_graph, fixture_fig3_example,
                    random_connected_query, random_multigraph, triangle_tail)
@@ -70,23 +72,7 @@ def test_fig3_example(ctx):
 
 # ------------------------------------------------------------- random corpus
 def _instance(seed):
-    rng = np.random.default_rng(10_000 + seed)
-    n = int(rng.integers(20, 301))
-    deg = float(rng.uniform(1.5, 8.0))
-    undirected = seed % 4 == 0
-    g = random_multigraph(n, int(n * deg / (2 if undirected else 1)), n_elabels=int(rng.integers(1, 5)),
-                          n_vlabels=int(rng.integers(1, 21)), seed=seed, undirected=undirected,
-                          self_loops=seed % 3 == 0, dup_prob=0.1)
-    k = int(rng.integers(4, 9))
-    if seed % 5 == 4:
-        q = random_connected_query(rng, min(k, 6), extra=int(rng.integers(0, 4)),
-                                   n_elabels=int(g.elab.max()) + 1 if g.elab is not None else 1,
-                                   n_vlabels=int(g.vlab.max()) + 1, p_wild_v=0.6, p_wild_e=0.6,
-                                   bound_choices=list(range(n)), p_bound=0.1)
-    else:
-        q = bfs_query(g, min(k, n), seed, induced=seed % 2 == 0, p_wild_v=float(rng.uniform(0, 1)),
-                      keep_elabels=seed % 3 != 1, bind_seed=seed % 7 == 3, max_children=int(rng.integers(0, 3)))
-    return g, q
+    return corpus.instance(seed)
 
 
 @pytest.mark.parametrize("seed", range(200))
@@ -135,6 +121,25 @@ def test_filter_soundness_and_monotone(ctx, seed):
         if prev is not None:
             assert not (c & ~prev).any()
         prev = c
+
+
+@pytest.mark.parametrize("seed", range(0, 200, 3))
+def test_filter_sets_equal_reference(gps, ctx, seed):
+    """Candidate bitmaps after check / initialisation / refinement == tests/filter_ref.py exactly,
+    and the visit order O == the reference planner's."""
+    g, q = _instance(seed)
+    G = ctx.load_graph(g)
+    try:
+        order, _ = ctx.plan(G, q)
+    except Exception:
+        pytest.skip("planner rejects the instance")
+    assert order == filter_ref.plan(g, q)[0]
+    for stage in (0, 1, 2):
+        assert np.array_equal(ctx.candidates(G, q, stage), filter_ref.candidates(g, q, stage)), stage
+    for rounds, rev, low in [(0, 1, 1), (2, 0, 2), (1, 1, 0)]:
+        o = gps.default_opts(refine_rounds=rounds, reverse_refine=rev, lowconn_threshold=low)
+        want = filter_ref.candidates(g, q, 2, refine_rounds=rounds, reverse_refine=bool(rev), lowconn_threshold=low)
+        assert np.array_equal(ctx.candidates(G, q, 2, o), want), (rounds, rev, low)
 
 
 @pytest.mark.parametrize("rounds,rev,low", [(0, 1, 1), (1, 0, 1), (3, 1, 1), (1, 1, 0), (2, 0, 2)])
