@@ -10,14 +10,14 @@
 //                  look-back (one pass), also emitting the per-word rank prefix (O(1) key
 //                  lookup) and the candidates' degree prefixes (the pair spaces of
 //                  explore and EC).
-//   k_explore<M>   a4/a5 kernel_explore (Alg. 2 lines 14-22) over the PAIR
-//                  space (job, candidate u', constraint, arc of adj_dir(u')): M=prune marks
-//                  the constraints u' satisfies (lines 15-18), M=propagate sets the fitting
-//                  neighbours of surviving candidates in per-neighbour scratch bitmaps
-//                  (lines 19-22).  Equal contiguous pair ranges per block replace the
-//                  paper's warp-per-candidate + block-per-hub split.
-//   k_post         end of a step, word-parallel: candidates that missed a constraint
-//                  leave B[u]; reading R15: B[v] &= propagated set, scratch reset.
+//   k_explore      a4/a5 kernel_explore (Alg. 2 lines 14-22) over the PAIR
+//                  space of each constraint job, walked from whichever side (the set being
+//                  filtered, or the set it must reach) has fewer pairs; it writes the
+//                  satisfying members as a bitmap.  Prune (lines 15-18) and propagation
+//                  (lines 19-22) are the same job with the roles swapped.  Equal contiguous
+//                  pair ranges per block replace the paper's warp-per-candidate +
+//                  block-per-hub split.
+//   k_post         word-parallel B &= (AND of the jobs' X bitmaps), scratch reset.
 #include "kernels.cuh"
 #include "lookback.cuh"
 #include "pairs.cuh"
@@ -134,7 +134,6 @@ __global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const Colle
             J.carr[rank] = v;
             J.seg_out[rank] = ro;
             J.seg_in[rank] = ri;
-            if (J.mask) J.mask[rank] = 0ull;
             ro += __ldg(g.off_out + v + 1) - __ldg(g.off_out + v);
             ri += __ldg(g.off_in + v + 1) - __ldg(g.off_in + v);
             rank++;
@@ -169,38 +168,48 @@ constexpr int kET = 256;
 constexpr int kEI = 8;
 constexpr int kEW = 512;
 
-struct ExMeta {             // one candidate row of an explore job, staged per chunk
-    uint32_t row, key, base, skip;
+struct ExMeta {             // one row (key vertex) of an explore job, staged per chunk
+    uint32_t key, base, skip, pad;
 };
+using ExSmem = PairSmem<ExMeta, kET, kEI, kEW, 2>;
 
-template <int MODE>   // 0: prune (mark satisfied constraints), 1: propagate
+__device__ __forceinline__ uint64_t ex_pairs(const ExploreJob& J, bool* s_side) {
+    const uint64_t pa = J.candA ? (uint64_t)__ldg(J.segA + *J.cntA) : ~0ull;
+    const uint64_t ps = J.candS ? (uint64_t)__ldg(J.segS + *J.cntS) : ~0ull;
+    *s_side = ps < pa;
+    return ps < pa ? ps : pa;
+}
+
 __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
-                                                 unsigned long long* bytes_acc) {
+                                                unsigned long long* bytes_acc) {
     extern __shared__ __align__(16) char s_dyn[];
-    using SM = PairSmem<ExMeta, kET, kEI, kEW, 2>;
     uint64_t* s_jp = reinterpret_cast<uint64_t*>(s_dyn);          // [nj+1] job pair prefix
-    char* s_bufs = s_dyn + SM::buf_off(nj);
-    SM::init(s_bufs);
-    job_prefix(nj, [&](uint32_t j) -> uint64_t { return __ldg(jobs[j].seg + *jobs[j].cnt); }, s_jp);
+    char* s_bufs = s_dyn + ExSmem::buf_off(nj);
+    ExSmem::init(s_bufs);
+    job_prefix(nj, [&](uint32_t j) -> uint64_t { bool sd; return ex_pairs(jobs[j], &sd); }, s_jp);
     uint64_t p0, p1;
     pairs_range(s_jp[nj], blockIdx.x, gridDim.x, p0, p1);
     for_job_ranges(s_jp, nj, p0, p1, [&](uint32_t jj, uint64_t lo, uint64_t hi) {
         const ExploreJob J = jobs[jj];             // by value: fields stay in registers across atomics
-        const uint32_t C = *J.cnt;
-        const uint32_t* off = J.dir ? g.off_in : g.off_out;
-        const uint32_t* arcs = J.dir ? g.arc_in : g.arc_out;
-        const unsigned long long bitm = 1ull << J.bit;
-        const unsigned long long full = J.nc >= 64 ? ~0ull : ((1ull << J.nc) - 1ull);
-        auto offs = [&](uint64_t i) -> uint64_t { return (uint64_t)__ldg(J.seg + i); };
+        bool sside;
+        ex_pairs(J, &sside);                       // uniform per job
+        // rows: keys of the walked side; arcs of direction dir (A-side) or 1 - dir (S-side)
+        const bool in = sside ? J.dir == 0 : J.dir != 0;
+        const uint32_t* off = in ? g.off_in : g.off_out;
+        const uint32_t* arcs = in ? g.arc_in : g.arc_out;
+        const uint32_t* cand = sside ? J.candS : J.candA;
+        const uint32_t* seg = sside ? J.segS : J.segA;
+        const uint32_t* Bkey = sside ? J.BS : J.BA;    // the row key must still be a member
+        const uint32_t* Btest = sside ? J.BA : J.BS;   // the arc's other end must be a member
+        const uint32_t C = sside ? *J.cntS : *J.cntA;
+        auto offs = [&](uint64_t i) -> uint64_t { return (uint64_t)__ldg(seg + i); };
         auto load = [&](uint64_t r) -> ExMeta {
             ExMeta m;
-            m.row = (uint32_t)r;
-            m.key = __ldg(J.cands + r);
+            m.key = __ldg(cand + r);
             m.base = __ldg(off + m.key);
-            const unsigned long long mk = __ldcg(J.mask + r);
-            // prune: constraint already satisfied (an earlier chunk found a fitting arc) -> skip the row;
-            // propagate: only candidates that satisfied every constraint propagate
-            m.skip = MODE == 0 ? ((mk & bitm) != 0) : (mk != full);
+            // skip keys that left the set; A-side also skips keys an earlier chunk already satisfied
+            m.skip = !bit_test(Bkey, m.key) || (!sside && ((__ldcg(J.X + (m.key >> 5)) >> (m.key & 31)) & 1u));
+            m.pad = 0;
             return m;
         };
         pair_chunks<ExMeta, kET, kEI, kEW, 2>(lo, hi, (uint64_t)C, offs, load, s_bufs,
@@ -218,20 +227,21 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
 #pragma unroll
             for (int it = 0; it < kEI; it++) {
                 const uint32_t d = arc[it] >> g.lbits;
-                fits[it] = live[it] && lab_ok(arc[it], g.lmask, J.lab) && d != sm[wi[it]].key && bit_test(J.Bv, d);
+                fits[it] = live[it] && lab_ok(arc[it], g.lmask, J.lab) && d != sm[wi[it]].key && bit_test(Btest, d);
             }
-            if (MODE == 0) {
+            if (!sside) {   // one X bit per satisfied key, aggregated over its run of pairs
                 uint32_t one[kEI];
 #pragma unroll
                 for (int it = 0; it < kEI; it++) one[it] = fits[it] ? 1u : 0u;
                 run_sum<kEI>(v, wi, one, [&](uint32_t w, uint32_t) {
-                    const uint32_t row = sm[w].row;
-                    if (!(__ldcg(J.mask + row) & bitm)) atomicOr(J.mask + row, bitm);
+                    const uint32_t key = sm[w].key;
+                    const uint32_t bit = 1u << (key & 31);
+                    if (!(__ldcg(J.X + (key >> 5)) & bit)) atomicOr(J.X + (key >> 5), bit);
                 });
             } else {
 #pragma unroll
                 for (int it = 0; it < kEI; it++)
-                    if (fits[it]) {
+                    if (fits[it]) {   // fire-and-forget reduction (no return value: RED)
                         const uint32_t d = arc[it] >> g.lbits;
                         atomicOr(J.X + (d >> 5), 1u << (d & 31));
                     }
@@ -241,27 +251,16 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
     if (bytes_acc && threadIdx.x == 0 && p1 > p0) atomicAdd(bytes_acc, (unsigned long long)(p1 - p0) * 4ull);
 }
 
-static size_t ex_smem(uint32_t nj) { return PairSmem<ExMeta, kET, kEI, kEW, 2>::bytes(nj, 0); }
+static size_t ex_smem(uint32_t nj) { return ExSmem::bytes(nj, 0); }
 
-void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj) {
+void run_explore(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, int cls) {
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
     const uint32_t G = (uint32_t)c->nsm * 6;
-    launch(c, GPS_K_EXPLORE, dim3(G), dim3(kET), ex_smem(nj), k_explore<0>, g, d_jobs, nj,
-           c->d_bytes + GPS_K_EXPLORE);
-}
-
-void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj) {
-    if (nj == 0) return;
-    if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
-    const uint32_t G = (uint32_t)c->nsm * 6;
-    launch(c, GPS_K_PROPAGATE, dim3(G), dim3(kET), ex_smem(nj), k_explore<1>, g, d_jobs, nj,
-           c->d_bytes + GPS_K_PROPAGATE);
+    launch(c, cls, dim3(G), dim3(kET), ex_smem(nj), k_explore, g, d_jobs, nj, c->d_bytes + cls);
 }
 
 // ------------------------------------------------------------ step end
-// One thread per 4 bitmap words of one job: the clear needs the candidates' ranks
-// (rp + popcount below the bit) to read their masks; the AND streams the scratch.
 constexpr int kPostWords = 4;
 
 __global__ void __launch_bounds__(256) k_post(DevGraph g, const PostJob* __restrict__ jobs,
@@ -269,31 +268,17 @@ __global__ void __launch_bounds__(256) k_post(DevGraph g, const PostJob* __restr
     const PostJob J = jobs[blockIdx.y];
     const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) * kPostWords;
     if (w0 >= g.nw) return;   // nws >= nw rounded up to 64 words: the 4-word vector stays in bounds
-    uint4 b4 = *reinterpret_cast<const uint4*>(J.B + w0);
-    uint32_t b[kPostWords] = {b4.x, b4.y, b4.z, b4.w};
-    if (J.mask) {
-#pragma unroll
-        for (int i = 0; i < kPostWords; i++) {
-            if (!b[i]) continue;
-            uint32_t rank = __ldg(J.rp + w0 + i), bits = b[i], fails = 0;
-            while (bits) {
-                const uint32_t bit = bits & (0u - bits);
-                bits ^= bit;
-                if (J.mask[rank++] != J.full) fails |= bit;
-            }
-            b[i] &= ~fails;
-        }
-    }
+    uint4 b = *reinterpret_cast<const uint4*>(J.B + w0);
     for (uint32_t x = J.x0; x < J.x1; x++) {
         uint4* xp = reinterpret_cast<uint4*>(xs[x] + w0);
         const uint4 v = *xp;
-        b[0] &= v.x;
-        b[1] &= v.y;
-        b[2] &= v.z;
-        b[3] &= v.w;
+        b.x &= v.x;
+        b.y &= v.y;
+        b.z &= v.z;
+        b.w &= v.w;
         *xp = make_uint4(0u, 0u, 0u, 0u);
     }
-    *reinterpret_cast<uint4*>(J.B + w0) = make_uint4(b[0], b[1], b[2], b[3]);
+    *reinterpret_cast<uint4*>(J.B + w0) = b;
 }
 
 void run_post(gps_ctx* c, const DevGraph& g, const PostJob* d_jobs, uint32_t* const* d_xs, uint32_t nj) {

@@ -37,8 +37,8 @@ void run_check(gps_ctx* c, const DevGraph& g, const QDesc* d_q, uint32_t nq, uin
 // Per job (query, vertex): c_array (sorted candidate ids), rank prefix rp
 // (exclusive popcount per bitmap word, rp[nw] = |C|), |C| in *cnt, and the
 // exclusive prefix sums of the candidates' out-/in-degrees (seg_out/seg_in,
-// C+1 entries) that index the pair spaces of explore and EC.  Optionally
-// zeroes mask[0..C).  One single-pass launch (decoupled look-back).
+// C+1 entries) that index the pair spaces of explore and EC.  One single-pass
+// launch (decoupled look-back).
 struct CollectJob {
     const uint32_t* B;
     uint32_t* rp;
@@ -46,42 +46,41 @@ struct CollectJob {
     uint32_t* cnt;
     uint32_t* seg_out;
     uint32_t* seg_in;
-    unsigned long long* mask;
     uint32_t* segtot;       // optional [2]: seg_out[C], seg_in[C] (pair-space sizes for the host)
 };
 void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32_t nj);
 
 // ---- a4/a5 kernel_explore (Alg. 2 lines 14-22) --------------------
-// Constraint of a candidate u' of u for one query arc between u and v:
-// adj_dir(u') must hold some v' != u' with a fitting label and v' in B[v].
-// One (query vertex u, constraint c) pair of an explore step: the pair space is
-// (candidate u' of u, arc of adj_dir(u')).
+// One constraint of the filter: a member a' of set A survives only if it has an
+// arc of direction dir (0: a' -> s', 1: s' -> a') with a fitting label to some
+// s' != a' of set S.  Prune (lines 14-18) is (A = u, S = v); propagation (lines
+// 19-22, reading R15) is (A = v, S = u).  The job writes X = the members of A
+// that satisfy it (k_post then ANDs X into B_A).  Both sides hold a (possibly
+// stale, i.e. superset) c_array; rows whose key left the current bitmap are
+// skipped.  Per job the kernel walks the cheaper side:
+//   A-side: pairs (a' in C(A), arc of adj_dir(a')), test s' in B_S, one X bit per a'
+//   S-side: pairs (s' in C(S), arc of adj_{1-dir}(s')), test a' in B_A, set X[a']
+// (the same set: a' has a fitting arc to S  <=>  a' is a fitting reverse neighbour of S).
 struct ExploreJob {
-    const uint32_t* cands;  // c_array[u]
-    const uint32_t* cnt;    // device |C(u)|
-    const uint32_t* seg;    // degree prefix of the candidates in direction dir
-    unsigned long long* mask;  // [|C(u)|] satisfied-constraint bits (zeroed by collect)
-    const uint32_t* Bv;     // bitmap of the neighbour v
-    uint32_t* X;            // propagation scratch for v
+    const uint32_t* candA;  // c_array of A (nullptr: none yet -> S-side; at least one side has one)
+    const uint32_t* cntA;   // device |C(A)|
+    const uint32_t* segA;   // degree prefix of C(A) in direction dir
+    const uint32_t* candS;  // c_array of S (nullptr: none yet -> A-side)
+    const uint32_t* cntS;
+    const uint32_t* segS;   // degree prefix of C(S) in direction 1 - dir
+    const uint32_t* BA;     // current bitmaps
+    const uint32_t* BS;
+    uint32_t* X;            // [nws] output bits (zero on entry)
     int32_t lab;            // edge label or -1
-    uint32_t dir;           // 0: arc u -> v (out-adjacency of u'), 1: arc v -> u (in-adjacency)
-    uint32_t bit;           // constraint index (bit in mask)
-    uint32_t nc;            // constraints of this (query, u) step (full mask = 2^nc - 1)
+    uint32_t dir;
 };
-// prune over all (u, constraint) jobs; propagate over the constraints of
-// initialisation steps
-void run_prune(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj);
-void run_propagate(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj);
+// cls: GPS_K_EXPLORE (prune jobs) or GPS_K_PROPAGATE (propagation jobs)
+void run_explore(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, int cls);
 
-// End of an explore step, one job per bitmap the step changes (word-parallel, no
-// atomics): if mask != null, the candidates (ranks from rp, taken at this step's
-// collect) that missed a constraint leave B (Alg. 2 line 18); then
-// B &= X[x0] & ... & X[x1-1] (reading R15) and that scratch is zeroed.
+// End of an explore launch, one job per bitmap it filters (word-parallel):
+// B &= X[x0] & ... & X[x1-1], then that scratch is zeroed.
 struct PostJob {
     uint32_t* B;
-    const uint32_t* rp;
-    const unsigned long long* mask;
-    unsigned long long full;
     uint32_t x0, x1;
 };
 void run_post(gps_ctx* c, const DevGraph& g, const PostJob* d_jobs, uint32_t* const* d_xs, uint32_t nj);

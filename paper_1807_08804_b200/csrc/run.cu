@@ -94,7 +94,6 @@ struct QS {                       // one query of a chunk
     uint32_t* carr[GPS_MAX_QV];
     uint32_t* seg[GPS_MAX_QV][2];
     uint32_t* cnt = nullptr;      // k counters, inside the chunk-wide counter array
-    unsigned long long* mask = nullptr;
     uint32_t C[GPS_MAX_QV];
     uint32_t P[GPS_MAX_QV][2];    // out / in pair-space size of C(u) (sum of degrees)
     bool live = true;
@@ -150,14 +149,11 @@ void carve_all(Chunk& ch, Carve& cv) {
     for (QS* q : ch.qs) {
         q->B = cv.take<uint32_t>((size_t)q->k * nws);
         q->rp = cv.take<uint32_t>((size_t)q->k * rps);
-        uint32_t maxcap = 1;
         for (int u = 0; u < q->k; u++) {
             q->carr[u] = cv.take<uint32_t>(q->cap[u]);
             q->seg[u][0] = cv.take<uint32_t>((size_t)q->cap[u] + 1);
             q->seg[u][1] = cv.take<uint32_t>((size_t)q->cap[u] + 1);
-            maxcap = std::max(maxcap, q->cap[u]);
         }
-        q->mask = cv.take<unsigned long long>(maxcap);
     }
 }
 
@@ -187,65 +183,79 @@ void filter_phase(Chunk& ch, int stage) {
         size_t s = q->plan.init_steps.size() + (stage >= 2 ? q->plan.refine_steps.size() : 0);
         S = std::max(S, s);
     }
+    // vertices whose candidate array exists (collected by an earlier step: a superset of
+    // the current set); a side without one cannot be walked
+    std::vector<uint32_t> have(ch.qs.size(), 0u);
+    auto job = [&](size_t qi, int A, int Sv, const Constraint& cs, int dir, uint32_t* X) {
+        QS* q = ch.qs[qi];
+        ExploreJob e{};
+        if (have[qi] >> A & 1u) {
+            e.candA = q->carr[A];
+            e.cntA = q->cnt + A;
+            e.segA = q->seg[A][dir];
+        }
+        if (have[qi] >> Sv & 1u) {
+            e.candS = q->carr[Sv];
+            e.cntS = q->cnt + Sv;
+            e.segS = q->seg[Sv][1 - dir];
+        }
+        e.BA = ch.Bp(*q, A);
+        e.BS = ch.Bp(*q, Sv);
+        e.X = X;
+        e.lab = q->plan.arcs[cs.arc].lab;
+        e.dir = (uint32_t)dir;
+        return e;
+    };
     for (size_t s = 0; s < S; s++) {
         std::vector<CollectJob> cj;
         std::vector<ExploreJob> ej, pj;
-        std::vector<PostJob> post;
+        std::vector<PostJob> post1, post2;
         std::vector<uint32_t*> xs;
-        for (QS* q : ch.qs) {
+        for (size_t qi = 0; qi < ch.qs.size(); qi++) {
+            QS* q = ch.qs[qi];
             const Plan& p = q->plan;
             const size_t ni = p.init_steps.size();
             const size_t nr = stage >= 2 ? p.refine_steps.size() : 0;
             if (s >= ni + nr) continue;
             const FilterStep& st = s < ni ? p.init_steps[s] : p.refine_steps[s - ni];
             const int u = st.u;
-            cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0], q->seg[u][1],
-                                    q->mask, nullptr});
             const uint32_t nc = (uint32_t)st.cons.size();
             if (nc == 0) continue;
+            have[qi] |= 1u << u;
+            cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0], q->seg[u][1],
+                                    nullptr});
+            // prune (Alg. 2 lines 14-18): A = u, S = v; X_i = members of C(u) meeting constraint i
+            const uint32_t x0 = (uint32_t)xs.size();
             for (uint32_t i = 0; i < nc; i++) {
                 const Constraint& cs = st.cons[i];
-                ExploreJob e{};
-                e.cands = q->carr[u];
-                e.cnt = q->cnt + u;
-                e.seg = q->seg[u][cs.dir];
-                e.mask = q->mask;
-                e.Bv = ch.Bp(*q, cs.v);
-                e.X = st.propagate ? ch.Xp(*q, (int)i) : nullptr;
-                e.lab = p.arcs[cs.arc].lab;
-                e.dir = (uint32_t)cs.dir;
-                e.bit = i;
-                e.nc = nc;
-                ej.push_back(e);
-                if (st.propagate) pj.push_back(e);
+                ej.push_back(job(qi, u, cs.v, cs, cs.dir, ch.Xp(*q, (int)i)));
+                xs.push_back(ch.Xp(*q, (int)i));
             }
-            const size_t pu = post.size();
-            post.push_back(PostJob{ch.Bp(*q, u), ch.rpp(*q, u), q->mask, nc >= 64 ? ~0ull : ((1ull << nc) - 1ull), 0, 0});
-            if (st.propagate) {
-                std::vector<int> targets;
-                for (const Constraint& cs : st.cons)
-                    if (std::find(targets.begin(), targets.end(), cs.v) == targets.end()) targets.push_back(cs.v);
-                for (int v : targets) {
-                    // one job per bitmap: a target equal to u (never for simple queries) shares u's job
-                    PostJob a{ch.Bp(*q, v), nullptr, nullptr, 0ull, (uint32_t)xs.size(), 0};
-                    for (uint32_t i = 0; i < nc; i++)
-                        if (st.cons[i].v == v) xs.push_back(ch.Xp(*q, (int)i));
-                    a.x1 = (uint32_t)xs.size();
-                    if (v == u) {
-                        post[pu].x0 = a.x0;
-                        post[pu].x1 = a.x1;
-                    } else {
-                        post.push_back(a);
-                    }
+            post1.push_back(PostJob{ch.Bp(*q, u), x0, (uint32_t)xs.size()});
+            if (!st.propagate) continue;
+            // propagation (lines 19-22, reading R15): A = v, S = u (arcs seen from v: direction flipped)
+            std::vector<int> targets;
+            for (const Constraint& cs : st.cons)
+                if (std::find(targets.begin(), targets.end(), cs.v) == targets.end()) targets.push_back(cs.v);
+            for (int v : targets) {
+                const uint32_t y0 = (uint32_t)xs.size();
+                for (uint32_t i = 0; i < nc; i++) {
+                    const Constraint& cs = st.cons[i];
+                    if (cs.v != v) continue;
+                    pj.push_back(job(qi, v, u, cs, 1 - cs.dir, ch.Xp(*q, (int)i)));
+                    xs.push_back(ch.Xp(*q, (int)i));
                 }
+                post2.push_back(PostJob{ch.Bp(*q, v), y0, (uint32_t)xs.size()});
             }
         }
         if (cj.empty()) continue;
+        uint32_t* const* dxs = upload(c, xs, ch.keep);
         run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
-        if (ej.empty()) continue;
-        run_prune(c, d, upload(c, ej, ch.keep), (uint32_t)ej.size());
-        if (!pj.empty()) run_propagate(c, d, upload(c, pj, ch.keep), (uint32_t)pj.size());
-        run_post(c, d, upload(c, post, ch.keep), xs.empty() ? nullptr : upload(c, xs, ch.keep), (uint32_t)post.size());
+        run_explore(c, d, upload(c, ej, ch.keep), (uint32_t)ej.size(), GPS_K_EXPLORE);
+        run_post(c, d, upload(c, post1, ch.keep), dxs, (uint32_t)post1.size());
+        if (pj.empty()) continue;
+        run_explore(c, d, upload(c, pj, ch.keep), (uint32_t)pj.size(), GPS_K_PROPAGATE);
+        run_post(c, d, upload(c, post2, ch.keep), dxs, (uint32_t)post2.size());
     }
 }
 
@@ -498,7 +508,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             QS* q = ch.qs[i];
             for (int u = 0; u < q->k; u++)
                 cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0],
-                                        q->seg[u][1], nullptr, ch.cnt_all + ch.ncnt + 2 * (ch.cnt_base[i] + u)});
+                                        q->seg[u][1], ch.cnt_all + ch.ncnt + 2 * (ch.cnt_base[i] + u)});
         }
         run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
         const size_t nc = ch.ncnt;
