@@ -2,6 +2,8 @@
 // pinned staging for job uploads, pinned host results, decoupled look-back
 // scratch, event timing, and the host worker pool of the batch API.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -179,6 +181,7 @@ void ctx_init(gps_ctx* c, int dev, cudaStream_t stream) {
     GPS_CK(cudaMalloc(&c->d_bytes, sizeof(unsigned long long) * GPS_K_NCLASSES));
     GPS_CK(cudaMemset(c->d_bytes, 0, sizeof(unsigned long long) * GPS_K_NCLASSES));
     GPS_CK(cudaMalloc(&c->d_info, sizeof(uint64_t) * 128));
+    GPS_CK(cudaMemset(c->d_info, 0, sizeof(uint64_t) * 128));
     GPS_CK(cudaMallocHost(&c->h_info, sizeof(uint64_t) * 128));
     GPS_CK(cudaMalloc(&c->d_done, sizeof(unsigned int) * 64));
     GPS_CK(cudaMemset(c->d_done, 0, sizeof(unsigned int) * 64));
@@ -187,6 +190,14 @@ void ctx_init(gps_ctx* c, int dev, cudaStream_t stream) {
 
 void ctx_release(gps_ctx* c) {
     cudaStreamSynchronize(c->stream);
+    if (std::getenv("GPS_EXPLORE_STATS") && c->d_info) {
+        uint64_t h[8];
+        if (cudaMemcpy(h, c->d_info + 96, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess && h[0] + h[4])
+            std::fprintf(stderr, "[gps] explore pairs %llu live %llu fit %llu s-side %llu | propagate pairs %llu live %llu "
+                         "fit %llu s-side %llu\n", (unsigned long long)h[0], (unsigned long long)h[1],
+                         (unsigned long long)h[2], (unsigned long long)h[3], (unsigned long long)h[4],
+                         (unsigned long long)h[5], (unsigned long long)h[6], (unsigned long long)h[7]);
+    }
     for (gps_result* r : c->results) {
         if (r->on_device) {
             r->hold.reset();

@@ -18,6 +18,8 @@
 //                  pair ranges per block replace the paper's warp-per-candidate +
 //                  block-per-hub split.
 //   k_post         word-parallel B &= (AND of the jobs' X bitmaps), scratch reset.
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "lookback.cuh"
 #include "pairs.cuh"
@@ -181,7 +183,7 @@ __device__ __forceinline__ uint64_t ex_pairs(const ExploreJob& J, bool* s_side) 
 }
 
 __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
-                                                unsigned long long* bytes_acc) {
+                                                unsigned long long* bytes_acc, unsigned long long* dbg) {
     extern __shared__ __align__(16) char s_dyn[];
     uint64_t* s_jp = reinterpret_cast<uint64_t*>(s_dyn);          // [nj+1] job pair prefix
     char* s_bufs = s_dyn + ExSmem::buf_off(nj);
@@ -189,6 +191,7 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
     job_prefix(nj, [&](uint32_t j) -> uint64_t { bool sd; return ex_pairs(jobs[j], &sd); }, s_jp);
     uint64_t p0, p1;
     pairs_range(s_jp[nj], blockIdx.x, gridDim.x, p0, p1);
+    uint32_t n_live = 0, n_fit = 0, n_sside = 0;
     for_job_ranges(s_jp, nj, p0, p1, [&](uint32_t jj, uint64_t lo, uint64_t hi) {
         const ExploreJob J = jobs[jj];             // by value: fields stay in registers across atomics
         bool sside;
@@ -202,13 +205,16 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
         const uint32_t* Bkey = sside ? J.BS : J.BA;    // the row key must still be a member
         const uint32_t* Btest = sside ? J.BA : J.BS;   // the arc's other end must be a member
         const uint32_t C = sside ? *J.cntS : *J.cntA;
+        const bool fresh = (sside ? J.freshS : J.freshA) != 0;
         auto offs = [&](uint64_t i) -> uint64_t { return (uint64_t)__ldg(seg + i); };
         auto load = [&](uint64_t r) -> ExMeta {
             ExMeta m;
             m.key = __ldg(cand + r);
             m.base = __ldg(off + m.key);
-            // skip keys that left the set; A-side also skips keys an earlier chunk already satisfied
-            m.skip = !bit_test(Bkey, m.key) || (!sside && ((__ldcg(J.X + (m.key >> 5)) >> (m.key & 31)) & 1u));
+            // skip keys that left the set (stale arrays only); A-side also skips keys an earlier chunk
+            // already satisfied
+            m.skip = (!fresh && !bit_test(Bkey, m.key)) ||
+                     (!sside && ((__ldcg(J.X + (m.key >> 5)) >> (m.key & 31)) & 1u));
             m.pad = 0;
             return m;
         };
@@ -228,16 +234,31 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
             for (int it = 0; it < kEI; it++) {
                 const uint32_t d = arc[it] >> g.lbits;
                 fits[it] = live[it] && lab_ok(arc[it], g.lmask, J.lab) && d != sm[wi[it]].key && bit_test(Btest, d);
+                if (dbg) {
+                    n_live += live[it];
+                    n_fit += fits[it];
+                    n_sside += sside && v[it];
+                }
             }
-            if (!sside) {   // one X bit per satisfied key, aggregated over its run of pairs
-                uint32_t one[kEI];
+            if (!sside) {   // one X bit per satisfied key: OR over the thread's run of the same row
+                uint32_t cur = 0xffffffffu;
+                bool any = false;
 #pragma unroll
-                for (int it = 0; it < kEI; it++) one[it] = fits[it] ? 1u : 0u;
-                run_sum<kEI>(v, wi, one, [&](uint32_t w, uint32_t) {
-                    const uint32_t key = sm[w].key;
-                    const uint32_t bit = 1u << (key & 31);
-                    if (!(__ldcg(J.X + (key >> 5)) & bit)) atomicOr(J.X + (key >> 5), bit);
-                });
+                for (int it = 0; it < kEI; it++) {
+                    if (wi[it] != cur) {
+                        if (any) {
+                            const uint32_t key = sm[cur].key;
+                            atomicOr(J.X + (key >> 5), 1u << (key & 31));
+                        }
+                        cur = wi[it];
+                        any = false;
+                    }
+                    any |= fits[it];
+                }
+                if (any) {
+                    const uint32_t key = sm[cur].key;
+                    atomicOr(J.X + (key >> 5), 1u << (key & 31));
+                }
             } else {
 #pragma unroll
                 for (int it = 0; it < kEI; it++)
@@ -249,6 +270,15 @@ __global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob
         });
     });
     if (bytes_acc && threadIdx.x == 0 && p1 > p0) atomicAdd(bytes_acc, (unsigned long long)(p1 - p0) * 4ull);
+    if (dbg) {   // GPS_EXPLORE_STATS: pairs / live pairs / fitting pairs / S-side pairs
+        const uint32_t a = block_sum(n_live), b = block_sum(n_fit), c = block_sum(n_sside);
+        if (threadIdx.x == 0) {
+            atomicAdd(dbg, (unsigned long long)(p1 - p0));
+            atomicAdd(dbg + 1, (unsigned long long)a);
+            atomicAdd(dbg + 2, (unsigned long long)b);
+            atomicAdd(dbg + 3, (unsigned long long)c);
+        }
+    }
 }
 
 static size_t ex_smem(uint32_t nj) { return ExSmem::bytes(nj, 0); }
@@ -257,7 +287,9 @@ void run_explore(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
     const uint32_t G = (uint32_t)c->nsm * 6;
-    launch(c, cls, dim3(G), dim3(kET), ex_smem(nj), k_explore, g, d_jobs, nj, c->d_bytes + cls);
+    static const bool dbg = std::getenv("GPS_EXPLORE_STATS") != nullptr;
+    launch(c, cls, dim3(G), dim3(kET), ex_smem(nj), k_explore, g, d_jobs, nj, c->d_bytes + cls,
+           dbg ? (unsigned long long*)c->d_info + 96 + (cls == GPS_K_PROPAGATE ? 4 : 0) : nullptr);
 }
 
 // ------------------------------------------------------------ step end

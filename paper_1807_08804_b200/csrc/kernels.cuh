@@ -73,6 +73,7 @@ struct ExploreJob {
     uint32_t* X;            // [nws] output bits (zero on entry)
     int32_t lab;            // edge label or -1
     uint32_t dir;
+    uint8_t freshA, freshS; // the c_array equals the current bitmap (no membership test per row)
 };
 // cls: GPS_K_EXPLORE (prune jobs) or GPS_K_PROPAGATE (propagation jobs)
 void run_explore(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, int cls);

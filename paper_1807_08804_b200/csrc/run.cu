@@ -229,6 +229,7 @@ void filter_phase(Chunk& ch, int stage) {
             for (uint32_t i = 0; i < nc; i++) {
                 const Constraint& cs = st.cons[i];
                 ej.push_back(job(qi, u, cs.v, cs, cs.dir, ch.Xp(*q, (int)i)));
+                ej.back().freshA = 1;   // u was collected by this step
                 xs.push_back(ch.Xp(*q, (int)i));
             }
             post1.push_back(PostJob{ch.Bp(*q, u), x0, (uint32_t)xs.size()});
@@ -243,6 +244,7 @@ void filter_phase(Chunk& ch, int stage) {
                     const Constraint& cs = st.cons[i];
                     if (cs.v != v) continue;
                     pj.push_back(job(qi, v, u, cs, 1 - cs.dir, ch.Xp(*q, (int)i)));
+                    pj.back().freshS = 1;   // u is re-collected after its prune
                     xs.push_back(ch.Xp(*q, (int)i));
                 }
                 post2.push_back(PostJob{ch.Bp(*q, v), y0, (uint32_t)xs.size()});
@@ -254,6 +256,11 @@ void filter_phase(Chunk& ch, int stage) {
         run_explore(c, d, upload(c, ej, ch.keep), (uint32_t)ej.size(), GPS_K_EXPLORE);
         run_post(c, d, upload(c, post1, ch.keep), dxs, (uint32_t)post1.size());
         if (pj.empty()) continue;
+        // re-collect the pruned vertices: propagation walks only the survivors
+        std::vector<CollectJob> cp;
+        for (const CollectJob& x : cj)
+            if (std::any_of(pj.begin(), pj.end(), [&](const ExploreJob& e) { return e.candS == x.carr; })) cp.push_back(x);
+        if (!cp.empty()) run_collect(c, d, upload(c, cp, ch.keep), (uint32_t)cp.size());
         run_explore(c, d, upload(c, pj, ch.keep), (uint32_t)pj.size(), GPS_K_PROPAGATE);
         run_post(c, d, upload(c, post2, ch.keep), dxs, (uint32_t)post2.size());
     }
