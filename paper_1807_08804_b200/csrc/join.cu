@@ -25,7 +25,7 @@ constexpr int kPT = 256;    // threads per block
 constexpr int kPI = 4;      // pairs per thread per chunk
 constexpr int kPW = 1024;   // EC: rows staged per chunk (keys are never empty: a chunk always fits)
 constexpr int kJW = 1024;   // join: rows staged (single buffer; fan-out can be 1)
-constexpr uint32_t kStageW = 8;   // join write: stage output rows of width <= 8 in shared memory
+constexpr uint32_t kStageW = kJoinStageCols;   // join: stage rows of width <= 8 in shared memory
 
 
 // ------------------------------------------------------------ a6 EC build
@@ -161,7 +161,7 @@ void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uin
 }
 
 // ------------------------------------------------------------ a8 join step
-constexpr int kSegRows = 8;
+constexpr int kSegRows = 4;
 constexpr int kSegTile = 256 * kSegRows;
 
 // largest j < nj with jobs[j].row0 <= r
@@ -175,53 +175,136 @@ __device__ __forceinline__ uint32_t job_of_row(const JoinJob* __restrict__ jobs,
 }
 
 // Per input row: O(1) key lookup -> EC segment start (s0) and the exclusive scan of
-// the segment lengths (poff, the step's pair space), one look-back pass.
+// the segment lengths (poff, the step's pair space), one look-back pass.  FAST
+// (closing-free steps): also the row values found in the segment (imask, w
+// independent binary searches advanced in lockstep) and the scans of the row's
+// valid (aoff) and written (woff) outputs -- three look-backs in three warps.
+template <bool FAST>
 __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
                                                   uint32_t epoch) {
-    __shared__ uint64_t s_pre;
+    __shared__ uint64_t s_pre[3];
     const uint32_t tile = lb_ticket(lb.ctr, ntiles);
     const uint64_t r0 = (uint64_t)tile * kSegTile + (uint64_t)threadIdx.x * kSegRows;
-    uint32_t len[kSegRows];
-    uint64_t tsum = 0;
+    uint32_t len[kSegRows], ac[kSegRows], wc[kSegRows];
+    uint64_t tsum = 0, asum = 0, wsum = 0;
     uint32_t jb = r0 < a.R ? job_of_row(a.jobs, a.nj, r0) : 0;
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {
         const uint64_t r = r0 + i;
-        len[i] = 0;
+        len[i] = ac[i] = wc[i] = 0;
         if (r < a.R) {
             while (jb + 1 < a.nj && a.jobs[jb + 1].row0 <= r) jb++;
             const JoinJob& J = a.jobs[jb];
-            const uint32_t key = __ldg(J.M + (r - J.row0) * a.w + J.x_col);
+            const uint32_t* row = J.M + (r - J.row0) * a.w;
+            const uint32_t key = __ldg(row + J.x_col);
             const uint32_t rk = bit_rank(J.Bx, J.rpx, key);
             const uint32_t s = __ldg(J.ec_off + rk);
             len[i] = __ldg(J.ec_off + rk + 1) - s;
             a.s0[r] = s;
+            if (FAST) {
+                uint32_t mask = 0;
+                for (uint32_t c0 = 0; c0 < a.w; c0 += 8) {   // up to 8 searches in lockstep
+                    uint32_t t[8], lo[8], hi[8];
+#pragma unroll
+                    for (int x = 0; x < 8; x++) {
+                        const bool on = c0 + x < a.w;
+                        t[x] = on ? __ldg(row + c0 + x) : 0u;
+                        lo[x] = s;
+                        hi[x] = on ? s + len[i] : s;
+                    }
+                    bool more = true;
+                    while (more) {
+                        more = false;
+#pragma unroll
+                        for (int x = 0; x < 8; x++) {
+                            if (lo[x] >= hi[x]) continue;
+                            const uint32_t mid = (lo[x] + hi[x]) >> 1;
+                            const uint32_t v = __ldg(a.ec_val + mid);
+                            if (v == t[x]) {
+                                mask |= 1u << (c0 + x);
+                                hi[x] = lo[x];
+                            } else if (v < t[x]) {
+                                lo[x] = mid + 1;
+                            } else {
+                                hi[x] = mid;
+                            }
+                            more |= lo[x] < hi[x];
+                        }
+                    }
+                }
+                a.imask[r] = mask;
+                ac[i] = len[i] - __popc(mask);
+                wc[i] = J.nowrite ? 0u : ac[i];
+            }
         }
         tsum += len[i];
+        asum += ac[i];
+        wsum += wc[i];
     }
-    uint64_t tot;
+    uint64_t tot, atot = 0, wtot = 0;
     const uint64_t pre = block_excl_scan(tsum, &tot);
-    if (threadIdx.x < 32) {
-        const uint64_t p = lb_warp_lookback(lb.status, tile, tot, epoch);
-        if (threadIdx.x == 0) s_pre = p;
+    uint64_t apre = 0, wpre = 0;
+    if (FAST) {
+        apre = block_excl_scan(asum, &atot);
+        wpre = block_excl_scan(wsum, &wtot);
+    }
+    const uint32_t wid = threadIdx.x >> 5;
+    if (wid < (FAST ? 3u : 1u)) {
+        const uint64_t agg = wid == 0 ? tot : (wid == 1 ? atot : wtot);
+        const uint64_t p = lb_warp_lookback(lb.status + (size_t)wid * lb.max_tiles, tile, agg, epoch);
+        if ((threadIdx.x & 31u) == 0) s_pre[wid] = p;
     }
     __syncthreads();
-    uint64_t run = s_pre + pre;
+    uint64_t run = s_pre[0] + pre, arun = 0, wrun = 0;
+    if (FAST) {
+        arun = s_pre[1] + apre;
+        wrun = s_pre[2] + wpre;
+    }
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {
         const uint64_t r = r0 + i;
-        if (r < a.R) a.poff[r] = run;
+        if (r < a.R) {
+            a.poff[r] = run;
+            if (FAST) {
+                a.aoff[r] = arun;
+                a.woff[r] = wrun;
+            }
+        }
         run += len[i];
+        arun += ac[i];
+        wrun += wc[i];
     }
-    if (tile == ntiles - 1 && threadIdx.x == 0) a.poff[a.R] = s_pre + tot;
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        a.poff[a.R] = s_pre[0] + tot;
+        if (FAST) {
+            a.aoff[a.R] = s_pre[1] + atot;
+            a.woff[a.R] = s_pre[2] + wtot;
+        }
+    }
 }
 
 void run_join_seg(gps_ctx* c, const JoinStep& s) {
     const uint64_t nt = (s.R + kSegTile - 1) / kSegTile;
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join table too large");
-    LbScratch lb = lb_scratch(c, 1, (uint32_t)nt);
-    launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg, s, lb, (uint32_t)nt, lb_next_epoch(c));
-    c->stats.k_bytes[GPS_K_JOIN_LEN] += 4.0 * s.R + 12.0 * s.R;
+    LbScratch lb = lb_scratch(c, 3, (uint32_t)nt);
+    if (s.fast)
+        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg<true>, s, lb, (uint32_t)nt,
+               lb_next_epoch(c));
+    else
+        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg<false>, s, lb, (uint32_t)nt,
+               lb_next_epoch(c));
+    c->stats.k_bytes[GPS_K_JOIN_LEN] += 4.0 * s.R * (s.w + 3);
+}
+
+__global__ void k_join_job_totals(const __grid_constant__ JoinStep a) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= a.nj) return;
+    const uint64_t lo = a.jobs[j].row0, hi = j + 1 < a.nj ? a.jobs[j + 1].row0 : a.R;
+    *a.jobs[j].total = a.aoff[hi] - a.aoff[lo];
+}
+
+void run_join_job_totals(gps_ctx* c, const JoinStep& s) {
+    launch(c, GPS_K_JOIN_LEN, dim3((s.nj + 127) / 128), dim3(128), 0, k_join_job_totals, s);
 }
 
 __device__ __forceinline__ bool seg_contains(const uint32_t* __restrict__ val, uint32_t lo, uint32_t hi, uint32_t t) {
@@ -391,6 +474,249 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
     }
 }
 
+// Single-pass join step for rows of <= kStageW output columns: the window stages,
+// per input row, its values (with the output permutation of a final step packed
+// in nibbles), EC segment start and flags, so injectivity, closing checks and the
+// output row come from shared memory instead of per-pair global loads.
+constexpr int kJVW = 512;   // window rows
+struct JVMeta {
+    uint32_t s0;            // EC segment start
+    uint32_t job;
+    uint32_t perm;          // output column of input column c (nibble c), of the new value (nibble w)
+    uint32_t flags;         // bit 0: count only, bit 1: has closing arcs
+    uint32_t val[kStageW];  // the row's w values, unused slots 0xffffffff (never a vertex id)
+};
+using JVSmem = PairSmem<JVMeta, kPT, kPI, kJVW, 1>;
+
+__device__ __forceinline__ bool close_ok(const JoinStep& a, const JoinJob& J, const uint32_t* val, uint32_t cand) {
+    for (uint32_t ci = 0; ci < J.nclose; ci++) {
+        const CloseChk& cl = a.cl[J.close0 + ci];
+        const uint32_t key = cl.key_new ? cand : val[cl.key_col];
+        const uint32_t tgt = cl.tgt_new ? cand : val[cl.tgt_col];
+        const uint32_t rk = bit_rank(cl.Bk, cl.rpk, key);
+        if (!seg_contains(a.ec_val, __ldg(cl.off + rk), __ldg(cl.off + rk + 1), tgt)) return false;
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(kPT) k_join_v(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
+                                                uint32_t epoch) {
+    extern __shared__ __align__(16) char s_dyn[];
+    uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);      // [nj+1] first row of every job
+    char* s_bufs = s_dyn + JVSmem::buf_off(a.nj);
+    uint32_t* s_out = reinterpret_cast<uint32_t*>(s_dyn + JVSmem::extra_off(a.nj));   // staged output rows
+    __shared__ uint64_t s_prefix;
+    const uint32_t t = lb_ticket(lb.ctr, ntiles);
+    JVSmem::init(s_bufs);
+    for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
+    if (threadIdx.x == 0) s_jr[a.nj] = a.R;
+    __syncthreads();
+    const uint32_t w = a.w, wout = a.wout;
+    auto offs = [&](uint64_t i) -> uint64_t { return __ldg(a.poff + i); };
+    auto load = [&](uint64_t r) -> JVMeta {
+        JVMeta m;
+        m.job = pairs_find_smem(s_jr, a.nj, r);
+        const JoinJob& J = a.jobs[m.job];
+        const uint32_t* rowp = J.M + (r - J.row0) * w;
+#pragma unroll
+        for (uint32_t c = 0; c < kStageW; c++) m.val[c] = c < w ? __ldg(rowp + c) : 0xffffffffu;
+        uint32_t perm = 0;
+        for (uint32_t c = 0; c <= w; c++) perm |= (J.final_ ? (uint32_t)J.perm[c] : c) << (4 * c);
+        m.perm = perm;
+        m.flags = (J.nowrite ? 1u : 0u) | (J.nclose ? 2u : 0u);
+        m.s0 = __ldg(a.s0 + r);
+        return m;
+    };
+    const uint64_t P = a.phi == ~0ull ? offs(a.R) - a.plo : a.phi - a.plo;
+    const uint64_t p0 = a.plo + (uint64_t)t * kTile;
+    const uint64_t p1 = p0 + kTile < a.plo + P ? p0 + kTile : a.plo + P;
+    uint32_t lc = 0;   // output rows staged by the tile so far (uniform)
+    pair_chunks<JVMeta, kPT, kPI, kJVW, 1>(p0, p1, a.R, offs, load, s_bufs,
+                                           [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
+                                               const uint32_t (&j)[kPI], const JVMeta* sm, uint64_t) {
+        uint32_t cand[kPI];
+#pragma unroll
+        for (int it = 0; it < kPI; it++) cand[it] = v[it] ? __ldg(a.ec_val + sm[wi[it]].s0 + j[it]) : 0u;
+        bool valid[kPI], writes[kPI];
+        uint32_t mine = 0;
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            const JVMeta& m = sm[wi[it]];
+            bool ok = v[it];
+#pragma unroll
+            for (uint32_t c = 0; c < kStageW; c++) ok = ok && m.val[c] != cand[it];   // injectivity (Def. 2)
+            if (ok && (m.flags & 2u)) ok = close_ok(a, a.jobs[m.job], m.val, cand[it]);
+            valid[it] = ok;
+            writes[it] = ok && !(m.flags & 1u);
+            mine += writes[it] ? 1u : 0u;
+        }
+        {   // per-job output totals: warp-wide when the warp's items share one job, else per run
+            const uint32_t lane0 = __shfl_sync(kFull, sm[wi[0]].job, 0);
+            uint32_t nv = 0;
+            bool same = true;
+#pragma unroll
+            for (int it = 0; it < kPI; it++) {
+                nv += valid[it] ? 1u : 0u;
+                same = same && (!v[it] || sm[wi[it]].job == lane0);
+            }
+            if (__all_sync(kFull, same)) {
+                const uint32_t s = __reduce_add_sync(kFull, nv);
+                if (lane_id() == 0 && s) atomicAdd(a.jobs[lane0].total, (unsigned long long)s);
+            } else {
+                uint32_t key[kPI], one[kPI];
+#pragma unroll
+                for (int it = 0; it < kPI; it++) {
+                    key[it] = sm[wi[it]].job;
+                    one[it] = valid[it] ? 1u : 0u;
+                }
+                run_sum<kPI>(v, key, one, [&](uint32_t job, uint32_t n) {
+                    atomicAdd(a.jobs[job].total, (unsigned long long)n);
+                });
+            }
+        }
+        uint32_t tot;
+        uint32_t lpos = lc + block_excl_scan(mine, &tot);
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            if (!writes[it]) continue;
+            const JVMeta& m = sm[wi[it]];
+            uint32_t* dst = s_out + (size_t)(lpos++) * wout;
+            for (uint32_t c = 0; c < w; c++) dst[(m.perm >> (4 * c)) & 15u] = m.val[c];
+            dst[(m.perm >> (4 * w)) & 15u] = cand[it];
+        }
+        lc += tot;
+    });
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const uint64_t pre = lb_warp_lookback(lb.status, t, lc, epoch);
+        if (threadIdx.x == 0) s_prefix = pre;
+    }
+    __syncthreads();
+    const uint64_t pre = s_prefix;
+    copy_out(a.out + pre * wout, s_out, lc * wout);
+    if (t == ntiles - 1 && threadIdx.x == 0) {
+        a.ctl.info[0] = P;
+        a.ctl.info[1] = pre + lc;
+    }
+}
+
+// Write pass of a closing-free step (no count pass): persistent blocks over
+// contiguous pair ranges; a valid pair (cand not among the row's values) goes to
+// output row woff[r] + j - #(row values in the segment before it).
+struct JFMeta {
+    uint64_t woff;          // first output row of this input row
+    uint32_t s0;            // EC segment start
+    uint32_t imask;         // output columns whose value occurs in the segment
+    uint32_t hole;          // output column of the new value; kStageW: count-only job (no output)
+    uint32_t pad;
+    uint32_t tmpl[kStageW]; // the output row with the new value's column unset (0xffffffff)
+};
+constexpr int kJFW = 256;   // window rows of the fast write (fan-out < 4 cuts chunks short)
+using JFSmem = PairSmem<JFMeta, kPT, kPI, kJFW, 1>;
+
+__global__ void __launch_bounds__(kPT) k_join_fast(const __grid_constant__ JoinStep a) {
+    extern __shared__ __align__(16) char s_dyn[];
+    uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);
+    char* s_bufs = s_dyn + JFSmem::buf_off(a.nj);
+    uint32_t* s_out = reinterpret_cast<uint32_t*>(s_dyn + JFSmem::extra_off(a.nj));   // the chunk's output rows
+    __shared__ uint64_t s_base;
+    JFSmem::init(s_bufs);
+    for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
+    if (threadIdx.x == 0) s_jr[a.nj] = a.R;
+    __syncthreads();
+    const uint32_t w = a.w, wout = a.wout;
+    auto offs = [&](uint64_t i) -> uint64_t { return __ldg(a.poff + i); };
+    auto load = [&](uint64_t r) -> JFMeta {
+        JFMeta m;
+        const uint32_t job = pairs_find_smem(s_jr, a.nj, r);
+        const JoinJob& J = a.jobs[job];
+        const uint32_t* rowp = J.M + (r - J.row0) * w;
+        const uint32_t perm = J.perm_packed, found = __ldg(a.imask + r);
+#pragma unroll
+        for (uint32_t c = 0; c < kStageW; c++) m.tmpl[c] = 0xffffffffu;
+        uint32_t im = 0;
+        for (uint32_t c = 0; c < w; c++) {
+            const uint32_t oc = (perm >> (4 * c)) & 15u;
+            m.tmpl[oc] = __ldg(rowp + c);
+            im |= ((found >> c) & 1u) << oc;
+        }
+        m.imask = im;
+        m.hole = J.nowrite ? kStageW : (perm >> (4 * w)) & 15u;
+        m.s0 = __ldg(a.s0 + r);
+        m.woff = __ldg(a.woff + r);
+        m.pad = 0;
+        return m;
+    };
+    const uint64_t P = offs(a.R);
+    uint64_t p0, p1;
+    pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
+    pair_chunks<JFMeta, kPT, kPI, kJFW, 1>(p0, p1, a.R, offs, load, s_bufs,
+                                           [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
+                                               const uint32_t (&j)[kPI], const JFMeta* sm, uint64_t) {
+        uint32_t cand[kPI];
+        bool ok[kPI];
+        uint32_t mine = 0;
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            const bool live = v[it] && sm[wi[it]].hole < kStageW;
+            cand[it] = live ? __ldg(a.ec_val + sm[wi[it]].s0 + j[it]) : 0u;
+        }
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            const JFMeta& m = sm[wi[it]];
+            bool good = v[it] && m.hole < kStageW;
+#pragma unroll
+            for (uint32_t c = 0; c < kStageW; c++) good = good && m.tmpl[c] != cand[it];   // injectivity (Def. 2)
+            ok[it] = good;
+            mine += good ? 1u : 0u;
+        }
+        // the chunk's outputs are consecutive rows: stage them in pair order, then one
+        // coalesced copy to the row of the chunk's first output (the only position that
+        // needs the row's own values counted: woff[r] + j - #(own values before it))
+        uint32_t tot;
+        uint32_t lpos = block_excl_scan(mine, &tot);
+        if (tot == 0) return;
+        if (mine && lpos == 0) {
+            int f = 0;
+#pragma unroll
+            for (int it = kPI - 1; it >= 0; it--)
+                if (ok[it]) f = it;
+            const JFMeta& m = sm[wi[f]];
+            uint32_t before = 0;
+#pragma unroll
+            for (uint32_t c = 0; c < kStageW; c++) before += ((m.imask >> c) & 1u) && m.tmpl[c] < cand[f];
+            s_base = m.woff + j[f] - before;
+        }
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            if (!ok[it]) continue;
+            const JFMeta& m = sm[wi[it]];
+            uint32_t* dst = s_out + (size_t)(lpos++) * wout;
+#pragma unroll
+            for (uint32_t c = 0; c < kStageW; c++)
+                if (c < wout) dst[c] = c == m.hole ? cand[it] : m.tmpl[c];
+        }
+        __syncthreads();
+        copy_out(a.out + s_base * wout, s_out, tot * wout);
+        __syncthreads();
+    });
+}
+
+void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint32_t G) {
+    if (s.wout > kStageW) fail(GPS_EINVAL, "internal: fast join row too wide");
+    static std::once_flag once;
+    std::call_once(once, [] {
+        GPS_CK(cudaFuncSetAttribute(k_join_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)JFSmem::bytes(kMaxJobsPerLaunch, sizeof(uint32_t) * kTile * kStageW)));
+    });
+    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), JFSmem::bytes(s.nj, sizeof(uint32_t) * kTile * s.wout),
+           k_join_fast, s);
+}
+
+static size_t join_v_smem(uint32_t nj, uint32_t wout) {
+    return JVSmem::bytes(nj, sizeof(uint32_t) * kTile * wout);
+}
+
 static size_t join_smem(uint32_t nj, int mode, uint32_t wout) {
     const size_t out = mode == 2 ? sizeof(uint32_t) * kTile * wout
                                  : (mode == 1 ? sizeof(uint32_t) * kTile * kStageW : 0);
@@ -409,6 +735,8 @@ static void allow_join_smem() {
                                     (int)join_smem(kMaxJobsPerLaunch, 1, 0)));
         GPS_CK(cudaFuncSetAttribute(k_join<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)join_smem(kMaxJobsPerLaunch, 2, GPS_MAX_QV)));
+        GPS_CK(cudaFuncSetAttribute(k_join_v, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)join_v_smem(kMaxJobsPerLaunch, kStageW)));
     });
 }
 
@@ -456,8 +784,12 @@ void run_join_tiles(gps_ctx* c, const JoinStep& s, uint64_t P) {
     if (s.wout > GPS_MAX_QV) fail(GPS_EINVAL, "internal: join row too wide");
     allow_join_smem();
     LbScratch lb = lb_scratch(c, 1, (uint32_t)nt);
-    launch(c, GPS_K_JOIN_WRITE, dim3((uint32_t)nt), dim3(kPT), join_smem(s.nj, 2, s.wout), k_join<2>, s, lb,
-           (uint32_t)nt, lb_next_epoch(c));
+    if (s.wout <= kStageW)
+        launch(c, GPS_K_JOIN_WRITE, dim3((uint32_t)nt), dim3(kPT), join_v_smem(s.nj, s.wout), k_join_v, s, lb,
+               (uint32_t)nt, lb_next_epoch(c));
+    else
+        launch(c, GPS_K_JOIN_WRITE, dim3((uint32_t)nt), dim3(kPT), join_smem(s.nj, 2, s.wout), k_join<2>, s, lb,
+               (uint32_t)nt, lb_next_epoch(c));
 }
 
 }  // namespace gps

@@ -21,6 +21,7 @@ LbScratch lb_scratch(gps_ctx* c, uint32_t slots, uint32_t tiles_needed);
 uint32_t lb_next_epoch(gps_ctx* c);
 
 constexpr uint32_t kMaxJobsPerLaunch = 2048;   // job prefix staged in shared memory
+constexpr uint32_t kJoinStageCols = 8;          // join rows of <= 8 columns are staged in shared memory
 
 // ---- a2 kernel_check (Def. 3; Alg. 2 line 7 P:723) -------------------
 struct QDesc {
@@ -135,6 +136,7 @@ struct JoinJob {           // one query's share of a join step
     uint32_t nclose, close0;
     uint32_t final_;       // last step: write in query-vertex order (perm)
     uint32_t nowrite;      // count only (gps_count's last level)
+    uint32_t perm_packed;  // perm (identity unless final_) in nibbles, rows of <= kJoinStageCols columns
     uint8_t perm[GPS_MAX_QV + 1];
 };
 struct JoinStep {
@@ -149,13 +151,26 @@ struct JoinStep {
     PassCtl ctl;
     uint32_t* out;         // output rows of the writing jobs, job order
     uint64_t plo = 0, phi = ~0ull;   // pair sub-range to process (row-sharded join); phi == ~0: all pairs
+    // closing-free steps (every job): validity is injectivity only, so a row's outputs are its
+    // segment minus the row's own values.  imask[r] = which of row r's values occur in its
+    // segment (binary searches in the seg pass); aoff / woff = exclusive scans of all / written
+    // outputs per row (R+1).  The count pass disappears and the write pass places each pair
+    // at woff[r] + j - #(row values in the segment before it).
+    int fast = 0;
+    uint32_t* imask = nullptr;
+    uint64_t* aoff = nullptr;
+    uint64_t* woff = nullptr;
 };
 // Row-sharded join: for each target pair range [lo[t], hi[t]) of the local pair
 // space (poff[0..R]), the local row range [i0, i1) covering it and poff[i0]
 // (rows[3t .. 3t+2]).
 void run_rows_for_ranges(gps_ctx* c, const uint64_t* poff, uint64_t R, const uint64_t* d_lohi, uint32_t n,
                          uint64_t* d_rows);
-void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (one look-back pass)
+void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (+ imask / aoff / woff if fast)
+// fast steps: per-job totals total[j] = aoff[row0(j+1)] - aoff[row0(j)]
+void run_join_job_totals(gps_ctx* c, const JoinStep& s);
+// fast steps: write pass over all P pairs (rows of count-only jobs are skipped)
+void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint32_t G);
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G);
 void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G);
 // Single pass (no count pass): P = pairs of the step (poff[R]); out must hold P rows

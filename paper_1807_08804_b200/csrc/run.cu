@@ -206,6 +206,14 @@ void filter_phase(Chunk& ch, int stage) {
         e.dir = (uint32_t)dir;
         return e;
     };
+    struct Staged {
+        uint32_t* const* xs = nullptr;
+        const CollectJob *cj = nullptr, *cp = nullptr;
+        const ExploreJob *ej = nullptr, *pj = nullptr;
+        const PostJob *post1 = nullptr, *post2 = nullptr;
+        uint32_t ncj = 0, ncp = 0, nej = 0, npj = 0, np1 = 0, np2 = 0;
+    };
+    std::vector<Staged> staged;
     for (size_t s = 0; s < S; s++) {
         std::vector<CollectJob> cj;
         std::vector<ExploreJob> ej, pj;
@@ -251,18 +259,39 @@ void filter_phase(Chunk& ch, int stage) {
             }
         }
         if (cj.empty()) continue;
-        uint32_t* const* dxs = upload(c, xs, ch.keep);
-        run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
-        run_explore(c, d, upload(c, ej, ch.keep), (uint32_t)ej.size(), GPS_K_EXPLORE);
-        run_post(c, d, upload(c, post1, ch.keep), dxs, (uint32_t)post1.size());
-        if (pj.empty()) continue;
-        // re-collect the pruned vertices: propagation walks only the survivors
-        std::vector<CollectJob> cp;
-        for (const CollectJob& x : cj)
-            if (std::any_of(pj.begin(), pj.end(), [&](const ExploreJob& e) { return e.candS == x.carr; })) cp.push_back(x);
-        if (!cp.empty()) run_collect(c, d, upload(c, cp, ch.keep), (uint32_t)cp.size());
-        run_explore(c, d, upload(c, pj, ch.keep), (uint32_t)pj.size(), GPS_K_PROPAGATE);
-        run_post(c, d, upload(c, post2, ch.keep), dxs, (uint32_t)post2.size());
+        // stage every job array of the step now; the launches below all run after the loop
+        // (one host->device copy covers the whole filter phase)
+        Staged x;
+        x.xs = upload(c, xs, ch.keep);
+        x.cj = upload(c, cj, ch.keep);
+        x.ncj = (uint32_t)cj.size();
+        x.ej = upload(c, ej, ch.keep);
+        x.nej = (uint32_t)ej.size();
+        x.post1 = upload(c, post1, ch.keep);
+        x.np1 = (uint32_t)post1.size();
+        if (!pj.empty()) {
+            // re-collect the pruned vertices: propagation walks only the survivors
+            std::vector<CollectJob> cp;
+            for (const CollectJob& y : cj)
+                if (std::any_of(pj.begin(), pj.end(), [&](const ExploreJob& e) { return e.candS == y.carr; }))
+                    cp.push_back(y);
+            x.cp = cp.empty() ? nullptr : upload(c, cp, ch.keep);
+            x.ncp = (uint32_t)cp.size();
+            x.pj = upload(c, pj, ch.keep);
+            x.npj = (uint32_t)pj.size();
+            x.post2 = upload(c, post2, ch.keep);
+            x.np2 = (uint32_t)post2.size();
+        }
+        staged.push_back(x);
+    }
+    for (const Staged& x : staged) {
+        run_collect(c, d, x.cj, x.ncj);
+        run_explore(c, d, x.ej, x.nej, GPS_K_EXPLORE);
+        run_post(c, d, x.post1, x.xs, x.np1);
+        if (!x.npj) continue;
+        if (x.ncp) run_collect(c, d, x.cp, x.ncp);
+        run_explore(c, d, x.pj, x.npj, GPS_K_PROPAGATE);
+        run_post(c, d, x.post2, x.xs, x.np2);
     }
 }
 
@@ -703,6 +732,8 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
                 for (uint32_t col = 0; col < w; col++) j.perm[col] = q->vert_of_col[col];
                 j.perm[w] = (uint8_t)st.nv;
             }
+            for (uint32_t col = 0; col <= w && col < kJoinStageCols; col++)
+                j.perm_packed |= (last ? (uint32_t)j.perm[col] : col) << (4 * col);
             jj.push_back(j);
             R += q->R;
         }
@@ -720,23 +751,43 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         js.s0 = s0.as<uint32_t>();
         js.poff = poff.as<uint64_t>();
         js.ctl = PassCtl{blk.as<uint64_t>(), c->d_done, c->d_info};
-        run_join_seg(c, js);
-        const uint64_t P0 = d2h_u64(c, js.poff + R, 1)[0];
         bool any_write = false;
         for (const JoinJob& x : jj) any_write |= !x.nowrite;
-        // single pass when an output block of P0 rows (an upper bound) is affordable: no
-        // count pass; else count -> exact allocation -> write
-        const bool single = !any_write || (double)P0 * 4.0 * (w + 1) <= single_pass_bytes();
+        // closing-free step with narrow rows: the seg pass finds each row's own values in its
+        // segment, which fixes every output position -- no count pass, one sync
+        const bool fast = cl.empty() && w + 1 <= kJoinStageCols && std::getenv("GPS_NO_FAST_JOIN") == nullptr;
+        DevPtr imask, aoff, woff;
+        if (fast) {
+            imask = DevPtr(c, sizeof(uint32_t) * (R + 1));
+            aoff = DevPtr(c, sizeof(uint64_t) * (R + 1));
+            woff = DevPtr(c, sizeof(uint64_t) * (R + 1));
+            js.fast = 1;
+            js.imask = imask.as<uint32_t>();
+            js.aoff = aoff.as<uint64_t>();
+            js.woff = woff.as<uint64_t>();
+        }
+        run_join_seg(c, js);
         Block ob;
-        if (single) {
-            if (any_write && P0) {
-                ob = make_block(c, sizeof(uint32_t) * P0 * (w + 1));
-                js.out = static_cast<uint32_t*>(ob->p);
-            }
-            if (P0) run_join_tiles(c, js, P0);
-            else GPS_CK(cudaMemsetAsync(c->d_info, 0, 16, c->stream));
+        bool single = false;
+        if (fast) {
+            run_join_job_totals(c, js);
+            GPS_CK(cudaMemcpyAsync(c->d_info, js.poff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
+            GPS_CK(cudaMemcpyAsync(c->d_info + 1, js.woff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
         } else {
-            run_join_count(c, js, G);
+            const uint64_t P0 = d2h_u64(c, js.poff + R, 1)[0];
+            // single pass when an output block of P0 rows (an upper bound) is affordable: no
+            // count pass; else count -> exact allocation -> write
+            single = !any_write || (double)P0 * 4.0 * (w + 1) <= single_pass_bytes();
+            if (single) {
+                if (any_write && P0) {
+                    ob = make_block(c, sizeof(uint32_t) * P0 * (w + 1));
+                    js.out = static_cast<uint32_t*>(ob->p);
+                }
+                if (P0) run_join_tiles(c, js, P0);
+                else GPS_CK(cudaMemsetAsync(c->d_info, 0, 16, c->stream));
+            } else {
+                run_join_count(c, js, G);
+            }
         }
         std::vector<uint64_t> tot(act.size());
         uint64_t P = 0, writes = 0;
@@ -751,16 +802,17 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             writes = h[act.size() + 1];
             pinned_release(c, h, got);
         }
-        tr.mark(single ? "join step synced (single pass)" : "join step synced");
+        tr.mark(fast ? "join step synced (fast)" : single ? "join step synced (single pass)" : "join step synced");
         if (single) {
             c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)P + 4.0 * (w + 1) * (double)writes;
         } else {
-            c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)P;
+            if (!fast) c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)P;
             if (writes) {
                 if (writes > (~0ull) / (4ull * (w + 1))) fail(GPS_EOVERFLOW, "result size overflows");
                 ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
                 js.out = static_cast<uint32_t*>(ob->p);
-                run_join_write(c, js, G);
+                if (fast) run_join_fast_write(c, js, G);
+                else run_join_write(c, js, G);
                 c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)P +
                                                       4.0 * (w + 1) * (double)writes;
             }

@@ -164,6 +164,46 @@ class _QueryArrays:
                               _addr(self.e) if self.e.shape[0] else None)
 
 
+_QDESC_DTYPE = np.dtype([("k", "<u4"), ("ne", "<u4"), ("vl", "<u8"), ("bd", "<u8"), ("e", "<u8")])
+assert _QDESC_DTYPE.itemsize == ctypes.sizeof(QueryDesc)
+
+
+class QueryBatch:
+    """A list of queries marshalled ONCE into contiguous arrays + a gps_query array.
+
+    Pass it instead of a list to the batch calls to keep per-call host work at a
+    single library call (the descriptors stay valid while this object lives)."""
+
+    def __init__(self, queries):
+        qs = [q if not isinstance(q, dict) else _DictQuery(q) for q in queries]
+        self.n = len(qs)
+        ks = np.fromiter((int(q.k) for q in qs), np.int64, self.n)
+        nes = np.fromiter((len(q.edges) for q in qs), np.int64, self.n)
+        self.vl = np.ascontiguousarray([int(x) for q in qs for x in q.vlabels], dtype=np.int32)
+        self.bd = np.ascontiguousarray([int(x) for q in qs for x in q.bound], dtype=np.int64)
+        self.e = np.ascontiguousarray([int(x) for q in qs for ed in q.edges for x in ed], dtype=np.int32)
+        if self.vl.shape[0] != ks.sum() or self.bd.shape[0] != ks.sum() or self.e.shape[0] != 3 * nes.sum():
+            raise ValueError("query arrays do not match their sizes")
+        vo = np.concatenate([[0], np.cumsum(ks)[:-1]]) if self.n else ks
+        eo = np.concatenate([[0], np.cumsum(nes)[:-1]]) if self.n else nes
+        d = np.zeros(max(self.n, 1), _QDESC_DTYPE)
+        d["k"][: self.n] = ks
+        d["ne"][: self.n] = nes
+        d["vl"][: self.n] = self.vl.ctypes.data + 4 * vo if self.vl.size else 0
+        d["bd"][: self.n] = self.bd.ctypes.data + 8 * vo if self.bd.size else 0
+        d["e"][: self.n] = np.where(nes > 0, self.e.ctypes.data + 12 * eo, 0) if self.e.size else 0
+        self.desc = d
+        self.arr = ctypes.cast(ctypes.c_void_p(d.ctypes.data), ctypes.POINTER(QueryDesc))
+
+    def __len__(self):
+        return self.n
+
+
+class _DictQuery:
+    def __init__(self, d):
+        self.k, self.vlabels, self.bound, self.edges = d["k"], d["vlabels"], d["bound"], d["edges"]
+
+
 class _DeviceRows:
     """Owner of a device gps_result; exposes __cuda_array_interface__ for torch."""
 
@@ -401,11 +441,8 @@ class Context:
         return flat[: rows.value * qa.k].reshape(rows.value, qa.k)
 
     def _batch_desc(self, queries):
-        qas = [_QueryArrays(q) for q in queries]
-        arr = (QueryDesc * max(len(qas), 1))()
-        for i, qa in enumerate(qas):
-            arr[i] = qa.desc
-        return qas, arr
+        qb = queries if isinstance(queries, QueryBatch) else QueryBatch(queries)
+        return [None] * qb.n, qb.arr, qb
 
     def match_batch(self, graph: Graph, queries, opts: Optional[MatchOpts] = None, device: bool = True):
         """All embeddings of every query, run concurrently by the library's worker pool.
@@ -413,7 +450,7 @@ class Context:
         Returns a list of torch uint32 (rows, k) CUDA tensors (zero-copy), or of
         numpy arrays copied to host by the library when device=False."""
         import torch
-        qas, arr = self._batch_desc(queries)
+        qas, arr, _qb = self._batch_desc(queries)
         n = len(qas)
         res = (ctypes.c_void_p * max(n, 1))()
         st = np.zeros(max(n, 1), np.int32)
@@ -445,7 +482,7 @@ class Context:
 
     def match_batch_raw(self, graph: Graph, queries, opts: Optional[MatchOpts] = None) -> "BatchResult":
         """Like match_batch but returns a BatchResult (row counts + lazily wrapped tensors)."""
-        qas, arr = self._batch_desc(queries)
+        qas, arr, _qb = self._batch_desc(queries)
         n = len(qas)
         res = (ctypes.c_void_p * max(n, 1))()
         o = opts if opts is not None else default_opts()
@@ -458,7 +495,7 @@ class Context:
     def match_batch_host(self, graph: Graph, queries, out, opts: Optional[MatchOpts] = None):
         """All embeddings copied by the library into ONE host buffer `out` (numpy uint32 or a
         pinned torch tensor).  Returns (offsets, rows) numpy arrays (word offsets into out)."""
-        qas, arr = self._batch_desc(queries)
+        qas, arr, _qb = self._batch_desc(queries)
         n = len(qas)
         offs = np.zeros(max(n, 1), np.uint64)
         rows = np.zeros(max(n, 1), np.uint64)
@@ -470,7 +507,7 @@ class Context:
         return offs[:n], rows[:n]
 
     def count_batch(self, graph: Graph, queries, opts: Optional[MatchOpts] = None) -> np.ndarray:
-        qas, arr = self._batch_desc(queries)
+        qas, arr, _qb = self._batch_desc(queries)
         n = len(qas)
         counts = np.zeros(max(n, 1), np.uint64)
         _check(lib.gps_count_batch(self._h, graph.handle, arr, n,

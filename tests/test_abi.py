@@ -8,6 +8,8 @@ import ctypes
 import os
 import re
 
+import numpy as np
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -74,3 +76,25 @@ def test_kernel_sass_is_sm100a(gps):
         pytest.skip("cuobjdump missing")
     out = subprocess.run([exe, "--list-elf", gps.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_query_batch_marshalling():
+    """QueryBatch's gps_query array decodes back to the queries (pointers into its arrays)."""
+    import ctypes
+    from paper_1807_08804_b200 import gpsense
+    import corpus
+    from synth import Query
+    qs = [corpus.instance(s)[1] for s in range(12)] + [Query(1, [3], [-1], [])]
+    qb = gpsense.QueryBatch(qs)
+    assert len(qb) == len(qs)
+    for i, q in enumerate(qs):
+        d = qb.arr[i]
+        assert d.n_vertices == q.k and d.n_edges == len(q.edges)
+        vl = np.ctypeslib.as_array(ctypes.cast(d.vertex_labels, ctypes.POINTER(ctypes.c_int32)), (q.k,))
+        bd = np.ctypeslib.as_array(ctypes.cast(d.bound, ctypes.POINTER(ctypes.c_int64)), (q.k,))
+        assert vl.tolist() == list(q.vlabels) and bd.tolist() == list(q.bound)
+        if q.edges:
+            e = np.ctypeslib.as_array(ctypes.cast(d.edges, ctypes.POINTER(ctypes.c_int32)), (len(q.edges), 3))
+            assert [tuple(x) for x in e.tolist()] == [tuple(x) for x in q.edges]
+        else:
+            assert not d.edges

@@ -89,10 +89,14 @@ def test_random_corpus(ctx, seed):
     _check(ctx, ctx.load_graph(g), og, q)
 
 
+@pytest.mark.parametrize("env", ["GPS_SINGLE_PASS_BYTES=0", "GPS_NO_FAST_JOIN=1"])
 @pytest.mark.parametrize("seed", range(0, 200, 5))
-def test_random_corpus_two_pass_join(ctx, seed, monkeypatch):
-    """Same corpus with every join step forced onto count -> exact allocation -> write."""
-    monkeypatch.setenv("GPS_SINGLE_PASS_BYTES", "0")
+def test_random_corpus_other_join_paths(ctx, seed, env, monkeypatch):
+    """Same corpus with the closing-free fast path off (GPS_NO_FAST_JOIN: look-back tiles) and
+    additionally the single pass off (GPS_SINGLE_PASS_BYTES=0: count -> exact allocation -> write)."""
+    monkeypatch.setenv("GPS_NO_FAST_JOIN", "1")
+    k, v = env.split("=")
+    monkeypatch.setenv(k, v)
     g, q = _instance(seed)
     og = oracle.OracleGraph(g)
     try:
@@ -204,9 +208,12 @@ def test_cfg2_counts_all_queries(ctx, cfg2):
         assert ctx.count(G, q) == item["oracle_count"], item["seed"]
 
 
-def test_cfg2_two_pass_join(ctx, cfg2, monkeypatch):
-    """Full-size config 2 with the count -> write join: same counts as the single-pass join."""
-    monkeypatch.setenv("GPS_SINGLE_PASS_BYTES", "0")
+@pytest.mark.parametrize("env", ["GPS_SINGLE_PASS_BYTES=0", "GPS_NO_FAST_JOIN=1"])
+def test_cfg2_other_join_paths(ctx, cfg2, env, monkeypatch):
+    """Full-size config 2 through the look-back-tile join and the count -> write join."""
+    monkeypatch.setenv("GPS_NO_FAST_JOIN", "1")
+    k, v = env.split("=")
+    monkeypatch.setenv(k, v)
     g, G, data = cfg2
     for item in data["queries"][:20]:
         assert ctx.count(G, Query.from_json(item["query"])) == item["oracle_count"], item["seed"]
