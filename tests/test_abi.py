@@ -23,7 +23,11 @@ def _declared():
 
 @pytest.fixture(scope="module")
 def gps():
-    from paper_1807_08804_b200 import _build
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_gps_build", os.path.join(ROOT, "paper_1807_08804_b200", "_build.py"))
+    _build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(_build)   # by path: the package __init__ needs the built .so
     _build.build()
     from paper_1807_08804_b200 import gpsense
     return gpsense
