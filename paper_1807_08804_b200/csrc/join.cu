@@ -161,8 +161,10 @@ void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uin
 }
 
 // ------------------------------------------------------------ a8 join step
-constexpr int kSegRows = 4;
-constexpr int kSegTile = 256 * kSegRows;
+// rows per thread: the plain pass is a short load chain per row, so 4 rows amortise the
+// scan; the FAST pass runs w binary searches per row, one dependent chain per thread.
+template <bool FAST> constexpr int seg_rows() { return FAST ? 1 : 4; }
+template <bool FAST> constexpr int seg_tile() { return 256 * seg_rows<FAST>(); }
 
 // largest j < nj with jobs[j].row0 <= r
 __device__ __forceinline__ uint32_t job_of_row(const JoinJob* __restrict__ jobs, uint32_t nj, uint64_t r) {
@@ -182,6 +184,7 @@ __device__ __forceinline__ uint32_t job_of_row(const JoinJob* __restrict__ jobs,
 template <bool FAST>
 __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
                                                   uint32_t epoch) {
+    constexpr int kSegRows = seg_rows<FAST>(), kSegTile = seg_tile<FAST>();
     __shared__ uint64_t s_pre[3];
     const uint32_t tile = lb_ticket(lb.ctr, ntiles);
     const uint64_t r0 = (uint64_t)tile * kSegTile + (uint64_t)threadIdx.x * kSegRows;
@@ -284,7 +287,8 @@ __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinSt
 }
 
 void run_join_seg(gps_ctx* c, const JoinStep& s) {
-    const uint64_t nt = (s.R + kSegTile - 1) / kSegTile;
+    const uint64_t tile = s.fast ? seg_tile<true>() : seg_tile<false>();
+    const uint64_t nt = (s.R + tile - 1) / tile;
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join table too large");
     LbScratch lb = lb_scratch(c, 3, (uint32_t)nt);
     if (s.fast)
@@ -602,29 +606,44 @@ __global__ void __launch_bounds__(kPT) k_join_v(const __grid_constant__ JoinStep
 
 // Write pass of a closing-free step (no count pass): persistent blocks over
 // contiguous pair ranges; a valid pair (cand not among the row's values) goes to
-// output row woff[r] + j - #(row values in the segment before it).
-struct JFMeta {
+// output row woff[r] + j - #(row values in the segment before it).  The chunk's
+// outputs are consecutive rows, so the chunk stages only (new value, window row)
+// per output row and the block then writes the rows WORD-parallel: thread x forms
+// words 4x..4x+3 of the chunk's output (template word or the new value) and
+// stores them as one 16-byte vector -- every warp store is 512 contiguous bytes.
+struct __align__(16) JFMeta {
+    uint32_t tmpl[kStageW]; // the output row with the new value's column unset (0xffffffff)
     uint64_t woff;          // first output row of this input row
     uint32_t s0;            // EC segment start
     uint32_t imask;         // output columns whose value occurs in the segment
     uint32_t hole;          // output column of the new value; kStageW: count-only job (no output)
-    uint32_t pad;
-    uint32_t tmpl[kStageW]; // the output row with the new value's column unset (0xffffffff)
 };
-constexpr int kJFW = 256;   // window rows of the fast write (fan-out < 4 cuts chunks short)
+constexpr int kJFW = 512;   // window rows of the fast write (fan-out < 2 cuts chunks short)
 using JFSmem = PairSmem<JFMeta, kPT, kPI, kJFW, 1>;
+__host__ __device__ constexpr size_t jf_stage(uint32_t) { return sizeof(uint2) * kTile; }
 
-__global__ void __launch_bounds__(kPT) k_join_fast(const __grid_constant__ JoinStep a) {
+template <uint32_t WOUT>
+__device__ __forceinline__ void jf_tmpl(const JFMeta& m, uint32_t (&t)[WOUT]) {
+    const uint4* tp = reinterpret_cast<const uint4*>(m.tmpl);
+    const uint4 x0 = tp[0];
+    const uint4 x1 = WOUT > 4 ? tp[1] : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t all[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+    for (uint32_t c = 0; c < WOUT; c++) t[c] = all[c];
+}
+
+template <uint32_t WOUT>
+__global__ void __launch_bounds__(kPT, 4) k_join_fast(const __grid_constant__ JoinStep a) {
     extern __shared__ __align__(16) char s_dyn[];
     uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);
     char* s_bufs = s_dyn + JFSmem::buf_off(a.nj);
-    uint32_t* s_out = reinterpret_cast<uint32_t*>(s_dyn + JFSmem::extra_off(a.nj));   // the chunk's output rows
+    uint2* s_ri = reinterpret_cast<uint2*>(s_dyn + JFSmem::extra_off(a.nj));   // (new value, window row) per output row
     __shared__ uint64_t s_base;
     JFSmem::init(s_bufs);
     for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
     if (threadIdx.x == 0) s_jr[a.nj] = a.R;
     __syncthreads();
-    const uint32_t w = a.w, wout = a.wout;
+    constexpr uint32_t w = WOUT - 1;
     auto offs = [&](uint64_t i) -> uint64_t { return __ldg(a.poff + i); };
     auto load = [&](uint64_t r) -> JFMeta {
         JFMeta m;
@@ -632,19 +651,26 @@ __global__ void __launch_bounds__(kPT) k_join_fast(const __grid_constant__ JoinS
         const JoinJob& J = a.jobs[job];
         const uint32_t* rowp = J.M + (r - J.row0) * w;
         const uint32_t perm = J.perm_packed, found = __ldg(a.imask + r);
+        uint32_t val[w];
 #pragma unroll
-        for (uint32_t c = 0; c < kStageW; c++) m.tmpl[c] = 0xffffffffu;
+        for (uint32_t c = 0; c < w; c++) val[c] = __ldg(rowp + c);
         uint32_t im = 0;
-        for (uint32_t c = 0; c < w; c++) {
-            const uint32_t oc = (perm >> (4 * c)) & 15u;
-            m.tmpl[oc] = __ldg(rowp + c);
-            im |= ((found >> c) & 1u) << oc;
+#pragma unroll
+        for (uint32_t oc = 0; oc < kStageW; oc++) {   // select, not a dynamic index: stays in registers
+            uint32_t t = 0xffffffffu, f = 0;
+#pragma unroll
+            for (uint32_t c = 0; c < w; c++)
+                if (((perm >> (4 * c)) & 15u) == oc) {
+                    t = val[c];
+                    f = (found >> c) & 1u;
+                }
+            m.tmpl[oc] = t;
+            im |= f << oc;
         }
         m.imask = im;
         m.hole = J.nowrite ? kStageW : (perm >> (4 * w)) & 15u;
         m.s0 = __ldg(a.s0 + r);
         m.woff = __ldg(a.woff + r);
-        m.pad = 0;
         return m;
     };
     const uint64_t P = offs(a.R);
@@ -664,53 +690,101 @@ __global__ void __launch_bounds__(kPT) k_join_fast(const __grid_constant__ JoinS
 #pragma unroll
         for (int it = 0; it < kPI; it++) {
             const JFMeta& m = sm[wi[it]];
+            uint32_t t[WOUT];
+            jf_tmpl<WOUT>(m, t);
             bool good = v[it] && m.hole < kStageW;
 #pragma unroll
-            for (uint32_t c = 0; c < kStageW; c++) good = good && m.tmpl[c] != cand[it];   // injectivity (Def. 2)
+            for (uint32_t c = 0; c < WOUT; c++) good = good && t[c] != cand[it];   // injectivity (Def. 2)
             ok[it] = good;
             mine += good ? 1u : 0u;
         }
-        // the chunk's outputs are consecutive rows: stage them in pair order, then one
-        // coalesced copy to the row of the chunk's first output (the only position that
-        // needs the row's own values counted: woff[r] + j - #(own values before it))
         uint32_t tot;
         uint32_t lpos = block_excl_scan(mine, &tot);
         if (tot == 0) return;
-        if (mine && lpos == 0) {
-            int f = 0;
+        if (mine && lpos == 0) {   // the chunk's first output: its global row fixes the chunk's base
+            uint32_t fc = 0, fw = 0, fj = 0;   // selected, not indexed (keeps the arrays in registers)
 #pragma unroll
             for (int it = kPI - 1; it >= 0; it--)
-                if (ok[it]) f = it;
-            const JFMeta& m = sm[wi[f]];
+                if (ok[it]) {
+                    fc = cand[it];
+                    fw = wi[it];
+                    fj = j[it];
+                }
+            const JFMeta& m = sm[fw];
             uint32_t before = 0;
 #pragma unroll
-            for (uint32_t c = 0; c < kStageW; c++) before += ((m.imask >> c) & 1u) && m.tmpl[c] < cand[f];
-            s_base = m.woff + j[f] - before;
+            for (uint32_t c = 0; c < WOUT; c++) before += ((m.imask >> c) & 1u) && m.tmpl[c] < fc;
+            s_base = m.woff + fj - before;
         }
 #pragma unroll
         for (int it = 0; it < kPI; it++) {
             if (!ok[it]) continue;
-            const JFMeta& m = sm[wi[it]];
-            uint32_t* dst = s_out + (size_t)(lpos++) * wout;
-#pragma unroll
-            for (uint32_t c = 0; c < kStageW; c++)
-                if (c < wout) dst[c] = c == m.hole ? cand[it] : m.tmpl[c];
+            s_ri[lpos++] = make_uint2(cand[it], wi[it]);
         }
         __syncthreads();
-        copy_out(a.out + s_base * wout, s_out, tot * wout);
+        // word-parallel: thread x forms words 4x..4x+3 of the chunk's output (a template
+        // word of the row's input row, or the new value) and stores one 16-byte vector
+        uint32_t* g = a.out + s_base * WOUT;
+        const uint32_t words = tot * WOUT;
+        const uint32_t head = min(words, (uint32_t)((16u - ((uintptr_t)g & 15u)) & 15u) >> 2);
+        auto word_at = [&](uint32_t row, uint32_t col) -> uint32_t {
+            const uint2 ri = s_ri[row];
+            const JFMeta& m = sm[ri.y];
+            return col == m.hole ? ri.x : m.tmpl[col];
+        };
+        if (threadIdx.x < head) g[threadIdx.x] = word_at(threadIdx.x / WOUT, threadIdx.x % WOUT);
+        const uint32_t nvec = (words - head) >> 2;
+        uint4* g4 = reinterpret_cast<uint4*>(g + head);
+        for (uint32_t x = threadIdx.x; x < nvec; x += kPT) {
+            const uint32_t o = head + 4 * x;
+            uint32_t row = o / WOUT, col = o - row * WOUT, wv[4];
+            uint2 ri = s_ri[row];
+            const JFMeta* m = sm + ri.y;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {   // 4 consecutive words: one division, row info reloaded per row
+                wv[k] = col == m->hole ? ri.x : m->tmpl[col];
+                if (++col == WOUT && k < 3) {
+                    col = 0;
+                    ri = s_ri[++row];
+                    m = sm + ri.y;
+                }
+            }
+            g4[x] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+        for (uint32_t o = head + 4 * nvec + threadIdx.x; o < words; o += kPT) g[o] = word_at(o / WOUT, o % WOUT);
         __syncthreads();
     });
 }
 
-void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint32_t G) {
-    if (s.wout > kStageW) fail(GPS_EINVAL, "internal: fast join row too wide");
+
+template <uint32_t WOUT>
+static void launch_join_fast(gps_ctx* c, const JoinStep& s, uint64_t P) {
     static std::once_flag once;
-    std::call_once(once, [] {
-        GPS_CK(cudaFuncSetAttribute(k_join_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)JFSmem::bytes(kMaxJobsPerLaunch, sizeof(uint32_t) * kTile * kStageW)));
+    static int occ = 1;
+    const size_t smax = JFSmem::bytes(kMaxJobsPerLaunch, jf_stage(WOUT));
+    std::call_once(once, [&] {
+        GPS_CK(cudaFuncSetAttribute(k_join_fast<WOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+        GPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_join_fast<WOUT>, kPT,
+                                                             JFSmem::bytes(64, jf_stage(WOUT))));
+        if (occ < 1) occ = 1;
     });
-    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), JFSmem::bytes(s.nj, sizeof(uint32_t) * kTile * s.wout),
-           k_join_fast, s);
+    // one resident wave; no more blocks than chunks (a block's fixed cost is a global search)
+    const uint64_t chunks = (P + kTile - 1) / kTile;
+    const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->nsm * occ, chunks));
+    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), JFSmem::bytes(s.nj, jf_stage(WOUT)), k_join_fast<WOUT>, s);
+}
+
+void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint64_t P) {
+    switch (s.wout) {
+        case 2: return launch_join_fast<2>(c, s, P);
+        case 3: return launch_join_fast<3>(c, s, P);
+        case 4: return launch_join_fast<4>(c, s, P);
+        case 5: return launch_join_fast<5>(c, s, P);
+        case 6: return launch_join_fast<6>(c, s, P);
+        case 7: return launch_join_fast<7>(c, s, P);
+        case 8: return launch_join_fast<8>(c, s, P);
+        default: fail(GPS_EINVAL, "internal: fast join row width out of range");
+    }
 }
 
 static size_t join_v_smem(uint32_t nj, uint32_t wout) {

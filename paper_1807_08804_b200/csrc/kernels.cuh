@@ -170,7 +170,7 @@ void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (+ imask / a
 // fast steps: per-job totals total[j] = aoff[row0(j+1)] - aoff[row0(j)]
 void run_join_job_totals(gps_ctx* c, const JoinStep& s);
 // fast steps: write pass over all P pairs (rows of count-only jobs are skipped)
-void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint32_t G);
+void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint64_t P);
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G);
 void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G);
 // Single pass (no count pass): P = pairs of the step (poff[R]); out must hold P rows

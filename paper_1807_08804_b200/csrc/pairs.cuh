@@ -209,17 +209,25 @@ __device__ __forceinline__ void pair_chunks(uint64_t p0, uint64_t p1, uint64_t n
         uint64_t cend = cp + CH < p1 ? cp + CH : p1;
         if (cend > wend) cend = wend;   // window exhausted: cut the chunk (wend > cp: row r0 contains cp)
         const uint32_t n = (uint32_t)(cend - cp);
-        for (uint32_t i = tid; i < wn; i += T) {
-            const uint64_t a = offs(r0 + i), b = offs(r0 + i + 1);
-            if (a < cend && b > cp && b > a) {   // a non-empty row meeting the chunk
-                const uint32_t rs = a > cp ? (uint32_t)(a - cp) : 0u;
-                const uint32_t re = (uint32_t)((b < cend ? b : cend) - cp);
-                s_start[i] = (uint32_t)(a - cp);   // mod 2^32: j = pair - start
-                if (rs) s_mark[rs] = (uint16_t)i;
-                for (uint32_t wb = (rs + WSPAN - 1) / WSPAN * WSPAN; wb < re; wb += WSPAN) s_wrow[wb / WSPAN] = i;
-                s_meta[i] = load_meta(r0 + i);
+        // scan the window T rows at a time and stop at the first T-row block starting past
+        // cend (uniform: every thread reads the same offset) -- a chunk of long rows costs
+        // one block of offsets, not the whole window
+        for (uint32_t base = 0; base < wn; base += T) {
+            const uint32_t i = base + tid;
+            if (i < wn) {
+                const uint64_t a = offs(r0 + i), b = offs(r0 + i + 1);
+                if (a < cend && b > cp && b > a) {   // a non-empty row meeting the chunk
+                    const uint32_t rs = a > cp ? (uint32_t)(a - cp) : 0u;
+                    const uint32_t re = (uint32_t)((b < cend ? b : cend) - cp);
+                    s_start[i] = (uint32_t)(a - cp);   // mod 2^32: j = pair - start
+                    if (rs) s_mark[rs] = (uint16_t)i;
+                    for (uint32_t wb = (rs + WSPAN - 1) / WSPAN * WSPAN; wb < re; wb += WSPAN) s_wrow[wb / WSPAN] = i;
+                    s_meta[i] = load_meta(r0 + i);
+                }
+                if (a <= cend && cend < b) *s_next = i;   // the row containing cend (if inside the window)
             }
-            if (a <= cend && cend < b) *s_next = i;   // the row containing cend (if inside the window)
+            // rows from base+T on start after cend: none meets the chunk or contains cend
+            if (base + T < wn && offs(r0 + base + T) > cend) break;
         }
         __syncthreads();
         const uint32_t q0 = tid * IPT;

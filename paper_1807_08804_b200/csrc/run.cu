@@ -811,7 +811,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
                 if (writes > (~0ull) / (4ull * (w + 1))) fail(GPS_EOVERFLOW, "result size overflows");
                 ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
                 js.out = static_cast<uint32_t*>(ob->p);
-                if (fast) run_join_fast_write(c, js, G);
+                if (fast) run_join_fast_write(c, js, P);
                 else run_join_write(c, js, G);
                 c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)P +
                                                       4.0 * (w + 1) * (double)writes;

@@ -11,7 +11,8 @@ ctx = gpsense.Context(0)
 ctx.set_workers(1)
 ctx.set_slice(int(os.environ.get("SLICE", "100")))
 G = ctx.load_graph(config_graph(2))
-ctx.count_batch(G, qs)
+if os.environ.get("MODE", "both") != "match":
+    ctx.count_batch(G, qs)
 outs = ctx.match_batch(G, qs)
 torch.cuda.synchronize()
 print("ok", sum(t.shape[0] for t in outs))
