@@ -5,6 +5,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "kernels.cuh"
 #include "runtime.h"
@@ -156,6 +159,25 @@ LbScratch lb_scratch(gps_ctx* c, uint32_t slots, uint32_t tiles) {
     }
     return LbScratch{c->lb_status, c->lb_ctr, c->lb_tiles};
 }
+uint32_t resident_grid(gps_ctx* c, const void* func, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, size_t>, int> cache;   // (kernel, smem rounded to 1 KB) -> blocks/SM
+    const size_t key_smem = (smem + 1023) & ~size_t(1023);
+    int occ = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find({func, key_smem});
+        if (it != cache.end()) occ = it->second;
+    }
+    if (occ == 0) {
+        GPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, threads, key_smem));
+        if (occ < 1) occ = 1;
+        std::lock_guard<std::mutex> lk(mu);
+        cache[{func, key_smem}] = occ;
+    }
+    return (uint32_t)(c->nsm * occ);
+}
+
 uint32_t lb_next_epoch(gps_ctx* c) {
     c->lb_epoch++;
     if (c->lb_epoch >= (1u << 20)) {   // wrap: clear stale words so old epochs cannot alias

@@ -40,8 +40,9 @@ __global__ void __launch_bounds__(256) k_check(DevGraph g, const QDesc* __restri
         uint32_t lab = 0, od = 0, id = 0;
         if (valid) {
             lab = g.vlab[v];
-            od = g.off_out[v + 1] - g.off_out[v];
-            id = g.off_in[v + 1] - g.off_in[v];
+            const uint2 d = g.deg[v];
+            od = d.x;
+            id = d.y;
         }
         for (uint32_t qi = 0; qi < nq; qi++) {
             const QDesc& q = qs[qi];
@@ -65,13 +66,14 @@ void run_check(gps_ctx* c, const DevGraph& g, const QDesc* d_q, uint32_t nq, uin
     uint32_t blocks = std::min<uint32_t>((g.nw + 7) / 8, (uint32_t)c->nsm * 8);
     launch(c, GPS_K_CHECK, dim3(blocks), dim3(256), 0, k_check, g, d_q, nq);
     // algorithmic: the vertex data once + k/8 bytes of bitmap per vertex and query
-    c->stats.k_bytes[GPS_K_CHECK] += (double)g.n * 10.0 + (double)nq * max_k * g.nw * 4.0;
+    c->stats.k_bytes[GPS_K_CHECK] += (double)g.n * 10.0 + (double)nq * max_k * g.nw * 4.0;   // 2 + 8 B per vertex
 }
 
 // -------------------------------------------------------------- a3 collect
 constexpr int kColThreads = 256;
 constexpr int kColWords = 4;                          // bitmap words (128 vertices) per thread
 constexpr int kColTile = kColThreads * kColWords;     // words per tile
+constexpr int kColBatch = 8;                          // candidates whose degrees are loaded together
 
 __global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const CollectJob* __restrict__ jobs,
                                                          LbScratch lb, uint32_t ntiles, uint32_t epoch) {
@@ -89,16 +91,24 @@ __global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const Colle
     } else {
         word[0] = word[1] = word[2] = word[3] = 0u;
     }
+    // the candidates' degrees, kColBatch independent 8-byte loads per round trip
     uint32_t c = 0, so = 0, si = 0;
 #pragma unroll
     for (int i = 0; i < kColWords; i++) {
         c += __popc(word[i]);
         uint32_t bits = word[i];
         while (bits) {
-            const uint32_t v = (w0 + i) * 32 + __ffs(bits) - 1;
-            bits &= bits - 1;
-            so += __ldg(g.off_out + v + 1) - __ldg(g.off_out + v);
-            si += __ldg(g.off_in + v + 1) - __ldg(g.off_in + v);
+            uint2 d[kColBatch];
+#pragma unroll
+            for (int k = 0; k < kColBatch; k++) {
+                d[k] = bits ? __ldg(g.deg + (w0 + i) * 32 + __ffs(bits) - 1) : make_uint2(0u, 0u);
+                bits &= bits - 1;
+            }
+#pragma unroll
+            for (int k = 0; k < kColBatch; k++) {
+                so += d[k].x;
+                si += d[k].y;
+            }
         }
     }
     uint32_t tc, tso, tsi;
@@ -131,14 +141,24 @@ __global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const Colle
     for (int i = 0; i < kColWords; i++) {
         uint32_t bits = word[i];
         while (bits) {
-            const uint32_t v = (w0 + i) * 32 + __ffs(bits) - 1;
-            bits &= bits - 1;
-            J.carr[rank] = v;
-            J.seg_out[rank] = ro;
-            J.seg_in[rank] = ri;
-            ro += __ldg(g.off_out + v + 1) - __ldg(g.off_out + v);
-            ri += __ldg(g.off_in + v + 1) - __ldg(g.off_in + v);
-            rank++;
+            uint32_t v[kColBatch];
+            uint2 d[kColBatch];
+#pragma unroll
+            for (int k = 0; k < kColBatch; k++) {
+                v[k] = bits ? (w0 + i) * 32 + __ffs(bits) - 1 : 0xffffffffu;
+                d[k] = bits ? __ldg(g.deg + v[k]) : make_uint2(0u, 0u);
+                bits &= bits - 1;
+            }
+#pragma unroll
+            for (int k = 0; k < kColBatch; k++) {
+                if (v[k] == 0xffffffffu) break;
+                J.carr[rank] = v[k];
+                J.seg_out[rank] = ro;
+                J.seg_in[rank] = ri;
+                ro += d[k].x;
+                ri += d[k].y;
+                rank++;
+            }
         }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
@@ -182,7 +202,7 @@ __device__ __forceinline__ uint64_t ex_pairs(const ExploreJob& J, bool* s_side) 
     return ps < pa ? ps : pa;
 }
 
-__global__ void __launch_bounds__(kET, 4) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
+__global__ void __launch_bounds__(kET, 5) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
                                                 unsigned long long* bytes_acc, unsigned long long* dbg) {
     extern __shared__ __align__(16) char s_dyn[];
     uint64_t* s_jp = reinterpret_cast<uint64_t*>(s_dyn);          // [nj+1] job pair prefix
@@ -286,7 +306,7 @@ static size_t ex_smem(uint32_t nj) { return ExSmem::bytes(nj, 0); }
 void run_explore(gps_ctx* c, const DevGraph& g, const ExploreJob* d_jobs, uint32_t nj, int cls) {
     if (nj == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many jobs per launch");
-    const uint32_t G = (uint32_t)c->nsm * 6;
+    const uint32_t G = resident_grid(c, (const void*)k_explore, kET, ex_smem(nj));
     static const bool dbg = std::getenv("GPS_EXPLORE_STATS") != nullptr;
     launch(c, cls, dim3(G), dim3(kET), ex_smem(nj), k_explore, g, d_jobs, nj, c->d_bytes + cls,
            dbg ? (unsigned long long*)c->d_info + 96 + (cls == GPS_K_PROPAGATE ? 4 : 0) : nullptr);

@@ -45,6 +45,7 @@ struct DevGraph {
     const uint32_t* off_in;   // [n+1]
     const uint32_t* arc_in;   // [m]
     const uint16_t* vlab;     // [n]
+    const uint2* deg;         // [n] (out-degree, in-degree): one 8-byte load per candidate
 };
 
 __device__ __forceinline__ bool bit_test(const uint32_t* __restrict__ B, uint32_t v) {

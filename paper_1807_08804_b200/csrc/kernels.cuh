@@ -19,6 +19,9 @@ struct LbScratch {
 };
 LbScratch lb_scratch(gps_ctx* c, uint32_t slots, uint32_t tiles_needed);
 uint32_t lb_next_epoch(gps_ctx* c);
+// Blocks of `func` (block size `threads`, dynamic smem `smem`) resident at once on the
+// whole GPU: the grid of a persistent kernel, so no block waits for a second wave.
+uint32_t resident_grid(gps_ctx* c, const void* func, int threads, size_t smem);
 
 constexpr uint32_t kMaxJobsPerLaunch = 2048;   // job prefix staged in shared memory
 constexpr uint32_t kJoinStageCols = 8;          // join rows of <= 8 columns are staged in shared memory

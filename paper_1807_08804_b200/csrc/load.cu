@@ -74,6 +74,12 @@ __global__ void k_transpose_keys(const uint64_t* __restrict__ ukeys, uint64_t m,
     out[i] = (dst << pbits) | (src << lbits) | lab;
 }
 
+__global__ void k_degrees(const uint32_t* __restrict__ off_out, const uint32_t* __restrict__ off_in, uint32_t n,
+                          uint2* __restrict__ deg) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        deg[v] = make_uint2(off_out[v + 1] - off_out[v], off_in[v + 1] - off_in[v]);
+}
+
 __global__ void k_label_hist(const uint16_t* __restrict__ vlab, uint32_t n, uint32_t nl,
                              unsigned long long* __restrict__ hist) {
     extern __shared__ unsigned int s_h[];
@@ -212,6 +218,12 @@ void load_graph(gps_ctx* c, const gps_csr_desc* d, gps_graph* g) {
     std::vector<unsigned long long> h(g->n_vlabels);
     GPS_CK(cudaMemcpyAsync(h.data(), dh.p, sizeof(unsigned long long) * g->n_vlabels, cudaMemcpyDeviceToHost,
                            c->stream));
+    uint2* deg = nullptr;
+    GPS_CK(cudaMalloc(&deg, sizeof(uint2) * (n + 1)));
+    g->mem[5] = deg;
+    if (n)
+        launch(c, GPS_K_LOAD, dim3(std::min<uint32_t>((n + 255) / 256, 4096)), dim3(256), 0, k_degrees,
+               (const uint32_t*)off_out, (const uint32_t*)off_in, n, deg);
     ctx_sync(c);
     g->lab_hist.assign(h.begin(), h.end());
     g->d.off_out = off_out;
@@ -219,6 +231,7 @@ void load_graph(gps_ctx* c, const gps_csr_desc* d, gps_graph* g) {
     g->d.off_in = off_in;
     g->d.arc_in = arc_in;
     g->d.vlab = vlab;
+    g->d.deg = deg;
 }
 
 void free_graph_mem(gps_graph* g) {

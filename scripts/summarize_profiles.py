@@ -15,7 +15,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LOAD = ("k_rs_", "k_make_keys", "k_build_rows", "k_dup_flags", "k_transpose_keys", "k_label_hist")
+LOAD = ("k_rs_", "k_degrees", "k_make_keys", "k_build_rows", "k_dup_flags", "k_transpose_keys", "k_label_hist")
 CLASS = [("k_explore<0>", "explore"), ("k_explore<1>", "propagate"), ("k_ec<0>", "ec_count"),
          ("k_ec<1>", "ec_write"), ("k_join<0>", "join_count"), ("k_join<1>", "join_write"),
          ("k_join_seg", "join_len"), ("k_collect", "collect"), ("k_check", "check"), ("k_bitand", "bitand"),
