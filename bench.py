@@ -177,8 +177,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--workers", type=int, default=4, help="library batch workers (0 = one query at a time)")
-    ap.add_argument("--slice", type=int, default=25, help="queries per worker hand-out (batch-synchronous unit)")
+    ap.add_argument("--workers", type=int, default=3, help="library batch workers (0 = one query at a time)")
+    ap.add_argument("--slice", type=int, default=34, help="queries per worker hand-out (batch-synchronous unit)")
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
     global CONFIG
@@ -256,10 +256,11 @@ def main():
         dominant = max(ms, key=ms.get)
         kd_iso = iso[dominant]
         total_iso = sum(ms.values())
-        if args.workers:
+        if args.workers:   # fresh worker contexts: warm them again (scratch growth, first launches)
             ctx.set_workers(args.workers)
             ctx.set_slice(args.slice)
-            step()
+            for _ in range(max(args.warmup, 3)):
+                step()
         ctx.set_profiling([dominant])
         ctx.reset_stats()
 
@@ -333,7 +334,8 @@ def main():
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dominant)
+        tj = json.load(open(tpath))   # ncu DRAM bytes per launch of the class (config 2; others prefixed)
+        traffic = tj.get(dominant) if CONFIG == 2 else tj.get(f"cfg{CONFIG}:{dominant}")
 
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,

@@ -28,45 +28,57 @@ namespace gps {
 
 // ---------------------------------------------------------------- a2 check
 // One warp per bitmap word (32 data vertices): the vertex data (label, out/in
-// degree) is read ONCE into registers and tested against every query vertex of
-// every query of the launch (one __ballot_sync per query vertex), so a batch of
-// queries streams vlab / off_out / off_in once instead of once per query.
-__global__ void __launch_bounds__(256) k_check(DevGraph g, const QDesc* __restrict__ qs, uint32_t nq) {
-    const uint32_t lane = lane_id();
+// degree) is read ONCE and tested against every query vertex of every query of
+// the launch, so a batch streams vlab / deg once instead of once per query.  The
+// warp parks its 32 vertices in shared memory; lane f then builds the whole word
+// of query vertex f (32 broadcast reads, no ballot per query vertex), so 32 query
+// vertices -- of any queries -- are tested in parallel.
+constexpr int kChkF = 512;   // query vertices staged in shared memory per pass
+
+__global__ void __launch_bounds__(256) k_check(DevGraph g, const ChkQV* __restrict__ qv, uint32_t nf) {
+    __shared__ ChkQV s_qv[kChkF];
+    __shared__ uint4 s_vd[8][32];   // per warp: (label or ~0 past n, out-degree, in-degree, id)
+    const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < g.nw; w += nwarps) {
-        const uint32_t v = w * 32 + lane;
-        const bool valid = v < g.n;
-        uint32_t lab = 0, od = 0, id = 0;
-        if (valid) {
-            lab = g.vlab[v];
-            const uint2 d = g.deg[v];
-            od = d.x;
-            id = d.y;
-        }
-        for (uint32_t qi = 0; qi < nq; qi++) {
-            const QDesc& q = qs[qi];
-            const int k = q.k;
-            uint32_t mine = 0;
-            for (int u = 0; u < k; u++) {
-                const int32_t ql = __ldg(&q.lab[u]);
-                const int64_t qb = __ldg(&q.bound[u]);
-                bool p = valid && (ql < 0 || lab == (uint32_t)ql) && (qb < 0 || (int64_t)v == qb) &&
-                         od >= __ldg(&q.qout[u]) && id >= __ldg(&q.qin[u]);
-                uint32_t m = __ballot_sync(kFull, p);
-                if ((int)lane == u) mine = m;
+    for (uint32_t f0 = 0; f0 < nf; f0 += kChkF) {
+        const uint32_t fn = min(nf - f0, (uint32_t)kChkF);
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < fn; i += blockDim.x) s_qv[i] = qv[f0 + i];
+        __syncthreads();
+        for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < g.nw; w += nwarps) {
+            const uint32_t v = w * 32 + lane;
+            uint4 d = make_uint4(0xffffffffu, 0u, 0u, v);
+            if (v < g.n) {
+                const uint2 dg = g.deg[v];
+                d = make_uint4(g.vlab[v], dg.x, dg.y, v);
             }
-            if ((int)lane < k) q.B[(size_t)lane * g.nws + w] = mine;
+            __syncwarp();
+            s_vd[wib][lane] = d;
+            __syncwarp();
+            for (uint32_t f = lane; f < fn; f += 32) {
+                const ChkQV q = s_qv[f];
+                const uint32_t ql = q.lab < 0 ? 0xfffffffeu : (uint32_t)q.lab;   // wildcard: any real label
+                uint32_t bits = 0;
+#pragma unroll 8
+                for (uint32_t t = 0; t < 32; t++) {
+                    const uint4 x = s_vd[wib][t];
+                    const bool p = x.x != 0xffffffffu && (ql == 0xfffffffeu || x.x == ql) &&
+                                   (q.bound < 0 || (int64_t)x.w == q.bound) && x.y >= q.qout && x.z >= q.qin;
+                    bits |= (p ? 1u : 0u) << t;
+                }
+                q.B[w] = bits;
+            }
         }
     }
 }
 
-void run_check(gps_ctx* c, const DevGraph& g, const QDesc* d_q, uint32_t nq, uint32_t max_k) {
-    if (nq == 0) return;
-    uint32_t blocks = std::min<uint32_t>((g.nw + 7) / 8, (uint32_t)c->nsm * 8);
-    launch(c, GPS_K_CHECK, dim3(blocks), dim3(256), 0, k_check, g, d_q, nq);
-    // algorithmic: the vertex data once + k/8 bytes of bitmap per vertex and query
-    c->stats.k_bytes[GPS_K_CHECK] += (double)g.n * 10.0 + (double)nq * max_k * g.nw * 4.0;   // 2 + 8 B per vertex
+void run_check(gps_ctx* c, const DevGraph& g, const ChkQV* d_qv, uint32_t nf) {
+    if (nf == 0) return;
+    const uint32_t blocks = std::min<uint32_t>((g.nw + 7) / 8, (uint32_t)c->nsm * 6);
+    launch(c, GPS_K_CHECK, dim3(blocks), dim3(256), 0, k_check, g, d_qv, nf);
+    // algorithmic: the vertex data once (2 B label + 8 B degrees) + one bitmap word per 32 vertices
+    // and query vertex
+    c->stats.k_bytes[GPS_K_CHECK] += (double)g.n * 10.0 + (double)nf * g.nw * 4.0;
 }
 
 // -------------------------------------------------------------- a3 collect

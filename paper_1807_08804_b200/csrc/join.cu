@@ -166,15 +166,6 @@ void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uin
 template <bool FAST> constexpr int seg_rows() { return FAST ? 1 : 4; }
 template <bool FAST> constexpr int seg_tile() { return 256 * seg_rows<FAST>(); }
 
-// largest j < nj with jobs[j].row0 <= r
-__device__ __forceinline__ uint32_t job_of_row(const JoinJob* __restrict__ jobs, uint32_t nj, uint64_t r) {
-    uint32_t lo = 0, hi = nj;
-    while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (jobs[mid].row0 <= r) lo = mid; else hi = mid;
-    }
-    return lo;
-}
 
 // Per input row: O(1) key lookup -> EC segment start (s0) and the exclusive scan of
 // the segment lengths (poff, the step's pair space), one look-back pass.  FAST
@@ -185,18 +176,23 @@ template <bool FAST>
 __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
                                                   uint32_t epoch) {
     constexpr int kSegRows = seg_rows<FAST>(), kSegTile = seg_tile<FAST>();
+    extern __shared__ __align__(16) char s_dyn[];
+    uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);   // [nj+1] first row of every job
     __shared__ uint64_t s_pre[3];
     const uint32_t tile = lb_ticket(lb.ctr, ntiles);
+    for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
+    if (threadIdx.x == 0) s_jr[a.nj] = a.R;
+    __syncthreads();
     const uint64_t r0 = (uint64_t)tile * kSegTile + (uint64_t)threadIdx.x * kSegRows;
     uint32_t len[kSegRows], ac[kSegRows], wc[kSegRows];
     uint64_t tsum = 0, asum = 0, wsum = 0;
-    uint32_t jb = r0 < a.R ? job_of_row(a.jobs, a.nj, r0) : 0;
+    uint32_t jb = r0 < a.R ? pairs_find_smem(s_jr, a.nj, r0) : 0;
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {
         const uint64_t r = r0 + i;
         len[i] = ac[i] = wc[i] = 0;
         if (r < a.R) {
-            while (jb + 1 < a.nj && a.jobs[jb + 1].row0 <= r) jb++;
+            while (jb + 1 < a.nj && s_jr[jb + 1] <= r) jb++;
             const JoinJob& J = a.jobs[jb];
             const uint32_t* row = J.M + (r - J.row0) * a.w;
             const uint32_t key = __ldg(row + J.x_col);
@@ -292,10 +288,12 @@ void run_join_seg(gps_ctx* c, const JoinStep& s) {
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join table too large");
     LbScratch lb = lb_scratch(c, 3, (uint32_t)nt);
     if (s.fast)
-        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg<true>, s, lb, (uint32_t)nt,
+        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), sizeof(uint64_t) * (s.nj + 1), k_join_seg<true>, s,
+               lb, (uint32_t)nt,
                lb_next_epoch(c));
     else
-        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), 0, k_join_seg<false>, s, lb, (uint32_t)nt,
+        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), sizeof(uint64_t) * (s.nj + 1), k_join_seg<false>, s,
+               lb, (uint32_t)nt,
                lb_next_epoch(c));
     c->stats.k_bytes[GPS_K_JOIN_LEN] += 4.0 * s.R * (s.w + 3);
 }

@@ -27,15 +27,14 @@ constexpr uint32_t kMaxJobsPerLaunch = 2048;   // job prefix staged in shared me
 constexpr uint32_t kJoinStageCols = 8;          // join rows of <= 8 columns are staged in shared memory
 
 // ---- a2 kernel_check (Def. 3; Alg. 2 line 7 P:723) -------------------
-struct QDesc {
-    int k;
-    int32_t lab[GPS_MAX_QV];     // vertex label or -1
-    int64_t bound[GPS_MAX_QV];   // bound data id or -1
-    uint32_t qout[GPS_MAX_QV];   // required out-degree
-    uint32_t qin[GPS_MAX_QV];    // required in-degree
-    uint32_t* B;                 // k bitmaps, row stride nws
+struct ChkQV {                   // one query vertex of a check launch (all queries flattened)
+    int32_t lab;                 // vertex label or -1
+    uint32_t qout, qin;          // required out- / in-degree
+    uint32_t pad;
+    int64_t bound;               // bound data id or -1
+    uint32_t* B;                 // its candidate bitmap (nws words)
 };
-void run_check(gps_ctx* c, const DevGraph& g, const QDesc* d_q, uint32_t nq, uint32_t max_k);
+void run_check(gps_ctx* c, const DevGraph& g, const ChkQV* d_qv, uint32_t nf);
 
 // ---- a3 kernel_collect ----------------------------------
 // Per job (query, vertex): c_array (sorted candidate ids), rank prefix rp

@@ -161,22 +161,18 @@ void carve_all(Chunk& ch, Carve& cv) {
 void filter_phase(Chunk& ch, int stage) {
     gps_ctx* c = ch.c;
     const DevGraph& d = ch.g->d;
-    std::vector<QDesc> qd;
-    uint32_t maxk = 0;
-    for (QS* q : ch.qs) {
-        QDesc x{};
-        x.k = q->k;
+    std::vector<ChkQV> qv;
+    for (QS* q : ch.qs)
         for (int u = 0; u < q->k; u++) {
-            x.lab[u] = q->plan.vlab[u];
-            x.bound[u] = q->plan.bound[u];
-            x.qout[u] = q->plan.qout[u];
-            x.qin[u] = q->plan.qin[u];
+            ChkQV x{};
+            x.lab = q->plan.vlab[u];
+            x.bound = q->plan.bound[u];
+            x.qout = q->plan.qout[u];
+            x.qin = q->plan.qin[u];
+            x.B = q->B + (size_t)u * d.nws;
+            qv.push_back(x);
         }
-        x.B = q->B;
-        qd.push_back(x);
-        maxk = std::max<uint32_t>(maxk, q->k);
-    }
-    run_check(c, d, upload(c, qd, ch.keep), (uint32_t)qd.size(), maxk);
+    run_check(c, d, upload(c, qv, ch.keep), (uint32_t)qv.size());
     if (stage < 1) return;
     size_t S = 0;
     for (QS* q : ch.qs) {

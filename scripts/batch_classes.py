@@ -45,7 +45,7 @@ def main():
                   f"GB/s {v['bytes'] / max(v['ms'], 1e-9) / 1e6:8.1f}")
     print(f"   sum of kernel time {tot:.3f} ms/step")
     ctx.set_profiling([])
-    for w, s in ((1, sl), (4, sl), (4, 10), (8, 13), (2, 50)):
+    for w, s in ((1, sl), (4, sl), (2, 50), (3, 34), (2, 25), (1, 100), (4, 13)):
         ctx.set_workers(w)
         ctx.set_slice(s)
         ctx.match_batch_raw(G, qb).free()

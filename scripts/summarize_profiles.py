@@ -16,10 +16,10 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LOAD = ("k_rs_", "k_degrees", "k_make_keys", "k_build_rows", "k_dup_flags", "k_transpose_keys", "k_label_hist")
-CLASS = [("k_explore<0>", "explore"), ("k_explore<1>", "propagate"), ("k_ec<0>", "ec_count"),
-         ("k_ec<1>", "ec_write"), ("k_join<0>", "join_count"), ("k_join<1>", "join_write"),
-         ("k_join_seg", "join_len"), ("k_collect", "collect"), ("k_check", "check"), ("k_bitand", "bitand"),
-         ("k_clear", "clear"), ("k_scan", "scan")]
+CLASS = [("k_explore", "explore"), ("k_ec", "ec_write"), ("k_join<0>", "join_count"), ("k_join<1>", "join_write"),
+         ("k_join<2>", "join_write"), ("k_join_v", "join_write"), ("k_join_fast", "join_write"),
+         ("k_join_seg", "join_len"), ("k_join_job_totals", "join_len"), ("k_collect", "collect"),
+         ("k_check", "check"), ("k_post", "bitand"), ("k_scan", "scan")]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
            "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -34,6 +34,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 
 
 def short(name):
     n = name.split("(")[0].replace("void ", "").replace("gps::", "")
+    n = n.replace("(unsigned int)", "").replace("u>", ">")
     n = n.replace("(bool)0", "0").replace("(bool)1", "1").replace("<false>", "<0>").replace("<true>", "<1>")
     return n
 
@@ -131,8 +132,9 @@ def main():
                       f"{g('smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio'):.2f} | "
                       f"{g('smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio'):.2f} |")
             per[klass(e["kernel"])].append(e.get("dram__bytes_read.sum", 0) + e.get("dram__bytes_write.sum", 0))
+        pre = os.environ.get("TRAFFIC_PREFIX", "")
         for c, v in per.items():
-            traffic[c] = sum(v) / len(v)
+            traffic[pre + c] = sum(v) / len(v)
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     open(os.path.join(prof, f"{rnd}_summary.md"), "w").write("\n".join(md) + "\n")
     print("\n".join(md[:40]))
