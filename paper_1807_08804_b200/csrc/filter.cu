@@ -29,44 +29,68 @@ namespace gps {
 // ---------------------------------------------------------------- a2 check
 // One warp per bitmap word (32 data vertices): the vertex data (label, out/in
 // degree) is read ONCE and tested against every query vertex of every query of
-// the launch, so a batch streams vlab / deg once instead of once per query.  The
-// warp parks its 32 vertices in shared memory; lane f then builds the whole word
-// of query vertex f (32 broadcast reads, no ballot per query vertex), so 32 query
-// vertices -- of any queries -- are tested in parallel.
-constexpr int kChkF = 512;   // query vertices staged in shared memory per pass
+// the launch (all queries flattened), so a batch streams vlab / deg once instead
+// of once per query.  A warp loads kChkW words' vertex data up front (kChkW
+// independent loads in flight per lane: the pass is HBM-bound on large graphs),
+// then for each query vertex f -- parameters packed in one shared-memory vector,
+// read as a broadcast -- tests its kChkW words with one __ballot_sync each; lane
+// f mod 32 keeps the word and stores it once 32 query vertices are done.
+constexpr int kChkF = 1024;   // query vertices staged in shared memory per pass
+constexpr int kChkW = 4;      // bitmap words per warp iteration
+constexpr uint32_t kChkAny = 0xffffffffu;   // wildcard label / free vertex
 
 __global__ void __launch_bounds__(256) k_check(DevGraph g, const ChkQV* __restrict__ qv, uint32_t nf) {
-    __shared__ ChkQV s_qv[kChkF];
-    __shared__ uint4 s_vd[8][32];   // per warp: (label or ~0 past n, out-degree, in-degree, id)
-    const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
+    __shared__ uint4 s_q[kChkF];        // (label or any, out-degree, in-degree, bound or free)
+    __shared__ uint32_t* s_b[kChkF];    // bitmap of query vertex f
+    const uint32_t lane = lane_id();
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     for (uint32_t f0 = 0; f0 < nf; f0 += kChkF) {
         const uint32_t fn = min(nf - f0, (uint32_t)kChkF);
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < fn; i += blockDim.x) s_qv[i] = qv[f0 + i];
+        for (uint32_t i = threadIdx.x; i < fn; i += blockDim.x) {
+            const ChkQV q = qv[f0 + i];
+            s_q[i] = make_uint4(q.lab < 0 ? kChkAny : (uint32_t)q.lab, q.qout, q.qin,
+                                q.bound < 0 ? kChkAny : (uint32_t)q.bound);
+            s_b[i] = q.B;
+        }
         __syncthreads();
-        for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < g.nw; w += nwarps) {
-            const uint32_t v = w * 32 + lane;
-            uint4 d = make_uint4(0xffffffffu, 0u, 0u, v);
-            if (v < g.n) {
-                const uint2 dg = g.deg[v];
-                d = make_uint4(g.vlab[v], dg.x, dg.y, v);
-            }
-            __syncwarp();
-            s_vd[wib][lane] = d;
-            __syncwarp();
-            for (uint32_t f = lane; f < fn; f += 32) {
-                const ChkQV q = s_qv[f];
-                const uint32_t ql = q.lab < 0 ? 0xfffffffeu : (uint32_t)q.lab;   // wildcard: any real label
-                uint32_t bits = 0;
-#pragma unroll 8
-                for (uint32_t t = 0; t < 32; t++) {
-                    const uint4 x = s_vd[wib][t];
-                    const bool p = x.x != 0xffffffffu && (ql == 0xfffffffeu || x.x == ql) &&
-                                   (q.bound < 0 || (int64_t)x.w == q.bound) && x.y >= q.qout && x.z >= q.qin;
-                    bits |= (p ? 1u : 0u) << t;
+        for (uint32_t w0 = gw * kChkW; w0 < g.nw; w0 += nwarps * kChkW) {
+            uint32_t lab[kChkW], od[kChkW], id[kChkW];
+            bool ok[kChkW];
+#pragma unroll
+            for (int i = 0; i < kChkW; i++) {
+                const uint32_t v = (w0 + i) * 32 + lane;
+                ok[i] = v < g.n;
+                uint2 dg = make_uint2(0u, 0u);
+                lab[i] = 0;
+                if (ok[i]) {
+                    dg = g.deg[v];
+                    lab[i] = g.vlab[v];
                 }
-                q.B[w] = bits;
+                od[i] = dg.x;
+                id[i] = dg.y;
+            }
+            for (uint32_t fb = 0; fb < fn; fb += 32) {
+                uint32_t mine[kChkW] = {};
+                const uint32_t fe = min(fn - fb, 32u);
+                for (uint32_t x = 0; x < fe; x++) {
+                    const uint4 q = s_q[fb + x];
+#pragma unroll
+                    for (int i = 0; i < kChkW; i++) {
+                        const uint32_t v = (w0 + i) * 32 + lane;
+                        const bool p = ok[i] && (q.x == kChkAny || lab[i] == q.x) && (q.w == kChkAny || v == q.w) &&
+                                       od[i] >= q.y && id[i] >= q.z;
+                        const uint32_t m = __ballot_sync(kFull, p);
+                        if (lane == x) mine[i] = m;
+                    }
+                }
+                if (lane < fe) {
+                    uint32_t* B = s_b[fb + lane];
+#pragma unroll
+                    for (int i = 0; i < kChkW; i++)
+                        if (w0 + i < g.nw) B[w0 + i] = mine[i];
+                }
             }
         }
     }
@@ -74,7 +98,7 @@ __global__ void __launch_bounds__(256) k_check(DevGraph g, const ChkQV* __restri
 
 void run_check(gps_ctx* c, const DevGraph& g, const ChkQV* d_qv, uint32_t nf) {
     if (nf == 0) return;
-    const uint32_t blocks = std::min<uint32_t>((g.nw + 7) / 8, (uint32_t)c->nsm * 6);
+    const uint32_t blocks = std::min<uint32_t>((g.nw + 8 * kChkW - 1) / (8 * kChkW), (uint32_t)c->nsm * 4);
     launch(c, GPS_K_CHECK, dim3(blocks), dim3(256), 0, k_check, g, d_qv, nf);
     // algorithmic: the vertex data once (2 B label + 8 B degrees) + one bitmap word per 32 vertices
     // and query vertex

@@ -19,4 +19,18 @@ for _ in range(2):
             n = int(br.rows().sum())
             br.free()
         torch.cuda.synchronize()
+if os.environ.get("CLASSES"):   # per-class breakdown of one more pass (event-timed, single stream)
+    ctx.set_profiling(gpsense.KERNEL_CLASSES)
+    ctx.reset_stats()
+    for name, q, mode in CFG4:
+        if mode == "count":
+            ctx.count(G, q)
+        else:
+            ctx.match_batch_raw(G, [q]).free()
+    torch.cuda.synchronize()
+    st = ctx.stats()
+    for k, v in sorted(st["kernels"].items(), key=lambda kv: -kv[1]["ms"]):
+        if v["launches"]:
+            print(f"   {k:12s} launches {v['launches']:5d}  ms {v['ms']:.4f}  MB {v['bytes'] / 1e6:9.2f}  "
+                  f"GB/s {v['bytes'] / max(v['ms'], 1e-9) / 1e6:8.1f}")
 print("ok")
