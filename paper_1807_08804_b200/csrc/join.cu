@@ -161,9 +161,8 @@ void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uin
 }
 
 // ------------------------------------------------------------ a8 join step
-// rows per thread: the plain pass is a short load chain per row, so 4 rows amortise the
-// scan; the FAST pass runs w binary searches per row, one dependent chain per thread.
-template <bool FAST> constexpr int seg_rows() { return FAST ? 1 : 4; }
+// rows per thread (4 rows amortise the scan; the FAST pass interleaves their searches)
+template <bool FAST> constexpr int seg_rows() { return 4; }
 template <bool FAST> constexpr int seg_tile() { return 256 * seg_rows<FAST>(); }
 
 
@@ -187,55 +186,87 @@ __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinSt
     uint32_t len[kSegRows], ac[kSegRows], wc[kSegRows];
     uint64_t tsum = 0, asum = 0, wsum = 0;
     uint32_t jb = r0 < a.R ? pairs_find_smem(s_jr, a.nj, r0) : 0;
+    const uint32_t* rowp[kSegRows];
+    uint32_t sst[kSegRows], nowr[kSegRows];
 #pragma unroll
-    for (int i = 0; i < kSegRows; i++) {
+    for (int i = 0; i < kSegRows; i++) {   // key -> rank -> segment: the rows' loads are independent
         const uint64_t r = r0 + i;
         len[i] = ac[i] = wc[i] = 0;
+        rowp[i] = nullptr;
+        sst[i] = nowr[i] = 0;
         if (r < a.R) {
             while (jb + 1 < a.nj && s_jr[jb + 1] <= r) jb++;
             const JoinJob& J = a.jobs[jb];
-            const uint32_t* row = J.M + (r - J.row0) * a.w;
-            const uint32_t key = __ldg(row + J.x_col);
+            rowp[i] = J.M + (r - J.row0) * a.w;
+            const uint32_t key = __ldg(rowp[i] + J.x_col);
             const uint32_t rk = bit_rank(J.Bx, J.rpx, key);
-            const uint32_t s = __ldg(J.ec_off + rk);
-            len[i] = __ldg(J.ec_off + rk + 1) - s;
-            a.s0[r] = s;
-            if (FAST) {
-                uint32_t mask = 0;
-                for (uint32_t c0 = 0; c0 < a.w; c0 += 8) {   // up to 8 searches in lockstep
-                    uint32_t t[8], lo[8], hi[8];
+            sst[i] = __ldg(J.ec_off + rk);
+            len[i] = __ldg(J.ec_off + rk + 1) - sst[i];
+            nowr[i] = J.nowrite;
+            a.s0[r] = sst[i];
+        }
+    }
+    if (FAST) {
+        // every (row, column) pair of the thread's rows is a binary search of the column's value
+        // in the row's segment; all of them run in lockstep, 8 at a time, so a thread keeps up to
+        // 8 independent loads in flight whatever the row width
+        uint32_t mask[kSegRows] = {};
+        const uint32_t nsearch = kSegRows * a.w;
+        for (uint32_t q0 = 0; q0 < nsearch; q0 += 8) {
+            uint32_t t[8], lo[8], hi[8], found = 0;
 #pragma unroll
-                    for (int x = 0; x < 8; x++) {
-                        const bool on = c0 + x < a.w;
-                        t[x] = on ? __ldg(row + c0 + x) : 0u;
-                        lo[x] = s;
-                        hi[x] = on ? s + len[i] : s;
-                    }
-                    bool more = true;
-                    while (more) {
-                        more = false;
+            for (int x = 0; x < 8; x++) {
+                const uint32_t q = q0 + x, qi = q / a.w, qc = q - qi * a.w;
+                const uint32_t* rp = nullptr;
+                uint32_t ss = 0, ll = 0;
 #pragma unroll
-                        for (int x = 0; x < 8; x++) {
-                            if (lo[x] >= hi[x]) continue;
-                            const uint32_t mid = (lo[x] + hi[x]) >> 1;
-                            const uint32_t v = __ldg(a.ec_val + mid);
-                            if (v == t[x]) {
-                                mask |= 1u << (c0 + x);
-                                hi[x] = lo[x];
-                            } else if (v < t[x]) {
-                                lo[x] = mid + 1;
-                            } else {
-                                hi[x] = mid;
-                            }
-                            more |= lo[x] < hi[x];
-                        }
+                for (int i = 0; i < kSegRows; i++)   // select, not index: the arrays stay in registers
+                    if (qi == (uint32_t)i) {
+                        rp = rowp[i];
+                        ss = sst[i];
+                        ll = len[i];
                     }
+                const bool on = q < nsearch && rp != nullptr && ll > 0;
+                t[x] = on ? __ldg(rp + qc) : 0u;
+                lo[x] = ss;
+                hi[x] = on ? ss + ll : ss;
+            }
+            bool more = true;
+            while (more) {
+                more = false;
+#pragma unroll
+                for (int x = 0; x < 8; x++) {
+                    if (lo[x] >= hi[x]) continue;
+                    const uint32_t mid = (lo[x] + hi[x]) >> 1;
+                    const uint32_t v = __ldg(a.ec_val + mid);
+                    if (v == t[x]) {
+                        found |= 1u << x;
+                        hi[x] = lo[x];
+                    } else if (v < t[x]) {
+                        lo[x] = mid + 1;
+                    } else {
+                        hi[x] = mid;
+                    }
+                    more |= lo[x] < hi[x];
                 }
-                a.imask[r] = mask;
-                ac[i] = len[i] - __popc(mask);
-                wc[i] = J.nowrite ? 0u : ac[i];
+            }
+            while (found) {   // search q0 + x found its value: bit (q mod w) of row q / w
+                const uint32_t x = __ffs(found) - 1, q = q0 + x, qi = q / a.w;
+                found &= found - 1;
+#pragma unroll
+                for (int i = 0; i < kSegRows; i++) mask[i] |= qi == (uint32_t)i ? 1u << (q - qi * a.w) : 0u;
             }
         }
+#pragma unroll
+        for (int i = 0; i < kSegRows; i++) {
+            if (rowp[i] == nullptr) continue;
+            a.imask[r0 + i] = mask[i];
+            ac[i] = len[i] - __popc(mask[i]);
+            wc[i] = nowr[i] ? 0u : ac[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kSegRows; i++) {
         tsum += len[i];
         asum += ac[i];
         wsum += wc[i];
