@@ -168,9 +168,9 @@ template <bool FAST> constexpr int seg_tile() { return 256 * seg_rows<FAST>(); }
 
 // Per input row: O(1) key lookup -> EC segment start (s0) and the exclusive scan of
 // the segment lengths (poff, the step's pair space), one look-back pass.  FAST
-// (closing-free steps): also the row values found in the segment (imask, w
-// independent binary searches advanced in lockstep) and the scans of the row's
-// valid (aoff) and written (woff) outputs -- three look-backs in three warps.
+// (closing-free steps): also the row values found in the segment (imask, binary
+// searches advanced in lockstep), the per-job output totals, and the scan of the
+// rows' written outputs (woff) -- two look-backs in two warps.
 template <bool FAST>
 __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
                                                   uint32_t epoch) {
@@ -184,16 +184,17 @@ __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinSt
     __syncthreads();
     const uint64_t r0 = (uint64_t)tile * kSegTile + (uint64_t)threadIdx.x * kSegRows;
     uint32_t len[kSegRows], ac[kSegRows], wc[kSegRows];
-    uint64_t tsum = 0, asum = 0, wsum = 0;
+    uint64_t tsum = 0, wsum = 0;
     uint32_t jb = r0 < a.R ? pairs_find_smem(s_jr, a.nj, r0) : 0;
     const uint32_t* rowp[kSegRows];
-    uint32_t sst[kSegRows], nowr[kSegRows];
+    uint32_t sst[kSegRows], nowr[kSegRows], jrow[kSegRows];
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {   // key -> rank -> segment: the rows' loads are independent
         const uint64_t r = r0 + i;
         len[i] = ac[i] = wc[i] = 0;
         rowp[i] = nullptr;
         sst[i] = nowr[i] = 0;
+        jrow[i] = jb;
         if (r < a.R) {
             while (jb + 1 < a.nj && s_jr[jb + 1] <= r) jb++;
             const JoinJob& J = a.jobs[jb];
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinSt
             sst[i] = __ldg(J.ec_off + rk);
             len[i] = __ldg(J.ec_off + rk + 1) - sst[i];
             nowr[i] = J.nowrite;
+            jrow[i] = jb;
             a.s0[r] = sst[i];
         }
     }
@@ -257,59 +259,59 @@ __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinSt
                 for (int i = 0; i < kSegRows; i++) mask[i] |= qi == (uint32_t)i ? 1u << (q - qi * a.w) : 0u;
             }
         }
+        bool live[kSegRows];
 #pragma unroll
         for (int i = 0; i < kSegRows; i++) {
-            if (rowp[i] == nullptr) continue;
+            live[i] = rowp[i] != nullptr;
+            if (!live[i]) continue;
             a.imask[r0 + i] = mask[i];
             ac[i] = len[i] - __popc(mask[i]);
             wc[i] = nowr[i] ? 0u : ac[i];
         }
+        // per-job output totals (the host sizes the output with them): run-length per thread,
+        // combined across the warp, one atomic per job run
+        run_sum<kSegRows>(live, jrow, ac, [&](uint32_t job, uint32_t n) {
+            atomicAdd(a.jobs[job].total, (unsigned long long)n);
+        });
     }
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {
         tsum += len[i];
-        asum += ac[i];
         wsum += wc[i];
     }
-    uint64_t tot, atot = 0, wtot = 0;
-    const uint64_t pre = block_excl_scan(tsum, &tot);
-    uint64_t apre = 0, wpre = 0;
+    // poff and (FAST) woff: the two scans in one pass of barriers, two look-backs in two warps
+    uint64_t tot, wtot = 0, pre, wpre = 0;
     if (FAST) {
-        apre = block_excl_scan(asum, &atot);
-        wpre = block_excl_scan(wsum, &wtot);
+        ulonglong2 t2;
+        const ulonglong2 p2 = block_excl_scan2(make_ulonglong2(tsum, wsum), &t2);
+        pre = p2.x;
+        wpre = p2.y;
+        tot = t2.x;
+        wtot = t2.y;
+    } else {
+        pre = block_excl_scan(tsum, &tot);
     }
     const uint32_t wid = threadIdx.x >> 5;
-    if (wid < (FAST ? 3u : 1u)) {
-        const uint64_t agg = wid == 0 ? tot : (wid == 1 ? atot : wtot);
+    if (wid < (FAST ? 2u : 1u)) {
+        const uint64_t agg = wid == 0 ? tot : wtot;
         const uint64_t p = lb_warp_lookback(lb.status + (size_t)wid * lb.max_tiles, tile, agg, epoch);
         if ((threadIdx.x & 31u) == 0) s_pre[wid] = p;
     }
     __syncthreads();
-    uint64_t run = s_pre[0] + pre, arun = 0, wrun = 0;
-    if (FAST) {
-        arun = s_pre[1] + apre;
-        wrun = s_pre[2] + wpre;
-    }
+    uint64_t run = s_pre[0] + pre, wrun = FAST ? s_pre[1] + wpre : 0;
 #pragma unroll
     for (int i = 0; i < kSegRows; i++) {
         const uint64_t r = r0 + i;
         if (r < a.R) {
             a.poff[r] = run;
-            if (FAST) {
-                a.aoff[r] = arun;
-                a.woff[r] = wrun;
-            }
+            if (FAST) a.woff[r] = wrun;
         }
         run += len[i];
-        arun += ac[i];
         wrun += wc[i];
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
         a.poff[a.R] = s_pre[0] + tot;
-        if (FAST) {
-            a.aoff[a.R] = s_pre[1] + atot;
-            a.woff[a.R] = s_pre[2] + wtot;
-        }
+        if (FAST) a.woff[a.R] = s_pre[1] + wtot;
     }
 }
 
@@ -317,7 +319,7 @@ void run_join_seg(gps_ctx* c, const JoinStep& s) {
     const uint64_t tile = s.fast ? seg_tile<true>() : seg_tile<false>();
     const uint64_t nt = (s.R + tile - 1) / tile;
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join table too large");
-    LbScratch lb = lb_scratch(c, 3, (uint32_t)nt);
+    LbScratch lb = lb_scratch(c, 2, (uint32_t)nt);
     if (s.fast)
         launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), sizeof(uint64_t) * (s.nj + 1), k_join_seg<true>, s,
                lb, (uint32_t)nt,
@@ -329,16 +331,6 @@ void run_join_seg(gps_ctx* c, const JoinStep& s) {
     c->stats.k_bytes[GPS_K_JOIN_LEN] += 4.0 * s.R * (s.w + 3);
 }
 
-__global__ void k_join_job_totals(const __grid_constant__ JoinStep a) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= a.nj) return;
-    const uint64_t lo = a.jobs[j].row0, hi = j + 1 < a.nj ? a.jobs[j + 1].row0 : a.R;
-    *a.jobs[j].total = a.aoff[hi] - a.aoff[lo];
-}
-
-void run_join_job_totals(gps_ctx* c, const JoinStep& s) {
-    launch(c, GPS_K_JOIN_LEN, dim3((s.nj + 127) / 128), dim3(128), 0, k_join_job_totals, s);
-}
 
 __device__ __forceinline__ bool seg_contains(const uint32_t* __restrict__ val, uint32_t lo, uint32_t hi, uint32_t t) {
     while (lo < hi) {
@@ -648,8 +640,10 @@ struct __align__(16) JFMeta {
     uint32_t hole;          // output column of the new value; kStageW: count-only job (no output)
 };
 constexpr int kJFW = 512;   // window rows of the fast write (fan-out < 2 cuts chunks short)
-using JFSmem = PairSmem<JFMeta, kPT, kPI, kJFW, 1>;
-__host__ __device__ constexpr size_t jf_stage(uint32_t) { return sizeof(uint2) * kTile; }
+constexpr int kFI = 4;      // pairs per thread per chunk of the fast write (8 measured slower: fewer chunks in flight)
+constexpr uint32_t kFTile = kPT * kFI;
+using JFSmem = PairSmem<JFMeta, kPT, kFI, kJFW, 1>;
+__host__ __device__ constexpr size_t jf_stage(uint32_t) { return sizeof(uint2) * kFTile; }
 
 template <uint32_t WOUT>
 __device__ __forceinline__ void jf_tmpl(const JFMeta& m, uint32_t (&t)[WOUT]) {
@@ -705,19 +699,19 @@ __global__ void __launch_bounds__(kPT, 4) k_join_fast(const __grid_constant__ Jo
     const uint64_t P = offs(a.R);
     uint64_t p0, p1;
     pairs_range(P, blockIdx.x, gridDim.x, p0, p1);
-    pair_chunks<JFMeta, kPT, kPI, kJFW, 1>(p0, p1, a.R, offs, load, s_bufs,
-                                           [&](const bool (&v)[kPI], const uint32_t (&wi)[kPI],
-                                               const uint32_t (&j)[kPI], const JFMeta* sm, uint64_t) {
-        uint32_t cand[kPI];
-        bool ok[kPI];
+    pair_chunks<JFMeta, kPT, kFI, kJFW, 1>(p0, p1, a.R, offs, load, s_bufs,
+                                           [&](const bool (&v)[kFI], const uint32_t (&wi)[kFI],
+                                               const uint32_t (&j)[kFI], const JFMeta* sm, uint64_t) {
+        uint32_t cand[kFI];
+        bool ok[kFI];
         uint32_t mine = 0;
 #pragma unroll
-        for (int it = 0; it < kPI; it++) {
+        for (int it = 0; it < kFI; it++) {
             const bool live = v[it] && sm[wi[it]].hole < kStageW;
             cand[it] = live ? __ldg(a.ec_val + sm[wi[it]].s0 + j[it]) : 0u;
         }
 #pragma unroll
-        for (int it = 0; it < kPI; it++) {
+        for (int it = 0; it < kFI; it++) {
             const JFMeta& m = sm[wi[it]];
             uint32_t t[WOUT];
             jf_tmpl<WOUT>(m, t);
@@ -733,7 +727,7 @@ __global__ void __launch_bounds__(kPT, 4) k_join_fast(const __grid_constant__ Jo
         if (mine && lpos == 0) {   // the chunk's first output: its global row fixes the chunk's base
             uint32_t fc = 0, fw = 0, fj = 0;   // selected, not indexed (keeps the arrays in registers)
 #pragma unroll
-            for (int it = kPI - 1; it >= 0; it--)
+            for (int it = kFI - 1; it >= 0; it--)
                 if (ok[it]) {
                     fc = cand[it];
                     fw = wi[it];
@@ -746,7 +740,7 @@ __global__ void __launch_bounds__(kPT, 4) k_join_fast(const __grid_constant__ Jo
             s_base = m.woff + fj - before;
         }
 #pragma unroll
-        for (int it = 0; it < kPI; it++) {
+        for (int it = 0; it < kFI; it++) {
             if (!ok[it]) continue;
             s_ri[lpos++] = make_uint2(cand[it], wi[it]);
         }
@@ -798,7 +792,7 @@ static void launch_join_fast(gps_ctx* c, const JoinStep& s, uint64_t P) {
         if (occ < 1) occ = 1;
     });
     // one resident wave; no more blocks than chunks (a block's fixed cost is a global search)
-    const uint64_t chunks = (P + kTile - 1) / kTile;
+    const uint64_t chunks = (P + kFTile - 1) / kFTile;
     const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->nsm * occ, chunks));
     launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), JFSmem::bytes(s.nj, jf_stage(WOUT)), k_join_fast<WOUT>, s);
 }

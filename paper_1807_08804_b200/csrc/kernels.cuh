@@ -155,12 +155,11 @@ struct JoinStep {
     uint64_t plo = 0, phi = ~0ull;   // pair sub-range to process (row-sharded join); phi == ~0: all pairs
     // closing-free steps (every job): validity is injectivity only, so a row's outputs are its
     // segment minus the row's own values.  imask[r] = which of row r's values occur in its
-    // segment (binary searches in the seg pass); aoff / woff = exclusive scans of all / written
+    // segment (binary searches in the seg pass); woff = exclusive scan of written
     // outputs per row (R+1).  The count pass disappears and the write pass places each pair
     // at woff[r] + j - #(row values in the segment before it).
     int fast = 0;
     uint32_t* imask = nullptr;
-    uint64_t* aoff = nullptr;
     uint64_t* woff = nullptr;
 };
 // Row-sharded join: for each target pair range [lo[t], hi[t]) of the local pair
@@ -168,9 +167,7 @@ struct JoinStep {
 // (rows[3t .. 3t+2]).
 void run_rows_for_ranges(gps_ctx* c, const uint64_t* poff, uint64_t R, const uint64_t* d_lohi, uint32_t n,
                          uint64_t* d_rows);
-void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (+ imask / aoff / woff if fast)
-// fast steps: per-job totals total[j] = aoff[row0(j+1)] - aoff[row0(j)]
-void run_join_job_totals(gps_ctx* c, const JoinStep& s);
+void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (+ imask / aoff / woff / jobs[].total if fast)
 // fast steps: write pass over all P pairs (rows of count-only jobs are skipped)
 void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint64_t P);
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G);

@@ -47,6 +47,30 @@ __device__ __forceinline__ T block_excl_scan(T v, T* total) {
     return pre + x - v;
 }
 
+// Two u64 exclusive scans sharing one set of barriers.
+__device__ __forceinline__ ulonglong2 block_excl_scan2(ulonglong2 v, ulonglong2* total) {
+    __shared__ unsigned long long s_w[2][32];
+    const uint32_t lane = lane_id(), wid = warp_id(), nwarps = blockDim.x >> 5;
+    unsigned long long x = warp_incl_scan(v.x), y = warp_incl_scan(v.y);
+    if (lane == 31) {
+        s_w[0][wid] = x;
+        s_w[1][wid] = y;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        unsigned long long a = lane < nwarps ? s_w[0][lane] : 0ull, b = lane < nwarps ? s_w[1][lane] : 0ull;
+        a = warp_incl_scan(a);
+        b = warp_incl_scan(b);
+        s_w[0][lane] = a;
+        s_w[1][lane] = b;
+    }
+    __syncthreads();
+    const unsigned long long pa = wid ? s_w[0][wid - 1] : 0ull, pb = wid ? s_w[1][wid - 1] : 0ull;
+    *total = make_ulonglong2(s_w[0][nwarps - 1], s_w[1][nwarps - 1]);
+    __syncthreads();
+    return make_ulonglong2(pa + x - v.x, pb + y - v.y);
+}
+
 template <typename T>
 __device__ __forceinline__ T block_sum(T v) {
     T tot;

@@ -752,21 +752,18 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         // closing-free step with narrow rows: the seg pass finds each row's own values in its
         // segment, which fixes every output position -- no count pass, one sync
         const bool fast = cl.empty() && w + 1 <= kJoinStageCols && std::getenv("GPS_NO_FAST_JOIN") == nullptr;
-        DevPtr imask, aoff, woff;
+        DevPtr imask, woff;
         if (fast) {
             imask = DevPtr(c, sizeof(uint32_t) * (R + 1));
-            aoff = DevPtr(c, sizeof(uint64_t) * (R + 1));
             woff = DevPtr(c, sizeof(uint64_t) * (R + 1));
             js.fast = 1;
             js.imask = imask.as<uint32_t>();
-            js.aoff = aoff.as<uint64_t>();
             js.woff = woff.as<uint64_t>();
         }
         run_join_seg(c, js);
         Block ob;
         bool single = false;
         if (fast) {
-            run_join_job_totals(c, js);
             GPS_CK(cudaMemcpyAsync(c->d_info, js.poff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
             GPS_CK(cudaMemcpyAsync(c->d_info + 1, js.woff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
         } else {
