@@ -127,6 +127,19 @@ __global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const Colle
     } else {
         word[0] = word[1] = word[2] = word[3] = 0u;
     }
+    if (J.x1 > J.x0 && w0 < g.nw) {   // folded post: B &= AND of the X bitmaps, X cleared
+        for (uint32_t x = J.x0; x < J.x1; x++) {
+            uint4* xp = reinterpret_cast<uint4*>(J.xs[x] + w0);
+            const uint4 v = *xp;
+            word[0] &= v.x;
+            word[1] &= v.y;
+            word[2] &= v.z;
+            word[3] &= v.w;
+            *xp = make_uint4(0u, 0u, 0u, 0u);
+        }
+        *reinterpret_cast<uint4*>(J.B + w0) = make_uint4(word[0], word[1], word[2], word[3]);
+    }
+    if (J.post_only) return;   // uniform per block (one job per grid row)
     // the candidates' degrees, kColBatch independent 8-byte loads per round trip
     uint32_t c = 0, so = 0, si = 0;
 #pragma unroll

@@ -42,14 +42,22 @@ void run_check(gps_ctx* c, const DevGraph& g, const ChkQV* d_qv, uint32_t nf);
 // exclusive prefix sums of the candidates' out-/in-degrees (seg_out/seg_in,
 // C+1 entries) that index the pair spaces of explore and EC.  One single-pass
 // launch (decoupled look-back).
+// A job may carry the end-of-step bitmap update of its vertex (a folded "post":
+// B &= AND of the X scratch bitmaps xs[x0..x1), which are cleared), applied word
+// by word before the compaction -- the update needs no grid-wide barrier of its
+// own, so it rides on the collect launch that follows it anyway.  post_only jobs
+// apply the update and compact nothing.
 struct CollectJob {
-    const uint32_t* B;
+    uint32_t* B;
     uint32_t* rp;
     uint32_t* carr;
     uint32_t* cnt;
     uint32_t* seg_out;
     uint32_t* seg_in;
     uint32_t* segtot;       // optional [2]: seg_out[C], seg_in[C] (pair-space sizes for the host)
+    uint32_t* const* xs = nullptr;
+    uint32_t x0 = 0, x1 = 0;
+    uint32_t post_only = 0;
 };
 void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32_t nj);
 

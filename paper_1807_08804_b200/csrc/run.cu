@@ -157,8 +157,12 @@ void carve_all(Chunk& ch, Carve& cv) {
     }
 }
 
-// kernel_check + initialisation + refinement (stage 0 / 1 / 2).
-void filter_phase(Chunk& ch, int stage) {
+// kernel_check + initialisation + refinement (stage 0 / 1 / 2).  The end-of-step
+// bitmap updates ("posts", B &= AND of a step's X scratch bitmaps) ride on the
+// next collect launch of the same vertex (CollectJob.xs); the last step's updates
+// are returned in *pending (the caller folds them into its final collect) or, if
+// pending is null, applied by a post-only collect launch.
+void filter_phase(Chunk& ch, int stage, std::vector<CollectJob>* pending = nullptr) {
     gps_ctx* c = ch.c;
     const DevGraph& d = ch.g->d;
     std::vector<ChkQV> qv;
@@ -203,17 +207,56 @@ void filter_phase(Chunk& ch, int stage) {
         return e;
     };
     struct Staged {
-        uint32_t* const* xs = nullptr;
         const CollectJob *cj = nullptr, *cp = nullptr;
         const ExploreJob *ej = nullptr, *pj = nullptr;
-        const PostJob *post1 = nullptr, *post2 = nullptr;
-        uint32_t ncj = 0, ncp = 0, nej = 0, npj = 0, np1 = 0, np2 = 0;
+        const PostJob* post1 = nullptr;
+        uint32_t* const* xs = nullptr;
+        uint32_t ncj = 0, ncp = 0, nej = 0, npj = 0, np1 = 0;
+    };
+    // a post waiting for the next collect launch: B of query qi's vertex v &= AND xs[x0..x1)
+    struct Pend {
+        size_t qi;
+        int v;
+        CollectJob job;   // post_only form (B, xs, x0, x1)
+    };
+    auto post_only = [](uint32_t* B, uint32_t* const* xs, uint32_t x0, uint32_t x1) {
+        CollectJob j{B, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        j.xs = xs;
+        j.x0 = x0;
+        j.x1 = x1;
+        j.post_only = 1;
+        return j;
+    };
+    // fold the pending posts of matching (query, vertex) into jobs; the rest become post-only jobs
+    auto fold = [](std::vector<Pend>& pend, std::vector<CollectJob>& jobs, const std::vector<size_t>& job_q,
+                   const std::vector<int>& job_u) {
+        for (const Pend& p : pend) {
+            bool done = false;
+            for (size_t i = 0; i < jobs.size() && !done; i++)
+                if (!jobs[i].post_only && job_q[i] == p.qi && job_u[i] == p.v && jobs[i].x1 == jobs[i].x0) {
+                    jobs[i].xs = p.job.xs;
+                    jobs[i].x0 = p.job.x0;
+                    jobs[i].x1 = p.job.x1;
+                    done = true;
+                }
+            if (!done) jobs.push_back(p.job);
+        }
+        pend.clear();
     };
     std::vector<Staged> staged;
+    std::vector<Pend> pend;   // posts of the previous step
     for (size_t s = 0; s < S; s++) {
         std::vector<CollectJob> cj;
+        std::vector<size_t> cj_q;
+        std::vector<int> cj_u;
         std::vector<ExploreJob> ej, pj;
-        std::vector<PostJob> post1, post2;
+        struct P {
+            size_t qi;
+            int v;
+            uint32_t* B;
+            uint32_t x0, x1;
+        };
+        std::vector<P> post1, post2;
         std::vector<uint32_t*> xs;
         for (size_t qi = 0; qi < ch.qs.size(); qi++) {
             QS* q = ch.qs[qi];
@@ -228,6 +271,8 @@ void filter_phase(Chunk& ch, int stage) {
             have[qi] |= 1u << u;
             cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0], q->seg[u][1],
                                     nullptr});
+            cj_q.push_back(qi);
+            cj_u.push_back(u);
             // prune (Alg. 2 lines 14-18): A = u, S = v; X_i = members of C(u) meeting constraint i
             const uint32_t x0 = (uint32_t)xs.size();
             for (uint32_t i = 0; i < nc; i++) {
@@ -236,7 +281,7 @@ void filter_phase(Chunk& ch, int stage) {
                 ej.back().freshA = 1;   // u was collected by this step
                 xs.push_back(ch.Xp(*q, (int)i));
             }
-            post1.push_back(PostJob{ch.Bp(*q, u), x0, (uint32_t)xs.size()});
+            post1.push_back(P{qi, u, ch.Bp(*q, u), x0, (uint32_t)xs.size()});
             if (!st.propagate) continue;
             // propagation (lines 19-22, reading R15): A = v, S = u (arcs seen from v: direction flipped)
             std::vector<int> targets;
@@ -251,7 +296,7 @@ void filter_phase(Chunk& ch, int stage) {
                     pj.back().freshS = 1;   // u is re-collected after its prune
                     xs.push_back(ch.Xp(*q, (int)i));
                 }
-                post2.push_back(PostJob{ch.Bp(*q, v), y0, (uint32_t)xs.size()});
+                post2.push_back(P{qi, v, ch.Bp(*q, v), y0, (uint32_t)xs.size()});
             }
         }
         if (cj.empty()) continue;
@@ -259,36 +304,68 @@ void filter_phase(Chunk& ch, int stage) {
         // (one host->device copy covers the whole filter phase)
         Staged x;
         x.xs = upload(c, xs, ch.keep);
+        fold(pend, cj, cj_q, cj_u);   // the previous step's posts ride on this step's collect
         x.cj = upload(c, cj, ch.keep);
         x.ncj = (uint32_t)cj.size();
         x.ej = upload(c, ej, ch.keep);
         x.nej = (uint32_t)ej.size();
-        x.post1 = upload(c, post1, ch.keep);
-        x.np1 = (uint32_t)post1.size();
         if (!pj.empty()) {
-            // re-collect the pruned vertices: propagation walks only the survivors
+            // re-collect the pruned vertices (propagation walks only the survivors); their prune
+            // posts ride on this re-collect, the other queries' prune posts go with it post-only
             std::vector<CollectJob> cp;
-            for (const CollectJob& y : cj)
-                if (std::any_of(pj.begin(), pj.end(), [&](const ExploreJob& e) { return e.candS == y.carr; }))
-                    cp.push_back(y);
-            x.cp = cp.empty() ? nullptr : upload(c, cp, ch.keep);
+            std::vector<size_t> cp_q;
+            std::vector<int> cp_u;
+            for (size_t i = 0; i < x.ncj; i++) {
+                const CollectJob& y = cj[i];
+                if (y.post_only) continue;
+                if (std::any_of(pj.begin(), pj.end(), [&](const ExploreJob& e) { return e.candS == y.carr; })) {
+                    CollectJob z = y;
+                    z.xs = nullptr;
+                    z.x0 = z.x1 = 0;
+                    cp.push_back(z);
+                    cp_q.push_back(cj_q[i]);
+                    cp_u.push_back(cj_u[i]);
+                }
+            }
+            std::vector<Pend> p1;
+            for (const P& e : post1) p1.push_back(Pend{e.qi, e.v, post_only(e.B, x.xs, e.x0, e.x1)});
+            fold(p1, cp, cp_q, cp_u);
+            x.cp = upload(c, cp, ch.keep);
             x.ncp = (uint32_t)cp.size();
             x.pj = upload(c, pj, ch.keep);
             x.npj = (uint32_t)pj.size();
-            x.post2 = upload(c, post2, ch.keep);
-            x.np2 = (uint32_t)post2.size();
+            for (const P& e : post2) pend.push_back(Pend{e.qi, e.v, post_only(e.B, x.xs, e.x0, e.x1)});
+        } else {
+            std::vector<PostJob> p1;
+            for (const P& e : post1) p1.push_back(PostJob{e.B, e.x0, e.x1});
+            x.post1 = upload(c, p1, ch.keep);
+            x.np1 = (uint32_t)p1.size();
         }
         staged.push_back(x);
+    }
+    const CollectJob* tail = nullptr;
+    uint32_t ntail = 0;
+    if (!pend.empty()) {
+        if (pending) {
+            for (const Pend& p : pend) pending->push_back(p.job);
+        } else {
+            std::vector<CollectJob> t;
+            for (const Pend& p : pend) t.push_back(p.job);
+            tail = upload(c, t, ch.keep);
+            ntail = (uint32_t)t.size();
+        }
     }
     for (const Staged& x : staged) {
         run_collect(c, d, x.cj, x.ncj);
         run_explore(c, d, x.ej, x.nej, GPS_K_EXPLORE);
-        run_post(c, d, x.post1, x.xs, x.np1);
-        if (!x.npj) continue;
-        if (x.ncp) run_collect(c, d, x.cp, x.ncp);
+        if (!x.npj) {
+            run_post(c, d, x.post1, x.xs, x.np1);
+            continue;
+        }
+        run_collect(c, d, x.cp, x.ncp);
         run_explore(c, d, x.pj, x.npj, GPS_K_PROPAGATE);
-        run_post(c, d, x.post2, x.xs, x.np2);
     }
+    if (ntail) run_collect(c, d, tail, ntail);
 }
 
 void setup_chunk(Chunk& ch) {
@@ -530,10 +607,11 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
     const DevGraph& d = g->d;
     setup_chunk(ch);
     tr.mark("setup (arena)");
-    filter_phase(ch, 2);
+    std::vector<CollectJob> pend;
+    filter_phase(ch, 2, &pend);
     tr.mark("filter enqueued");
 
-    // ---- final collect of every query vertex, sync #1 ----
+    // ---- final collect of every query vertex (+ the last filter step's posts), sync #1 ----
     {
         std::vector<CollectJob> cj;
         for (size_t i = 0; i < ch.qs.size(); i++) {
@@ -541,6 +619,16 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             for (int u = 0; u < q->k; u++)
                 cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0],
                                         q->seg[u][1], ch.cnt_all + ch.ncnt + 2 * (ch.cnt_base[i] + u)});
+        }
+        for (const CollectJob& p : pend) {   // every vertex is collected here: each post finds its job
+            auto it = std::find_if(cj.begin(), cj.end(), [&](const CollectJob& y) { return y.B == p.B && y.x1 == y.x0; });
+            if (it == cj.end()) {
+                cj.push_back(p);
+            } else {
+                it->xs = p.xs;
+                it->x0 = p.x0;
+                it->x1 = p.x1;
+            }
         }
         run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
         const size_t nc = ch.ncnt;
