@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <string>
 #include <mutex>
 #include <utility>
 
@@ -53,7 +54,24 @@ void ctx_sync(gps_ctx* c) {
     ctx_harvest(c);
 }
 
+// Test hook: GPS_FAULT_ALLOC=N makes the N-th device allocation after the variable
+// (re)takes that value fail with GPS_ENOMEM, so tests can drive every failure path.
+static void fault_injection() {
+    static std::mutex mu;
+    static std::string last;
+    static long count = 0;
+    const char* e = std::getenv("GPS_FAULT_ALLOC");
+    if (!e || !*e) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (last != e) {
+        last = e;
+        count = 0;
+    }
+    if (++count == std::atol(e)) fail(GPS_ENOMEM, "injected device allocation failure");
+}
+
 void* dmalloc(gps_ctx* c, size_t bytes) {
+    fault_injection();
     void* p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, c->stream);
     if (e != cudaSuccess) {
@@ -148,8 +166,12 @@ LbScratch lb_scratch(gps_ctx* c, uint32_t slots, uint32_t tiles) {
     if (tiles > c->lb_tiles || slots > c->lb_slots) {
         const uint32_t tcap = std::max<uint32_t>(std::max(tiles, c->lb_tiles), 64);
         const uint32_t scap = std::max<uint32_t>(std::max(slots, c->lb_slots), 192);
+        // drop the old buffers first and forget them, so a failed allocation leaves no dangling state
         if (c->lb_status) dfree(c, c->lb_status);
         if (c->lb_ctr) dfree(c, c->lb_ctr);
+        c->lb_status = nullptr;
+        c->lb_ctr = nullptr;
+        c->lb_tiles = c->lb_slots = 0;
         c->lb_status = static_cast<uint64_t*>(dmalloc(c, sizeof(uint64_t) * (size_t)tcap * scap));
         c->lb_ctr = static_cast<unsigned int*>(dmalloc(c, sizeof(unsigned int) * scap));
         GPS_CK(cudaMemsetAsync(c->lb_status, 0, sizeof(uint64_t) * (size_t)tcap * scap, c->stream));

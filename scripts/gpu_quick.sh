@@ -1,2 +1,2 @@
-timeout 400 python bench.py > gpurun_out/bench_cfg2.log 2> gpurun_out/bench_cfg2.err
-tail -1 gpurun_out/bench_cfg2.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], json.dumps(d['roofline']))"
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k recovers 2>&1 | tail -15
+timeout 300 python scripts/repro_big.py 11 0,1 2>&1 | tail -3

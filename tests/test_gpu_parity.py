@@ -377,3 +377,27 @@ def test_cfg2_match_batch_host(ctx, cfg2):
     t = br.tensor(0)
     assert t.shape == (want_rows[0], 6)
     br.free()
+
+
+def test_recovers_after_allocation_failures(gps, ctx, cfg1, monkeypatch):
+    """Every device-allocation failure path (GPS_FAULT_ALLOC=N fails the N-th allocation) reports
+    GPS_ENOMEM and leaves the context usable: the next calls still give the oracle's answers
+    (A27: GPS_ENOMEM is a reported resource error, never a corrupted context)."""
+    g, G, og = cfg1
+    q = triangle_tail()
+    q2 = Query(4, [-1] * 4, [-1] * 4, [(0, 1, -1), (1, 2, -1), (2, 3, -1), (3, 0, -1)])   # closing edge
+    want, want2 = oracle.match(og, q), oracle.count(og, q2)
+    failed = 0
+    for n in range(1, 80):
+        monkeypatch.setenv("GPS_FAULT_ALLOC", str(n))
+        try:
+            ctx.match(G, q)
+            ctx.count(G, q2)
+            ctx.match_batch(G, [q, q2, q])
+        except gps.GpsError as e:
+            assert "ENOMEM" in str(e), e
+            failed += 1
+        monkeypatch.delenv("GPS_FAULT_ALLOC")
+        assert np.array_equal(_rows(ctx.match(G, q)), want), n
+        assert ctx.count(G, q2) == want2, n
+    assert failed > 10   # the hook reached many allocation sites
