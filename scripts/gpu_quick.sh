@@ -1,2 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k recovers 2>&1 | tail -15
-timeout 300 python scripts/repro_big.py 11 0,1 2>&1 | tail -3
+timeout 1500 python scripts/ablation_refine20.py 24 > gpurun_out/ablation20.txt 2>&1; tail -30 gpurun_out/ablation20.txt
