@@ -209,9 +209,8 @@ void filter_phase(Chunk& ch, int stage, std::vector<CollectJob>* pending = nullp
     struct Staged {
         const CollectJob *cj = nullptr, *cp = nullptr;
         const ExploreJob *ej = nullptr, *pj = nullptr;
-        const PostJob* post1 = nullptr;
         uint32_t* const* xs = nullptr;
-        uint32_t ncj = 0, ncp = 0, nej = 0, npj = 0, np1 = 0;
+        uint32_t ncj = 0, ncp = 0, nej = 0, npj = 0;
     };
     // a post waiting for the next collect launch: B of query qi's vertex v &= AND xs[x0..x1)
     struct Pend {
@@ -335,11 +334,8 @@ void filter_phase(Chunk& ch, int stage, std::vector<CollectJob>* pending = nullp
             x.pj = upload(c, pj, ch.keep);
             x.npj = (uint32_t)pj.size();
             for (const P& e : post2) pend.push_back(Pend{e.qi, e.v, post_only(e.B, x.xs, e.x0, e.x1)});
-        } else {
-            std::vector<PostJob> p1;
-            for (const P& e : post1) p1.push_back(PostJob{e.B, e.x0, e.x1});
-            x.post1 = upload(c, p1, ch.keep);
-            x.np1 = (uint32_t)p1.size();
+        } else {   // no propagation: the prune updates ride on the next collect launch
+            for (const P& e : post1) pend.push_back(Pend{e.qi, e.v, post_only(e.B, x.xs, e.x0, e.x1)});
         }
         staged.push_back(x);
     }
@@ -358,10 +354,7 @@ void filter_phase(Chunk& ch, int stage, std::vector<CollectJob>* pending = nullp
     for (const Staged& x : staged) {
         run_collect(c, d, x.cj, x.ncj);
         run_explore(c, d, x.ej, x.nej, GPS_K_EXPLORE);
-        if (!x.npj) {
-            run_post(c, d, x.post1, x.xs, x.np1);
-            continue;
-        }
+        if (!x.npj) continue;
         run_collect(c, d, x.cp, x.ncp);
         run_explore(c, d, x.pj, x.npj, GPS_K_PROPAGATE);
     }

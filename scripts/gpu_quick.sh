@@ -1,4 +1,5 @@
-MODE=match SLICE=34 timeout 600 ncu -f --set full --import-source on --clock-control none -k regex:"k_explore" -c 6 -o /tmp/prof_ex python scripts/ncu_target.py > /dev/null 2>&1
-python scripts/ncu_lines.py /tmp/prof_ex.ncu-rep gpurun_out/ex_lines 6
-M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,sm__warps_active.avg.pct_of_peak_sustained_active,sm__throughput.avg.pct_of_peak_sustained_elapsed,launch__grid_size,launch__registers_per_thread,smsp__inst_executed.sum,smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio,smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio,smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio,smsp__average_warps_issue_stalled_wait_per_issue_active.ratio,smsp__thread_inst_executed_per_inst_executed.ratio
-ncu -i /tmp/prof_ex.ncu-rep --page raw --csv --metrics $M > gpurun_out/ex_raw.csv
+(timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo exit $? >> gpurun_out/gpu_tests.log)
+tail -2 gpurun_out/gpu_tests.log
+python scripts/batch_classes.py 2 34 > gpurun_out/classes_cfg2.txt 2>&1; head -11 gpurun_out/classes_cfg2.txt
+timeout 400 python bench.py --no-cpu-baseline > gpurun_out/bench_cfg2.log 2> gpurun_out/bench_cfg2.err
+tail -1 gpurun_out/bench_cfg2.log | cut -c 1-250
