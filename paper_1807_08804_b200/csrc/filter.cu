@@ -111,7 +111,7 @@ constexpr int kColWords = 4;                          // bitmap words (128 verti
 constexpr int kColTile = kColThreads * kColWords;     // words per tile
 constexpr int kColBatch = 8;                          // candidates whose degrees are loaded together
 
-__global__ void __launch_bounds__(kColThreads) k_collect(DevGraph g, const CollectJob* __restrict__ jobs,
+__global__ void __launch_bounds__(kColThreads, 5) k_collect(DevGraph g, const CollectJob* __restrict__ jobs,
                                                          LbScratch lb, uint32_t ntiles, uint32_t epoch) {
     const uint32_t y = blockIdx.y;
     const CollectJob& J = jobs[y];

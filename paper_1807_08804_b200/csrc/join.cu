@@ -49,7 +49,7 @@ __host__ __device__ inline size_t ec_smem_n(uint32_t nj) {
     return EcSmem::bytes(nj, sizeof(uint32_t) * kEcTile + 16);
 }
 
-__global__ void __launch_bounds__(kPT) k_ec(DevGraph g, const ECJob* __restrict__ jobs, uint32_t nj, LbScratch lb,
+__global__ void __launch_bounds__(kPT, 5) k_ec(DevGraph g, const ECJob* __restrict__ jobs, uint32_t nj, LbScratch lb,
                                            uint32_t ntiles, uint32_t epoch, uint32_t* __restrict__ val,
                                            uint64_t base, unsigned long long* bytes_acc) {
     extern __shared__ __align__(16) char s_dyn[];
