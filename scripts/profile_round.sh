@@ -2,7 +2,7 @@
 # Round evidence: launch list of the default bench, full captures of one cfg2 batch (bench slicing)
 # and of the cfg4 joins, summarised into profiles/ and copied to gpurun_out/ (profiles/ on the box
 # does not travel back).   usage: bash scripts/profile_round.sh ROUND
-R=${1:-r01c}
+R=${1:-r01d}
 mkdir -p gpurun_out/profiles
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file /tmp/launches_$R.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/profiles/${R}_bench_under_ncu.log 2>&1
