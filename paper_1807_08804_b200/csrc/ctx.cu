@@ -234,6 +234,7 @@ void ctx_init(gps_ctx* c, int dev, cudaStream_t stream) {
 
 void ctx_release(gps_ctx* c) {
     cudaStreamSynchronize(c->stream);
+    c->arena_cache.reset();
     if (std::getenv("GPS_EXPLORE_STATS") && c->d_info) {
         uint64_t h[8];
         if (cudaMemcpy(h, c->d_info + 96, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess && h[0] + h[4])

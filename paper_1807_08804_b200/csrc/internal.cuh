@@ -69,6 +69,10 @@ struct PendingTiming {
 
 }  // namespace gps
 
+namespace gps {
+struct DevBlock;
+}
+
 struct gps_ctx {
     int device = 0;
     int nsm = 148;
@@ -105,6 +109,10 @@ struct gps_ctx {
     uint32_t nworkers_req = 0;               // 0 = default (2)
     uint32_t slice = 0;                      // queries per worker hand-out (0 = default 64)
     gps::Comm* comm = nullptr;               // row-sharded join across ranks (world > 1)
+    // the previous run's filter-state arena, reused by the next run when large enough and no
+    // result holds it (saves an allocation per batch slice)
+    std::shared_ptr<gps::DevBlock> arena_cache;
+    size_t arena_cache_bytes = 0;
 };
 
 struct gps_graph {

@@ -367,7 +367,16 @@ void setup_chunk(Chunk& ch) {
     ch.rps = ch.g->d.nws + 64;
     Carve sz;
     carve_all(ch, sz);
-    ch.arena = make_block(c, sz.off + kAlign);
+    const size_t need = sz.off + kAlign;
+    if (c->arena_cache && c->arena_cache_bytes >= need && c->arena_cache.use_count() == 1) {
+        ch.arena = c->arena_cache;   // the last run is over (arena_reset synced the stream)
+    } else {
+        c->arena_cache.reset();
+        const size_t cap = need + need / 4;
+        ch.arena = make_block(c, cap);
+        c->arena_cache = ch.arena;
+        c->arena_cache_bytes = cap;
+    }
     Carve cv;
     cv.base = static_cast<char*>(ch.arena->p);
     carve_all(ch, cv);
