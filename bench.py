@@ -256,10 +256,10 @@ def main():
         dominant = max(ms, key=ms.get)
         kd_iso = iso[dominant]
         total_iso = sum(ms.values())
-        if args.workers:   # fresh worker contexts: warm them again (scratch growth, first launches)
-            ctx.set_workers(args.workers)
+        if args.workers:   # fresh worker contexts: warm them again (scratch growth, first launches;
+            ctx.set_workers(args.workers)   # their first steps can stall on driver allocations)
             ctx.set_slice(args.slice)
-            for _ in range(max(args.warmup, 3)):
+            for _ in range(max(args.warmup, 10)):
                 step()
         ctx.set_profiling([dominant])
         ctx.reset_stats()
