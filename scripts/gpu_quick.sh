@@ -1,5 +1,7 @@
+# One gpurun round trip: GPU parity tests, smoke, default bench line.
+#   /usr/local/graft/bin/gpurun --timeout 1500 -- 'bash scripts/gpu_quick.sh'
+(timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo exit $? >> gpurun_out/gpu_tests.log)
+tail -2 gpurun_out/gpu_tests.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
 timeout 400 python bench.py > gpurun_out/bench_cfg2.log 2> gpurun_out/bench_cfg2.err
-timeout 400 python bench.py --config 5 --steps 5 --no-cpu-baseline > gpurun_out/bench_cfg5.log 2> gpurun_out/bench_cfg5.err
-timeout 400 python bench.py --config 3 --no-cpu-baseline > gpurun_out/bench_cfg3.log 2> gpurun_out/bench_cfg3.err
-timeout 400 python bench.py > gpurun_out/bench_cfg2b.log 2> gpurun_out/bench_cfg2b.err
-for c in 2 3 5 2b; do tail -1 gpurun_out/bench_cfg$c.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['value'],1), round(d['ms_per_step'],3), '%.3g'%d['embeddings_per_s'], d['roofline']['kernel'], round(d['roofline']['achieved'],1), round(d['roofline']['frac'],4), round(d['e2e']['value'],1), d.get('cpu_baseline',{}).get('value'), d['clocks']['reasons'], d.get('latency_ms',{}).get('p99'))"; done
+tail -1 gpurun_out/bench_cfg2.log | cut -c 1-300
