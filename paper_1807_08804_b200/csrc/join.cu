@@ -162,8 +162,9 @@ void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uin
 
 // ------------------------------------------------------------ a8 join step
 // rows per thread (4 rows amortise the scan; the FAST pass interleaves their searches)
-template <bool FAST> constexpr int seg_rows() { return 4; }
-template <bool FAST> constexpr int seg_tile() { return 256 * seg_rows<FAST>(); }
+// (FAST: 2 rows per thread on small tables -- more threads, shorter chains; 4 on large ones --
+// more searches in flight per thread; measured on configs 2 and 4)
+constexpr uint64_t kSegBigRows = 1u << 22;
 
 
 // Per input row: O(1) key lookup -> EC segment start (s0) and the exclusive scan of
@@ -171,10 +172,10 @@ template <bool FAST> constexpr int seg_tile() { return 256 * seg_rows<FAST>(); }
 // (closing-free steps): also the row values found in the segment (imask, binary
 // searches advanced in lockstep), the per-job output totals, and the scan of the
 // rows' written outputs (woff) -- two look-backs in two warps.
-template <bool FAST>
+template <bool FAST, int kSegRows>
 __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
                                                   uint32_t epoch) {
-    constexpr int kSegRows = seg_rows<FAST>(), kSegTile = seg_tile<FAST>();
+    constexpr int kSegTile = 256 * kSegRows;
     extern __shared__ __align__(16) char s_dyn[];
     uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);   // [nj+1] first row of every job
     __shared__ uint64_t s_pre[3];
@@ -316,18 +317,19 @@ __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinSt
 }
 
 void run_join_seg(gps_ctx* c, const JoinStep& s) {
-    const uint64_t tile = s.fast ? seg_tile<true>() : seg_tile<false>();
+    const int rows = (s.fast && s.R < kSegBigRows) ? 2 : 4;
+    const uint64_t tile = 256ull * rows;
     const uint64_t nt = (s.R + tile - 1) / tile;
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join table too large");
     LbScratch lb = lb_scratch(c, 2, (uint32_t)nt);
-    if (s.fast)
-        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), sizeof(uint64_t) * (s.nj + 1), k_join_seg<true>, s,
-               lb, (uint32_t)nt,
-               lb_next_epoch(c));
+    const size_t smem = sizeof(uint64_t) * (s.nj + 1);
+    const uint32_t ep = lb_next_epoch(c);
+    if (!s.fast)
+        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), smem, k_join_seg<false, 4>, s, lb, (uint32_t)nt, ep);
+    else if (rows == 2)
+        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), smem, k_join_seg<true, 2>, s, lb, (uint32_t)nt, ep);
     else
-        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), sizeof(uint64_t) * (s.nj + 1), k_join_seg<false>, s,
-               lb, (uint32_t)nt,
-               lb_next_epoch(c));
+        launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), smem, k_join_seg<true, 4>, s, lb, (uint32_t)nt, ep);
     c->stats.k_bytes[GPS_K_JOIN_LEN] += 4.0 * s.R * (s.w + 3);
 }
 
