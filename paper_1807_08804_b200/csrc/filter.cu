@@ -236,7 +236,7 @@ void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32
 
 // -------------------------------------------------------------- a4 explore
 constexpr int kET = 256;
-constexpr int kEI = 8;
+constexpr int kEI = 4;   // pairs per thread per chunk (8 measured slower on configs 2 and 4)
 constexpr int kEW = 512;
 
 struct ExMeta {             // one row (key vertex) of an explore job, staged per chunk
