@@ -22,7 +22,7 @@ EINVAL, EDISCONNECTED, ELIMIT, ENOMEM = -1, -2, -3, -4
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", _LIB, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC])
     return _LIB
 
 
@@ -43,6 +43,9 @@ def _load():
         lib.oracle_match.argtypes = [P, ctypes.c_uint32, P, P, ctypes.c_uint32, P, P, P, P,
                                      ctypes.c_uint64, ctypes.c_uint64]
         lib.oracle_set_work_limit.argtypes = [ctypes.c_uint64]
+        lib.oracle_run.restype = None
+        lib.oracle_run.argtypes = [P, ctypes.c_uint32, P, P, ctypes.c_uint32, P, P, P, ctypes.c_uint32,
+                                   ctypes.c_uint32, ctypes.c_uint32, P, ctypes.c_uint64, ctypes.c_uint64, P]
         _lib = lib
     return _lib
 
@@ -121,3 +124,64 @@ def sort_rows(rows: np.ndarray) -> np.ndarray:
         return rows
     order = np.lexsort(rows.T[::-1])
     return rows[order]
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int64), ("hash", ctypes.c_uint64), ("level", ctypes.c_uint64 * 32),
+                ("pi", ctypes.c_uint32 * 32), ("threads", ctypes.c_uint32)]
+
+
+def run(og: OracleGraph, q, threads: int = 1, col0_range=None, rows: bool = False, limit: int = 0,
+        cap: int = 0) -> dict:
+    """One oracle search with its bookkeeping (oracle.c oracle_run).
+
+    threads > 1: the OpenMP timing variant (same result).  col0_range=(lo, hi): only
+    embeddings whose image of query vertex 0 lies in [lo, hi).  rows=True also returns
+    the sorted rows (cap rows at most: pass the count from a first run).  Returns
+    dict(count, hash (multiset hash, see oracle.c row_hash), levels (#partial maps per
+    BFS depth), order (the BFS order), threads, rows (if asked)).  count = ELIMIT when
+    the search was cut by `limit` / the work limit."""
+    lib = _load()
+    vl, bd, a, b, lab = _qarrays(q)
+    res = _Result()
+    lo, hi = (0, 0) if col0_range is None else (int(col0_range[0]), int(col0_range[1]))
+    if col0_range is not None and hi <= lo:
+        out = dict(count=0, hash=0, levels=[0] * q.k, order=[], threads=threads)
+        if rows:
+            out["rows"] = np.zeros((0, q.k), np.uint32)
+        return out
+    buf = np.zeros((max(cap, 1), q.k), np.uint32) if rows else None
+    lib.oracle_run(og._h, q.k, _ptr(vl), _ptr(bd), a.shape[0], _ptr(a), _ptr(b), _ptr(lab), int(threads),
+                   lo, hi, _ptr(buf), cap if rows else 0, int(limit), ctypes.byref(res))
+    c = int(res.count)
+    if c < 0 and c != ELIMIT:
+        raise ValueError(f"oracle error {c}")
+    out = dict(count=c, hash=int(res.hash), levels=[int(res.level[i]) for i in range(q.k)],
+               order=[int(res.pi[i]) for i in range(q.k)], threads=int(res.threads))
+    if rows:
+        if c > cap:
+            raise OverflowError(f"{c} rows > cap {cap}")
+        out["rows"] = sort_rows(buf[:max(c, 0)])
+    return out
+
+
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(x: int) -> int:
+    z = (x + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def row_hash_py(row) -> int:
+    """Pure-Python restatement of oracle.c row_hash (for pinning it)."""
+    h = 0x243F6A8885A308D3 ^ len(row)
+    for v in row:
+        h = _splitmix64(h ^ int(v))
+    return h
+
+
+def multiset_hash_py(rows) -> int:
+    return sum(row_hash_py(r) for r in rows) & _M64
