@@ -118,6 +118,15 @@ typedef struct {
     int32_t result_on_device;    /* gps_match: 1 = rows stay in device memory (default), 0 = host copy */
     float rebalance_threshold;   /* row-sharded join: exchange rows when max/mean pairs per rank exceeds
                                     this (default 1.10; 0 = always, very large = never) */
+    uint64_t row_budget_bytes;   /* largest partial-embedding table (bytes) a join step may materialise
+                                    at once (reading R27, "intermediate results ... a key
+                                    challenge"): a step whose output exceeds it is split into pair
+                                    ranges and each piece runs the remaining steps depth-first (the
+                                    result set does not depend on it).  0 (default) = one third of the
+                                    device memory free at the time of the step.  gps_count never
+                                    materialises its last level, so it never fails for lack of
+                                    memory on the tables; gps_match returns GPS_ENOMEM only when the
+                                    final rows themselves cannot be allocated. */
 } gps_match_opts;
 
 GPS_API gps_status gps_default_opts(gps_match_opts* opts);
@@ -155,10 +164,13 @@ GPS_API gps_status gps_count(gps_ctx* ctx, const gps_graph* g, const gps_query* 
 /* Batched execution of nq independent queries (the QA-batch use, BASELINE
  * configs[4]): the library runs them concurrently on a pool of worker host
  * threads, each owning a CUDA stream and scratch (set its size with
- * gps_set_workers; default 8).  results[i] / counts[i] / statuses[i] (statuses
- * may be NULL) as for the single-query calls; results are owned by the caller
- * (gps_result_free).  The ctx stream is ordered before / after the batch.
- * Returns the first failing status (GPS_OK if all succeeded). */
+ * gps_set_workers; default 2).  results[i] / counts[i] / statuses[i] (statuses
+ * may be NULL) as for the single-query calls: every entry of statuses is written,
+ * a query that failed has results[i] = NULL.  A query whose candidate-edge tables
+ * alone exceed the 32-bit table limits fails with GPS_EOVERFLOW without affecting
+ * the others.  Results are owned by the caller (gps_result_free) and by the ctx
+ * (its stream orders their release).  The ctx stream is ordered before / after the
+ * batch.  Returns the first failing status (GPS_OK if all succeeded). */
 GPS_API gps_status gps_match_batch(gps_ctx* ctx, const gps_graph* g, const gps_query* queries, uint32_t nq,
                                    const gps_match_opts* opts, gps_result** results, gps_status* statuses);
 GPS_API gps_status gps_count_batch(gps_ctx* ctx, const gps_graph* g, const gps_query* queries, uint32_t nq,
@@ -199,6 +211,11 @@ GPS_API gps_status gps_create_local_rank(const gps_ctx_opts* opts, gps_local_com
 GPS_API gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols,
                            const uint32_t** data, int* on_device);
 GPS_API void gps_result_free(gps_result* r);
+/* Like gps_result_free, but the device memory is released only after the work
+ * enqueued so far on `stream` (a cudaStream_t, e.g. the torch stream that read the
+ * rows) has completed: the ctx stream waits on an event recorded on `stream`.
+ * NULL stream = gps_result_free. */
+GPS_API void gps_result_free_after(gps_result* r, void* stream);
 
 GPS_API const char* gps_last_error(void);
 

@@ -22,8 +22,10 @@
  *   1. pi = BFS order of the query's undirected skeleton from vertex 0
  *      (neighbours in increasing id).  Disconnected -> error.
  *   2. rec(i): u = pi[i]; candidates = {bound(u)} if bound, all V if i == 0,
- *      else the distinct out- (or in-) neighbours of f(p) for the earliest
- *      already-mapped query neighbour p (following the arc's direction).
+ *      else the distinct out- (or in-) neighbours of f(p) for the already-mapped
+ *      query neighbour p whose image has the shortest adjacency list in the
+ *      arc's direction (any mapped neighbour gives the same set once every arc
+ *      is checked; the shortest list is the fewest tries).
  *      Keep v iff label(u) in {*, l(v)}, v unused, and EVERY query arc between
  *      u and an already-mapped vertex is present in the data with a matching
  *      label.  Recurse; at i == k emit f.
@@ -256,9 +258,22 @@ static void rec(orc_state *s, uint32_t i, uint32_t stop_at, leaf_fn leaf, void *
             if (try_vertex(s, i, v)) take(s, i, v, stop_at, leaf, user);
         return;
     }
+    /* candidates: the distinct neighbours of the mapped query neighbour whose image has
+       the shortest adjacency list in the needed direction (every other arc is checked by
+       try_vertex, so any mapped neighbour gives the same set; the shortest list is the
+       fewest tries -- a hub image would otherwise be scanned for every partial map) */
     uint32_t w = s->f[p->parent[u]];
-    const uint64_t *off = p->parent_out[u] ? g->out_off : g->in_off;
-    const oarc_t *arc = p->parent_out[u] ? g->out_arc : g->in_arc;
+    int use_out = p->parent_out[u];
+    uint64_t best = (use_out ? g->out_off : g->in_off)[w + 1] - (use_out ? g->out_off : g->in_off)[w];
+    for (int c = 0; c < p->nchk[i]; c++) {
+        const chk_t *ck = &p->chk[i][c];
+        uint32_t x = s->f[ck->other];
+        int xo = !ck->out;   /* arc other->u: u is an out-neighbour of f(other) */
+        uint64_t len = (xo ? g->out_off : g->in_off)[x + 1] - (xo ? g->out_off : g->in_off)[x];
+        if (len < best) { best = len; w = x; use_out = xo; }
+    }
+    const uint64_t *off = use_out ? g->out_off : g->in_off;
+    const oarc_t *arc = use_out ? g->out_arc : g->in_arc;
     for (uint64_t e = off[w]; e < off[w + 1] && !s->sh->over; e++) {
         uint32_t v = arc[e].v;
         if (e > off[w] && arc[e - 1].v == v) continue;   /* distinct neighbours only */

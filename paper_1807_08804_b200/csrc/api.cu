@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -54,7 +55,10 @@ static void check_args(gps_ctx* c, const gps_graph* g) {
 }
 
 // Wrap one query's outcome as a gps_result owned by ctx c (device rows or pinned host rows).
-static gps_result* wrap_result(gps_ctx* c, QueryResult& qr, bool on_device) {
+// owner: the ctx the caller holds (a batch's worker results are re-homed to it, so they
+// outlive gps_set_workers and are released on the caller's ctx stream, which the batch
+// call ordered after every worker stream).
+static gps_result* wrap_result(gps_ctx* c, QueryResult& qr, bool on_device, gps_ctx* owner = nullptr) {
     gps_result* r = new gps_result();
     r->rows = qr.rows;
     r->cols = qr.cols;
@@ -77,7 +81,15 @@ static gps_result* wrap_result(gps_ctx* c, QueryResult& qr, bool on_device) {
         r->host_bytes = got;
         if (bytes) GPS_CK(cudaMemcpyAsync(r->data, qr.data, bytes, cudaMemcpyDeviceToHost, c->stream));
     }
-    c->results.push_back(r);
+    if (owner && owner != c) {
+        if (r->hold) r->hold->c = owner;   // freed on the owner's stream from now on
+        r->ctx = owner;
+        std::lock_guard<std::mutex> lk(owner->results_mu);
+        owner->results.push_back(r);
+    } else {
+        std::lock_guard<std::mutex> lk(c->results_mu);
+        c->results.push_back(r);
+    }
     return r;
 }
 
@@ -108,7 +120,10 @@ static void drop_workers(gps_ctx* c) {
 // Split the batch into contiguous slices handed out dynamically to the workers;
 // each worker runs its slice batch-synchronously on its own stream
 // (run_queries).  body(worker ctx, first query, count) fills the outputs.
-static void run_sliced(gps_ctx* c, uint32_t nq, const std::function<void(gps_ctx*, uint32_t, uint32_t)>& body) {
+// A slice whose worker threw reports the error as the status of each of its queries
+// (on_fail(lo, cnt, status)); the other slices are unaffected.
+static void run_sliced(gps_ctx* c, uint32_t nq, const std::function<void(gps_ctx*, uint32_t, uint32_t)>& body,
+                       const std::function<void(uint32_t, uint32_t, gps_status)>& on_fail) {
     if (c->comm && c->comm->world > 1) {   // SPMD ranks: every rank walks the batch in the same order
         body(c, 0, nq);
         return;
@@ -136,9 +151,11 @@ static void run_sliced(gps_ctx* c, uint32_t nq, const std::function<void(gps_ctx
             } catch (const Error& e) {
                 std::lock_guard<std::mutex> lk(emu);
                 errs.push_back(e);
+                on_fail(lo, cnt, e.status);
             } catch (...) {
                 std::lock_guard<std::mutex> lk(emu);
                 errs.push_back(Error{GPS_ECUDA, "unexpected internal error in a batch worker"});
+                on_fail(lo, cnt, GPS_ECUDA);
             }
         }
         cudaEventCreateWithFlags(&fin[w], cudaEventDisableTiming);
@@ -150,7 +167,7 @@ static void run_sliced(gps_ctx* c, uint32_t nq, const std::function<void(gps_ctx
             cudaEventDestroy(e);
         }
     cudaEventDestroy(start);
-    if (!errs.empty()) throw errs.front();
+    if (!errs.empty()) set_last_error(errs.front().msg);
 }
 
 static std::vector<gps_ctx*> all_ctx(gps_ctx* c) {
@@ -172,6 +189,7 @@ gps_status gps_default_opts(gps_match_opts* o) {
     o->lowconn_threshold = 1;
     o->result_on_device = 1;
     o->rebalance_threshold = 1.10f;
+    o->row_budget_bytes = 0;
     return GPS_OK;
 }
 
@@ -366,9 +384,12 @@ gps_status gps_match_batch(gps_ctx* c, const gps_graph* g, const gps_query* qs, 
             run_queries(sc, g, qs + lo, cnt, o, false, qr);
             for (uint32_t i = 0; i < cnt; i++) {
                 st[lo + i] = qr[i].status;
-                if (qr[i].status == GPS_OK) results[lo + i] = wrap_result(sc, qr[i], o.result_on_device != 0);
+                if (qr[i].status == GPS_OK) results[lo + i] = wrap_result(sc, qr[i], o.result_on_device != 0, c);
             }
             ctx_sync(sc);
+        }, [&](uint32_t lo, uint32_t cnt, gps_status e) {
+            for (uint32_t i = lo; i < lo + cnt; i++)
+                if (!results[i]) st[i] = e;
         });
         gps_status first = GPS_OK;
         for (uint32_t i = 0; i < nq; i++) {
@@ -407,6 +428,8 @@ gps_status gps_match_batch_host(gps_ctx* c, const gps_graph* g, const gps_query*
                     GPS_CK(cudaMemcpyAsync(host_out + at, qr[i].data, words * 4, cudaMemcpyDeviceToHost, sc->stream));
             }
             ctx_sync(sc);
+        }, [&](uint32_t lo, uint32_t cnt, gps_status e) {
+            for (uint32_t i = lo; i < lo + cnt; i++) st[i] = e;
         });
         gps_status first = GPS_OK;
         for (uint32_t i = 0; i < nq; i++) {
@@ -434,6 +457,11 @@ gps_status gps_count_batch(gps_ctx* c, const gps_graph* g, const gps_query* qs, 
                 st[lo + i] = qr[i].status;
                 counts[lo + i] = qr[i].global_rows;
             }
+        }, [&](uint32_t lo, uint32_t cnt, gps_status e) {
+            for (uint32_t i = lo; i < lo + cnt; i++) {
+                st[i] = e;
+                counts[i] = 0;
+            }
         });
         gps_status first = GPS_OK;
         for (uint32_t i = 0; i < nq; i++) {
@@ -454,20 +482,37 @@ gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols, 
     return GPS_OK;
 }
 
-void gps_result_free(gps_result* r) {
+void gps_result_free_after(gps_result* r, void* stream) {
     if (!r) return;
     if (r->ctx) {
         gps_ctx* c = r->ctx;
         int prev = -1;
         cudaGetDevice(&prev);
         if (prev != c->device) cudaSetDevice(c->device);
+        if (r->on_device && stream && (cudaStream_t)stream != c->stream) {
+            // the consumer's stream may still be reading the rows: order the release after it
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+                cudaEventRecord(e, (cudaStream_t)stream);
+                cudaStreamWaitEvent(c->stream, e, 0);
+                cudaEventDestroy(e);
+            } else {
+                (void)cudaGetLastError();
+                cudaStreamSynchronize((cudaStream_t)stream);
+            }
+        }
         if (r->on_device) r->hold.reset();
         else pinned_release(c, r->data, r->host_bytes);
-        c->results.erase(std::remove(c->results.begin(), c->results.end(), r), c->results.end());
+        {
+            std::lock_guard<std::mutex> lk(c->results_mu);
+            c->results.erase(std::remove(c->results.begin(), c->results.end(), r), c->results.end());
+        }
         if (prev >= 0 && prev != c->device) cudaSetDevice(prev);
     }
     delete r;
 }
+
+void gps_result_free(gps_result* r) { gps_result_free_after(r, nullptr); }
 
 gps_status gps_get_stats(gps_ctx* c, gps_stats* out) {
     return guarded([&] {

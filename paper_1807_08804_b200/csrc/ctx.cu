@@ -70,10 +70,49 @@ static void fault_injection() {
     if (++count == std::atol(e)) fail(GPS_ENOMEM, "injected device allocation failure");
 }
 
+// The library's own stream-ordered memory pool per device (never the device's default
+// pool, whose attributes other users of the process own).  Freed blocks stay cached
+// up to GPS_POOL_KEEP_BYTES (default 16 GiB) across synchronisations, so a steady
+// stream of same-sized queries reuses memory without driver calls; anything above is
+// returned to the driver at the next synchronisation.
+cudaMemPool_t device_pool(int dev) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = pools.find(dev);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    GPS_CK(cudaMemPoolCreate(&pool, &props));
+    const char* e = std::getenv("GPS_POOL_KEEP_BYTES");
+    uint64_t keep = (e && *e) ? std::strtoull(e, nullptr, 10) : (16ull << 30);
+    GPS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    pools[dev] = pool;
+    return pool;
+}
+
+// Dynamic shared memory opt-in of a kernel on the CURRENT device (the attribute is per
+// function per device context), once per (device, kernel, size).
+void allow_smem(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;
+    int dev = 0;
+    GPS_CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto& have = done[{dev, func}];
+    if (have >= bytes) return;
+    GPS_CK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
+}
+
 void* dmalloc(gps_ctx* c, size_t bytes) {
     fault_injection();
     void* p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, c->stream);
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, c->pool_mem, c->stream);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
         fail(GPS_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed");
@@ -218,10 +257,7 @@ void ctx_init(gps_ctx* c, int dev, cudaStream_t stream) {
         GPS_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
     }
-    cudaMemPool_t pool;
-    GPS_CK(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t thr = ~0ull;
-    GPS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    c->pool_mem = device_pool(dev);
     GPS_CK(cudaMalloc(&c->d_bytes, sizeof(unsigned long long) * GPS_K_NCLASSES));
     GPS_CK(cudaMemset(c->d_bytes, 0, sizeof(unsigned long long) * GPS_K_NCLASSES));
     GPS_CK(cudaMalloc(&c->d_info, sizeof(uint64_t) * 128));

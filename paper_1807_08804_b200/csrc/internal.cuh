@@ -6,6 +6,7 @@
 
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -77,6 +78,7 @@ struct gps_ctx {
     int device = 0;
     int nsm = 148;
     cudaStream_t stream = nullptr;
+    cudaMemPool_t pool_mem = nullptr;        // the library's memory pool of this device (ctx.cu device_pool)
     bool own_stream = false;
     uint32_t prof_mask = 0;
     gps_stats stats{};
@@ -102,7 +104,8 @@ struct gps_ctx {
     size_t arena_seg = 0, h_arena_off = 0;
     size_t h_flushed = 0;                    // [h_flushed, h_arena_off) of the current segment not yet copied
     std::multimap<size_t, void*> pinned_free;  // pinned host buffers for host results (reused)
-    std::vector<gps_result*> results;        // live device results (freed at destroy)
+    std::vector<gps_result*> results;        // live results (freed at destroy)
+    std::mutex results_mu;                   // batch workers register results concurrently
     // batch execution: worker sub-contexts (own stream + scratch) driven by a host thread pool
     std::vector<gps_ctx*> workers;
     gps::WorkerPool* pool = nullptr;
@@ -179,6 +182,9 @@ inline void launch(gps_ctx* c, int cls, dim3 grid, dim3 block, size_t smem, Kern
 }
 
 // ---- stream-ordered device memory -----------------------------------------
+cudaMemPool_t device_pool(int dev);
+// opt a kernel in to `bytes` of dynamic shared memory on the current device (idempotent, thread-safe)
+void allow_smem(const void* func, int bytes);
 void* dmalloc(gps_ctx* c, size_t bytes);
 void dfree(gps_ctx* c, void* p);
 template <typename T>

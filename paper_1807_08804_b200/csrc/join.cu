@@ -150,11 +150,7 @@ void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uin
             uint64_t base) {
     if (nj == 0 || ntiles == 0) return;
     if (nj > kMaxJobsPerLaunch) fail(GPS_EINVAL, "too many EC jobs per launch");
-    static std::once_flag once;
-    std::call_once(once, [] {
-        GPS_CK(cudaFuncSetAttribute(k_ec, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)ec_smem_n(kMaxJobsPerLaunch)));
-    });
+    allow_smem((const void*)k_ec, (int)ec_smem_n(kMaxJobsPerLaunch));
     LbScratch lb = lb_scratch(c, 1, ntiles);
     launch(c, GPS_K_EC_WRITE, dim3(ntiles), dim3(kPT), ec_smem_n(nj), k_ec, g, d_jobs, nj, lb, ntiles,
            lb_next_epoch(c), val, base, c->d_bytes + GPS_K_EC_WRITE);
@@ -784,18 +780,12 @@ __global__ void __launch_bounds__(kPT, 4) k_join_fast(const __grid_constant__ Jo
 
 template <uint32_t WOUT>
 static void launch_join_fast(gps_ctx* c, const JoinStep& s, uint64_t P) {
-    static std::once_flag once;
-    static int occ = 1;
     const size_t smax = JFSmem::bytes(kMaxJobsPerLaunch, jf_stage(WOUT));
-    std::call_once(once, [&] {
-        GPS_CK(cudaFuncSetAttribute(k_join_fast<WOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
-        GPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_join_fast<WOUT>, kPT,
-                                                             JFSmem::bytes(64, jf_stage(WOUT))));
-        if (occ < 1) occ = 1;
-    });
+    allow_smem((const void*)k_join_fast<WOUT>, (int)smax);
     // one resident wave; no more blocks than chunks (a block's fixed cost is a global search)
     const uint64_t chunks = (P + kFTile - 1) / kFTile;
-    const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->nsm * occ, chunks));
+    const uint32_t wave = resident_grid(c, (const void*)k_join_fast<WOUT>, kPT, JFSmem::bytes(64, jf_stage(WOUT)));
+    const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)wave, chunks));
     launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), JFSmem::bytes(s.nj, jf_stage(WOUT)), k_join_fast<WOUT>, s);
 }
 
@@ -826,17 +816,10 @@ static size_t join_smem(uint32_t nj, int mode, uint32_t wout) {
 // attribute is per function; setting it per launch would race between the
 // batch worker threads).
 static void allow_join_smem() {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        GPS_CK(cudaFuncSetAttribute(k_join<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)join_smem(kMaxJobsPerLaunch, 0, 0)));
-        GPS_CK(cudaFuncSetAttribute(k_join<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)join_smem(kMaxJobsPerLaunch, 1, 0)));
-        GPS_CK(cudaFuncSetAttribute(k_join<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)join_smem(kMaxJobsPerLaunch, 2, GPS_MAX_QV)));
-        GPS_CK(cudaFuncSetAttribute(k_join_v, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)join_v_smem(kMaxJobsPerLaunch, kStageW)));
-    });
+    allow_smem((const void*)k_join<0>, (int)join_smem(kMaxJobsPerLaunch, 0, 0));
+    allow_smem((const void*)k_join<1>, (int)join_smem(kMaxJobsPerLaunch, 1, 0));
+    allow_smem((const void*)k_join<2>, (int)join_smem(kMaxJobsPerLaunch, 2, GPS_MAX_QV));
+    allow_smem((const void*)k_join_v, (int)join_v_smem(kMaxJobsPerLaunch, kStageW));
 }
 
 __global__ void k_rows_for_ranges(const uint64_t* __restrict__ poff, uint64_t R, const uint64_t* __restrict__ lohi,

@@ -40,6 +40,26 @@ double single_pass_bytes() {
     return e && *e ? std::atof(e) : 24.0 * (1ull << 30);
 }
 
+// Limit on the candidate-edge pairs of one chunk (32-bit value positions); GPS_EC_PAIR_LIMIT
+// lowers it (test hook: drives the deferral and per-query overflow paths).
+uint64_t ec_pair_limit() {
+    const char* e = std::getenv("GPS_EC_PAIR_LIMIT");
+    const uint64_t lim = 1ull << 32;
+    return e && *e ? std::min<uint64_t>(lim, std::strtoull(e, nullptr, 10)) : lim;
+}
+
+// Row budget of a join step (gps_match_opts.row_budget_bytes; 0 = one third of the
+// device memory free now, reading R27).
+uint64_t step_budget(uint64_t opt) {
+    if (opt) return opt;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 1ull << 30;
+    }
+    return std::max<uint64_t>(fr / 3, 64ull << 20);
+}
+
 struct Carve {
     char* base = nullptr;
     size_t off = 0;
@@ -115,6 +135,7 @@ struct Chunk {
     std::vector<uint32_t> cnt_base;
     std::vector<DevPtr> keep;     // uploaded job arrays
     float rebalance = 1.10f;      // row-sharded join threshold
+    uint64_t budget_opt = 0;      // gps_match_opts.row_budget_bytes
     uint32_t nws = 0, rps = 0;
     uint32_t* Bp(const QS& q, int u) const { return q.B + (size_t)u * nws; }
     uint32_t* Xp(const QS& q, int s) const { return q.X + (size_t)s * nws; }
@@ -597,8 +618,156 @@ void join_sharded(Chunk& ch, QS* q, const uint32_t* ec_val, const std::function<
     }
 }
 
+// Depth-first join of ONE query from step s on (reading R27): the step's
+// pair space is cut into ranges whose output fits the row budget; each range is
+// counted, written and carried through the remaining steps before the next range
+// starts, so at most one piece per level is alive.  The result set is the same as the
+// breadth-first batch path (pieces partition the pair space; the last level's pieces
+// are concatenated in pair order).  Used when a step of the batch path would exceed
+// the budget or its allocation fails.
+struct DeepOut {
+    uint64_t count = 0;
+    std::vector<std::pair<Block, uint64_t>> pieces;   // final rows (match mode), in pair order
+};
+
+void join_deep(Chunk& ch, QS* q, size_t s, const uint32_t* M, uint64_t R, const uint32_t* ec_val,
+               const std::function<const uint32_t*(int)>& ec_off_of, uint64_t* blk, bool count_only,
+               DeepOut& acc) {
+    gps_ctx* c = ch.c;
+    const JoinStepPlan& st = q->steps[s];
+    const uint32_t w = (uint32_t)s + 1;
+    const bool last = s + 1 == q->steps.size();
+    const uint32_t G = (uint32_t)c->nsm * 4;
+    if (R == 0) return;
+    DevPtr jt(c, sizeof(unsigned long long));
+    JoinJob j{};
+    j.row0 = 0;
+    j.M = M;
+    j.Bx = ch.Bp(*q, st.key);
+    j.rpx = ch.rpp(*q, st.key);
+    j.ec_off = ec_off_of(q->ecjob[st.arc][st.key_dir]);
+    j.total = jt.as<unsigned long long>();
+    j.x_col = (uint32_t)q->col_of[st.key];
+    std::vector<CloseChk> cl;
+    for (int ci : st.closing) cl.push_back(make_close(ch, *q, ci, st.nv, ec_off_of));
+    j.nclose = (uint32_t)cl.size();
+    j.final_ = last ? 1u : 0u;
+    j.nowrite = (last && count_only) ? 1u : 0u;
+    if (last) {
+        for (uint32_t col = 0; col < w; col++) j.perm[col] = q->vert_of_col[col];
+        j.perm[w] = (uint8_t)st.nv;
+    }
+    for (uint32_t col = 0; col <= w && col < kJoinStageCols; col++)
+        j.perm_packed |= (last ? (uint32_t)j.perm[col] : col) << (4 * col);
+    DevPtr s0(c, sizeof(uint32_t) * (R + 1));
+    DevPtr poff(c, sizeof(uint64_t) * (R + 1));
+    JoinStep js{};
+    js.w = w;
+    js.wout = w + 1;
+    js.R = R;
+    js.jobs = upload(c, std::vector<JoinJob>{j}, ch.keep);
+    js.nj = 1;
+    js.cl = cl.empty() ? nullptr : upload(c, cl, ch.keep);
+    js.ec_val = ec_val;
+    js.s0 = s0.as<uint32_t>();
+    js.poff = poff.as<uint64_t>();
+    js.ctl = PassCtl{blk, c->d_done, c->d_info};
+    run_join_seg(c, js);
+    const uint64_t P = d2h_u64(c, js.poff + R, 1)[0];
+    if (P == 0) return;
+    const int nv = st.nv;
+    // one pair range: count -> (split if over budget) -> write -> descend
+    std::function<void(uint64_t, uint64_t)> range = [&](uint64_t lo, uint64_t hi) {
+        GPS_CK(cudaMemsetAsync(jt.p, 0, sizeof(unsigned long long), c->stream));
+        js.plo = lo;
+        js.phi = hi;
+        run_join_count(c, js, G);
+        const uint64_t valid = d2h_u64(c, (const uint64_t*)j.total, 1)[0];
+        const uint64_t writes = d2h_u64(c, c->d_info + 1, 1)[0];
+        c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * (double)(hi - lo);
+        if (last && count_only) {
+            acc.count += valid;
+            return;
+        }
+        if (writes == 0) return;
+        const double bytes = 4.0 * (w + 1) * (double)writes;
+        const uint64_t budget = step_budget(ch.budget_opt);
+        const bool final_rows = last;   // the final rows are the result: never split for the budget
+        if (!final_rows && bytes > (double)budget && hi - lo > 1) {
+            const uint64_t parts = std::min<uint64_t>(hi - lo, (uint64_t)(bytes / (double)budget) + 1);
+            for (uint64_t t = 0; t < parts; t++) {
+                uint64_t a, b;
+                pairs_range_host(hi - lo, (uint32_t)t, (uint32_t)parts, a, b);
+                if (b > a) range(lo + a, lo + b);
+            }
+            return;
+        }
+        Block ob;
+        try {
+            ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
+        } catch (const Error& e) {
+            if (e.status != GPS_ENOMEM || final_rows || hi - lo < 2) throw;
+            const uint64_t mid = lo + (hi - lo) / 2;   // the table does not fit now: halve it
+            range(lo, mid);
+            range(mid, hi);
+            return;
+        }
+        // the count pass left this range's per-block offsets in blk: the write pass uses them
+        GPS_CK(cudaMemsetAsync(jt.p, 0, sizeof(unsigned long long), c->stream));
+        js.out = static_cast<uint32_t*>(ob->p);
+        run_join_write(c, js, G);
+        c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * (double)(hi - lo) + 4.0 * (w + 1) * (double)writes;
+        if (last) {
+            acc.pieces.emplace_back(ob, writes);
+            return;
+        }
+        c->stats.join_rows_max = std::max<uint64_t>(c->stats.join_rows_max, writes);
+        c->stats.join_rows_total += writes;
+        q->col_of[nv] = (int)w;
+        q->vert_of_col[w] = (uint8_t)nv;
+        join_deep(ch, q, s + 1, static_cast<const uint32_t*>(ob->p), writes, ec_val, ec_off_of, blk, count_only,
+                  acc);
+    };
+    range(0, P);
+}
+
+// Finish a query with join_deep from step s (its input table q->M, q->R).
+void finish_deep(Chunk& ch, QS* q, size_t s, const uint32_t* ec_val,
+                 const std::function<const uint32_t*(int)>& ec_off_of, uint64_t* blk, bool count_only,
+                 QueryResult& r) {
+    gps_ctx* c = ch.c;
+    DeepOut acc;
+    join_deep(ch, q, s, q->M, q->R, ec_val, ec_off_of, blk, count_only, acc);
+    q->live = false;
+    if (count_only) {
+        r.rows = acc.count;
+        return;
+    }
+    uint64_t total = 0;
+    for (auto& pc : acc.pieces) total += pc.second;
+    r.rows = total;
+    if (total == 0) return;
+    if (acc.pieces.size() == 1) {
+        r.block = acc.pieces[0].first;
+    } else {
+        const size_t k = (size_t)q->k;
+        if (total > (~0ull) / (4ull * k)) fail(GPS_EOVERFLOW, "result size overflows");
+        r.block = make_block(c, sizeof(uint32_t) * total * k);   // GPS_ENOMEM: the final rows do not fit
+        uint64_t at = 0;
+        for (auto& pc : acc.pieces) {
+            GPS_CK(cudaMemcpyAsync(static_cast<uint32_t*>(r.block->p) + at * k, pc.first->p,
+                                   sizeof(uint32_t) * pc.second * k, cudaMemcpyDeviceToDevice, c->stream));
+            at += pc.second;
+        }
+        acc.pieces.clear();
+    }
+    r.data = static_cast<const uint32_t*>(r.block->p);
+}
+
+// deferred: queries of this chunk whose candidate-edge tables do not fit next to the others'
+// (32-bit value positions / tile numbers); the caller runs them in a later chunk.
 void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count_only, float thr,
-               std::vector<QueryResult>& out) {
+               uint64_t budget_opt, std::vector<QueryResult>& out, std::vector<QS*>& deferred) {
     Trace tr("gps chunk", qsv.size());
     arena_reset(c);   // previous chunks' kernels are complete (their last step synced)
     Chunk ch;
@@ -606,6 +775,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
     ch.g = g;
     ch.qs = qsv;
     ch.rebalance = thr;
+    ch.budget_opt = budget_opt;
     const DevGraph& d = g->d;
     setup_chunk(ch);
     tr.mark("setup (arena)");
@@ -700,6 +870,36 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         kc_off.push_back(kc_total);
         kc_total += (uint64_t)q->C[key] + 1;
     };
+    // the candidate-edge values of the chunk share one array with 32-bit positions and one
+    // 31-bit tile numbering: a query that would push either over its limit waits for a later
+    // chunk (or, first in its chunk, fails alone with GPS_EOVERFLOW)
+    {
+        uint64_t pairs = 0, tiles = 0;
+        bool first = true;
+        for (QS* q : ch.qs) {
+            if (!q->live) continue;
+            uint64_t qp = 0, qt = 0;
+            for (int e = 0; e < q->E; e++) {
+                const QArc& a = q->plan.arcs[e];
+                const uint64_t p0 = q->P[a.a][0], p1 = q->P[a.b][1];
+                qp += p0 + p1;
+                qt += (p0 + kEcPairTile - 1) / kEcPairTile + (p1 + kEcPairTile - 1) / kEcPairTile;
+            }
+            if (pairs + qp >= ec_pair_limit() || tiles + qt > 0x7fffffffull) {
+                q->live = false;
+                if (first) {
+                    out[q->idx].status = GPS_EOVERFLOW;
+                    out[q->idx].error = "more than 2^32 candidate-edge pairs in one query";
+                } else {
+                    deferred.push_back(q);
+                }
+                continue;
+            }
+            first = false;
+            pairs += qp;
+            tiles += qt;
+        }
+    }
     uint64_t both_dirs = 0;   // value capacity: every pair of both directions (upper bound)
     for (QS* q : ch.qs) {
         if (!q->live) continue;
@@ -851,6 +1051,13 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             js.woff = woff.as<uint64_t>();
         }
         run_join_seg(c, js);
+        const uint64_t budget = step_budget(ch.budget_opt);
+        // the step's tables exceed the row budget (or cannot be allocated): every query of the
+        // step finishes depth-first, one pair range at a time (join_deep)
+        auto go_deep = [&]() {
+            for (QS* q : act)
+                finish_deep(ch, q, s, val.as<uint32_t>(), ec_off_of, blk.as<uint64_t>(), count_only, out[q->idx]);
+        };
         Block ob;
         bool single = false;
         if (fast) {
@@ -860,12 +1067,20 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             const uint64_t P0 = d2h_u64(c, js.poff + R, 1)[0];
             // single pass when an output block of P0 rows (an upper bound) is affordable: no
             // count pass; else count -> exact allocation -> write
-            single = !any_write || (double)P0 * 4.0 * (w + 1) <= single_pass_bytes();
+            single = !any_write ||
+                     (double)P0 * 4.0 * (w + 1) <= std::min<double>(single_pass_bytes(), (double)budget);
             if (single) {
                 if (any_write && P0) {
-                    ob = make_block(c, sizeof(uint32_t) * P0 * (w + 1));
-                    js.out = static_cast<uint32_t*>(ob->p);
+                    try {
+                        ob = make_block(c, sizeof(uint32_t) * P0 * (w + 1));
+                    } catch (const Error& e) {
+                        if (e.status != GPS_ENOMEM) throw;
+                        single = false;   // no room for the upper bound: count first
+                    }
+                    if (ob) js.out = static_cast<uint32_t*>(ob->p);
                 }
+            }
+            if (single) {
                 if (P0) run_join_tiles(c, js, P0);
                 else GPS_CK(cudaMemsetAsync(c->d_info, 0, 16, c->stream));
             } else {
@@ -886,13 +1101,29 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             pinned_release(c, h, got);
         }
         tr.mark(fast ? "join step synced (fast)" : single ? "join step synced (single pass)" : "join step synced");
+        if (!single && writes && (double)writes * 4.0 * (w + 1) > (double)budget) {
+            bool fin = true;   // a step whose written rows are all final results is never split
+            for (QS* q : act) fin = fin && s + 1 == q->steps.size();
+            if (!fin) {
+                go_deep();
+                break;
+            }
+        }
         if (single) {
             c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)P + 4.0 * (w + 1) * (double)writes;
         } else {
             if (!fast) c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)P;
             if (writes) {
                 if (writes > (~0ull) / (4ull * (w + 1))) fail(GPS_EOVERFLOW, "result size overflows");
-                ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
+                bool all_final = true;
+                for (QS* q : act) all_final = all_final && s + 1 == q->steps.size();
+                try {
+                    ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
+                } catch (const Error& e) {
+                    if (e.status != GPS_ENOMEM || all_final) throw;
+                    go_deep();
+                    break;
+                }
                 js.out = static_cast<uint32_t*>(ob->p);
                 if (fast) run_join_fast_write(c, js, P);
                 else run_join_write(c, js, G);
@@ -975,7 +1206,11 @@ void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t n
             vtx += (size_t)q->k;
             i++;
         }
-        run_chunk(c, g, chunk, count_only, o.rebalance_threshold, out);
+        std::vector<QS*> deferred;
+        run_chunk(c, g, chunk, count_only, o.rebalance_threshold, o.row_budget_bytes, out, deferred);
+        // a deferred query starts the next chunk (where it is first, so it never defers again)
+        todo.insert(todo.begin() + (std::ptrdiff_t)i, deferred.begin(), deferred.end());
+        for (QS* q : deferred) q->live = true;
     }
     const bool sharded = c->comm && c->comm->world > 1;
     for (uint32_t j = 0; j < nq; j++)

@@ -63,7 +63,7 @@ class QueryDesc(ctypes.Structure):
 class MatchOpts(ctypes.Structure):
     _fields_ = [("refine_rounds", ctypes.c_uint32), ("reverse_refine", ctypes.c_int32),
                 ("lowconn_threshold", ctypes.c_uint32), ("result_on_device", ctypes.c_int32),
-                ("rebalance_threshold", ctypes.c_float)]
+                ("rebalance_threshold", ctypes.c_float), ("row_budget_bytes", ctypes.c_uint64)]
 
 
 class Stats(ctypes.Structure):
@@ -93,6 +93,7 @@ def _load_lib():
         "gps_count": (S, [P, P, P, P, P]),
         "gps_result_info": (S, [P, P, P, P, P]),
         "gps_result_free": (None, [P]),
+        "gps_result_free_after": (None, [P, P]),
         "gps_last_error": (ctypes.c_char_p, []),
         "gps_get_stats": (S, [P, P]),
         "gps_reset_stats": (S, [P]),
@@ -119,7 +120,7 @@ def _load_lib():
 lib = _load_lib()
 EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_graph", "gps_free_graph",
             "gps_graph_info", "gps_match", "gps_match_host", "gps_count", "gps_result_info",
-            "gps_result_free", "gps_last_error", "gps_get_stats", "gps_reset_stats",
+            "gps_result_free", "gps_result_free_after", "gps_last_error", "gps_get_stats", "gps_reset_stats",
             "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates", "gps_match_batch",
             "gps_count_batch", "gps_set_workers", "gps_set_slice", "gps_match_batch_host",
             "gps_result_global_rows", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
@@ -144,7 +145,7 @@ def default_opts(**kw) -> MatchOpts:
 
 def _with_device(o: MatchOpts, on_device: bool) -> MatchOpts:
     return MatchOpts(o.refine_rounds, o.reverse_refine, o.lowconn_threshold, 1 if on_device else 0,
-                     o.rebalance_threshold)
+                     o.rebalance_threshold, o.row_budget_bytes)
 
 
 class _QueryArrays:
@@ -204,11 +205,24 @@ class _DictQuery:
         self.k, self.vlabels, self.bound, self.edges = d["k"], d["vlabels"], d["bound"], d["edges"]
 
 
-class _DeviceRows:
-    """Owner of a device gps_result; exposes __cuda_array_interface__ for torch."""
+def _consumer_stream(device: int):
+    try:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    except Exception:
+        return None
 
-    def __init__(self, res, rows, cols, ptr):
+
+class _DeviceRows:
+    """Owner of a device gps_result; exposes __cuda_array_interface__ for torch.
+
+    Holds the Context (the ctx owns the rows' memory and its stream orders their
+    release), and frees with gps_result_free_after on the torch stream current at
+    release time, so kernels still reading the rows finish before the memory is reused."""
+
+    def __init__(self, res, rows, cols, ptr, ctx=None):
         self._res = res
+        self._ctx = ctx
         self.__cuda_array_interface__ = {"shape": (int(rows), int(cols)), "typestr": "<u4",
                                          "data": (int(ptr), False), "version": 3, "strides": None,
                                          "stream": None}
@@ -216,17 +230,20 @@ class _DeviceRows:
     def __del__(self):
         if self._res and lib is not None:
             try:
-                lib.gps_result_free(self._res)
+                dev = self._ctx.device if self._ctx is not None else 0
+                lib.gps_result_free_after(self._res, _consumer_stream(dev))
             except Exception:
                 pass
             self._res = None
+        self._ctx = None
 
 
 class _HostRows:
     """Owner of a host (pinned) gps_result; exposes __array_interface__ for numpy (zero-copy)."""
 
-    def __init__(self, res, rows, cols, ptr):
+    def __init__(self, res, rows, cols, ptr, ctx=None):
         self._res = res
+        self._ctx = ctx   # the ctx owns the pinned rows
         self.__array_interface__ = {"shape": (int(rows), int(cols)), "typestr": "<u4",
                                     "data": (int(ptr), False), "version": 3}
 
@@ -268,9 +285,10 @@ class BatchResult:
 
     def free(self):
         if self._res is not None and lib is not None:
+            st = _consumer_stream(self.ctx.device)
             for i in range(self.n):
                 if self._res[i]:
-                    lib.gps_result_free(self._res[i])
+                    lib.gps_result_free_after(self._res[i], st)
                     self._res[i] = None
         self._res = None
 
@@ -391,7 +409,7 @@ class Context:
                                    ctypes.byref(ondev)))
         if device:
             import torch
-            holder = _DeviceRows(res, rows.value, cols.value, ptr.value)
+            holder = _DeviceRows(res, rows.value, cols.value, ptr.value, self)
             if rows.value == 0:
                 del holder
                 return torch.empty((0, cols.value), dtype=torch.uint32, device=f"cuda:{self.device}")
@@ -469,9 +487,10 @@ class Context:
                     lib.gps_result_free(ctypes.c_void_p(res[i]))
                     out.append(np.zeros((0, cols.value), np.uint32))
                 else:   # zero-copy view of the library's pinned host rows
-                    out.append(np.asarray(_HostRows(ctypes.c_void_p(res[i]), rows.value, cols.value, ptr.value)))
+                    out.append(np.asarray(_HostRows(ctypes.c_void_p(res[i]), rows.value, cols.value, ptr.value,
+                                                    self)))
                 continue
-            holder = _DeviceRows(ctypes.c_void_p(res[i]), rows.value, cols.value, ptr.value)
+            holder = _DeviceRows(ctypes.c_void_p(res[i]), rows.value, cols.value, ptr.value, self)
             if rows.value == 0:
                 del holder
                 out.append(torch.empty((0, cols.value), dtype=torch.uint32, device=f"cuda:{self.device}"))
@@ -506,13 +525,18 @@ class Context:
                                         None))
         return offs[:n], rows[:n]
 
-    def count_batch(self, graph: Graph, queries, opts: Optional[MatchOpts] = None) -> np.ndarray:
+    def count_batch(self, graph: Graph, queries, opts: Optional[MatchOpts] = None, statuses: bool = False):
+        """Counts of every query (numpy u64).  statuses=True: return (counts, per-query
+        statuses) instead of raising when some queries fail."""
         qas, arr, _qb = self._batch_desc(queries)
         n = len(qas)
         counts = np.zeros(max(n, 1), np.uint64)
-        _check(lib.gps_count_batch(self._h, graph.handle, arr, n,
-                                   ctypes.byref(opts) if opts is not None else None,
-                                   ctypes.c_void_p(counts.ctypes.data), None))
+        st = np.zeros(max(n, 1), np.int32)
+        rc = lib.gps_count_batch(self._h, graph.handle, arr, n, ctypes.byref(opts) if opts is not None else None,
+                                 ctypes.c_void_p(counts.ctypes.data), ctypes.c_void_p(st.ctypes.data))
+        if statuses:
+            return counts[:n], st[:n]
+        _check(rc)
         return counts[:n]
 
     def count(self, graph: Graph, q, opts: Optional[MatchOpts] = None) -> int:

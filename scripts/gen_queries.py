@@ -5,6 +5,15 @@ per BFS expansion, vertex labels kept with prob 0.5 (else '*'), edge labels kept
 accepted iff 10^3 <= #Emb <= 10^6 by the CPU oracle (count with a limit).
 Seeds 2000+i in order; the first 100 accepted are stored with their oracle counts.
 
+cfg3: 8/10/12-vertex CYCLIC queries (all induced arcs among the chosen
+vertices, wildcard edge labels) from the dense hub core, whose intermediate tables are
+large: starting from the fully labelled query, vertex labels are replaced by '*' one
+at a time in a seeded order (a replacement that makes the oracle exceed its limits is
+undone) until the oracle's largest BFS-prefix table (#embeddings of the sub-query
+induced on a BFS prefix, oracle.run levels) reaches 10^7 rows; accepted iff that
+happens with #Emb <= 10^8.  10 queries per size.  Stored with the oracle's count,
+multiset hash and per-depth table sizes.
+
 Usage: python scripts/gen_queries.py cfg2 [n_queries]
 Writes synth/data/<cfg>_queries.json.  Never touches the CUDA path.
 """
@@ -27,7 +36,8 @@ RECIPES = {
     # configs[2]: 8/10/12-vertex CYCLIC queries from the dense hub core (top 1% seeds, highest-degree
     # neighbours first, induced arcs -- one per vertex pair, wildcard edge labels, vertex labels kept)
     "cfg3": dict(cfg=2, k=(8, 10, 12), seed0=3000, induced=True, max_children=2, p_wild_v=0.0,
-                 keep_elabels=False, prefer_hubs=True, top_fraction=0.01, lo=10**2, hi=10**7, n=30),
+                 keep_elabels=False, prefer_hubs=True, top_fraction=0.01, lo=1, hi=10**8, n=30,
+                 dial=True, peak=10**7, work=600_000_000, per_size=10),
     # configs[4]: QA batch -- 3..5 vertices, BFS seed bound as a concept node, induced arcs with
     # relation labels, non-bound vertex labels '*' with p = 0.5; every query accepted
     "cfg5": dict(cfg=2, k=(3, 4, 5), seed0=5000, induced=True, max_children=0, p_wild_v=0.5,
@@ -45,9 +55,35 @@ def _init(cfg):
     oracle.set_work_limit(300_000_000)   # give up on searches that would take minutes
 
 
+def _dial(seed, r, k):
+    """cfg3: wildcard vertex labels one at a time until the oracle's peak table >= r['peak']."""
+    import numpy as np
+    from synth import Query
+    q = bfs_query(_G, k, seed, induced=r["induced"], max_children=r["max_children"], p_wild_v=0.0,
+                  keep_elabels=r.get("keep_elabels", True), prefer_hubs=r.get("prefer_hubs", False),
+                  top_fraction=r.get("top_fraction", 0.1))
+    oracle.set_work_limit(r["work"])
+    perm = np.random.default_rng(seed + 777).permutation(k)
+    vl = list(q.vlabels)
+    t = time.time()
+    for u in perm:
+        trial = list(vl)
+        trial[int(u)] = -1
+        qt = Query(q.k, trial, q.bound, q.edges)
+        res = oracle.run(_OG, qt, threads=1, limit=r["hi"])
+        if res["count"] < 0:
+            continue   # too large for the oracle / over the final bound: keep this label
+        vl = trial
+        if max(res["levels"]) >= r["peak"]:
+            return seed, qt.to_json(), res, time.time() - t
+    return seed, None, None, time.time() - t
+
+
 def _try(args):
     seed, r = args
     k = r["k"] if isinstance(r["k"], int) else r["k"][seed % len(r["k"])]
+    if r.get("dial"):
+        return _dial(seed, r, k)
     q = bfs_query(_G, k, seed, induced=r["induced"], max_children=r["max_children"],
                   p_wild_v=r["p_wild_v"], keep_elabels=r.get("keep_elabels", True),
                   prefer_hubs=r.get("prefer_hubs", False), top_fraction=r.get("top_fraction", 0.1),
@@ -63,12 +99,38 @@ def main():
     want = int(sys.argv[2]) if len(sys.argv) > 2 else r["n"]
     out = []
     seed = r["seed0"]
+    if r.get("dial"):   # seeds in order, evaluated in parallel; the first per_size accepted per size
+        with mp.Pool(min(8, os.cpu_count() or 1), initializer=_init, initargs=(r["cfg"],)) as pool:
+            it = pool.imap(_try, ((s, r) for s in range(seed, seed + 100000)), chunksize=1)
+            for s, qj, c, dt in it:
+                if qj is not None and sum(1 for x in out if x["query"]["k"] == qj["k"]) < r["per_size"]:
+                    out.append({"seed": s, "query": qj, "oracle_count": c["count"], "oracle_hash": str(c["hash"]),
+                                "oracle_levels": c["levels"], "oracle_order": c["order"],
+                                "oracle_seconds_1thread": round(dt, 2)})
+                    print(f"  accept seed {s} k={qj['k']} count={c['count']} peak={max(c['levels'])} "
+                          f"({dt:.0f} s)", flush=True)
+                elif s % 8 == 0:
+                    print(f"  seed {s}: accepted {len(out)}", flush=True)
+                if len(out) >= want:
+                    pool.terminate()
+                    break
     with mp.Pool(min(8, os.cpu_count() or 1), initializer=_init, initargs=(r["cfg"],)) as pool:
         while len(out) < want:
-            step = 32 if want <= 1000 else 2048
+            step = 8 if r.get("dial") else (32 if want <= 1000 else 2048)
             batch = [(s, r) for s in range(seed, seed + step)]
             seed += step
             for s, qj, c, dt in pool.map(_try, batch):
+                if r.get("dial"):
+                    if qj is None:
+                        continue
+                    kk = qj["k"]
+                    if sum(1 for x in out if x["query"]["k"] == kk) >= r["per_size"]:
+                        continue
+                    out.append({"seed": s, "query": qj, "oracle_count": c["count"], "oracle_hash": str(c["hash"]),
+                                "oracle_levels": c["levels"], "oracle_order": c["order"],
+                                "oracle_seconds_1thread": round(dt, 2)})
+                    print(f"  accept seed {s} k={kk} count={c['count']} peak={max(c['levels'])}", flush=True)
+                    continue
                 if r["lo"] <= c <= r["hi"] and len(out) < want:
                     out.append({"seed": s, "query": qj, "oracle_count": c})
             print(f"tried up to seed {seed}, accepted {len(out)}", flush=True)

@@ -129,7 +129,8 @@ def _skeleton(g: DataGraph) -> _Skeleton:
 def bfs_query(g: DataGraph, k: int, seed: int, induced: bool = False,
               keep_vlabels: bool = True, keep_elabels: bool = True,
               p_wild_v: float = 0.0, bind_seed: bool = False,
-              top_fraction: float = 0.1, max_children: int = 0, prefer_hubs: bool = False) -> Query:
+              top_fraction: float = 0.1, max_children: int = 0, prefer_hubs: bool = False,
+              max_extra: int = -1) -> Query:
     """BFS-extracted query ("picking a node ... following breadth-first
     search ... nodes in the dense area").
 
@@ -185,6 +186,22 @@ def bfs_query(g: DataGraph, k: int, seed: int, induced: bool = False,
         sel = np.zeros(g.n, bool)
         sel[chosen] = True
         arcs = np.nonzero(sel[sk.s] & sel[sk.d] & (sk.s != sk.d))[0].tolist()
+        if max_extra >= 0:
+            tset = set(int(a) for a in tree)
+            tpairs = {(min(int(sk.s[a]), int(sk.d[a])), max(int(sk.s[a]), int(sk.d[a]))) for a in tree}
+            extra = [a for a in arcs if a not in tset and
+                     (min(int(sk.s[a]), int(sk.d[a])), max(int(sk.s[a]), int(sk.d[a]))) not in tpairs]
+            extra = [extra[i] for i in rng.permutation(len(extra))]
+            chosen_extra, epairs = [], set()
+            for a in extra:
+                pk = (min(int(sk.s[a]), int(sk.d[a])), max(int(sk.s[a]), int(sk.d[a])))
+                if pk in epairs:
+                    continue
+                epairs.add(pk)
+                chosen_extra.append(a)
+                if len(chosen_extra) >= max_extra:
+                    break
+            arcs = [int(a) for a in tree] + chosen_extra
     else:
         arcs = tree
     edges = []

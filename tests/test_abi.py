@@ -46,14 +46,38 @@ def test_library_exports_every_declared_symbol(gps):
     assert sorted(gps.EXPORTED) == _declared()
 
 
+def _c_layouts():
+    """sizeof / offsetof of the header's structs, as gcc lays them out (x86-64 SysV)."""
+    import subprocess
+    import tempfile
+    structs = {"gps_ctx_opts": "CtxOpts", "gps_csr_desc": "CsrDesc", "gps_qedge": "QEdge",
+               "gps_query": "QueryDesc", "gps_match_opts": "MatchOpts", "gps_stats": "Stats"}
+    import paper_1807_08804_b200.gpsense as g
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "gpsense.h"', "int main(void) {"]
+    for cs, py in structs.items():
+        lines.append(f'printf("{cs} size %zu\\n", sizeof({cs}));')
+        for f, _ in getattr(g, py)._fields_:
+            lines.append(f'printf("{cs} {f} %zu\\n", offsetof({cs}, {f}));')
+    lines.append("return 0; }")
+    d = tempfile.mkdtemp()
+    src, exe = os.path.join(d, "l.c"), os.path.join(d, "l")
+    open(src, "w").write("\n".join(lines))
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), src, "-o", exe])
+    out = {}
+    for ln in subprocess.check_output([exe], text=True).splitlines():
+        a, b, c = ln.split()
+        out[(a, b)] = int(c)
+    return structs, out
+
+
 def test_struct_layouts(gps):
-    # offsets/sizes of the C structs as laid out by the x86-64 SysV ABI
-    assert ctypes.sizeof(gps.CtxOpts) == 32
-    assert ctypes.sizeof(gps.CsrDesc) == 56
-    assert ctypes.sizeof(gps.QEdge) == 12
-    assert ctypes.sizeof(gps.QueryDesc) == 32
-    assert ctypes.sizeof(gps.MatchOpts) == 20
-    assert ctypes.sizeof(gps.Stats) == 32 + 4 * 8 * gps.NK + 16
+    """Every ctypes struct of the binding has the header's size and field offsets."""
+    structs, c = _c_layouts()
+    for cs, py in structs.items():
+        st = getattr(gps, py)
+        assert ctypes.sizeof(st) == c[(cs, "size")], cs
+        for f, _ in st._fields_:
+            assert getattr(st, f).offset == c[(cs, f)], (cs, f)
 
 
 def test_default_opts(gps):
