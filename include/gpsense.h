@@ -71,7 +71,8 @@ typedef struct {
     void* stream;            /* cudaStream_t to run on (e.g. torch.cuda.current_stream().cuda_stream);
                                 NULL = the library creates its own non-blocking stream */
     void* nccl_comm;         /* ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()) for the row-sharded
-                                join; NULL / world <= 1 = single GPU */
+                                join; NULL = single GPU.  world = 1 with a communicator
+                                runs the sharded path (and its collectives) on one rank */
     int rank, world;         /* this process's rank and the number of ranks of nccl_comm */
 } gps_ctx_opts;
 
@@ -198,6 +199,24 @@ GPS_API gps_status gps_set_slice(gps_ctx* ctx, uint32_t queries);
  * GLOBAL count on every rank; gps_match returns this rank's shard (shards in rank
  * order = the global result); gps_result_global_rows gives the global size. */
 GPS_API gps_status gps_result_global_rows(const gps_result* r, uint64_t* global_rows);
+
+/* Host arithmetic of the row-sharded join (no device work; identical on every rank,
+ * exposed so multi-process tests can check it without GPUs).  Rank order is the
+ * global row order; rank t's global share of a step's P pairs is
+ * [t*P/world, (t+1)*P/world) (remainder to the first ranks).
+ *   gps_shard_plan: pairs_all[world] = every rank's local pairs (all-gathered);
+ *     local_targets[world+1] = where rank t's share starts in THIS rank's local pair
+ *     space, clamped to [0, pairs_all[rank] + 1]: local row i goes to the rank t with
+ *     local_targets[t] <= poff[i] < local_targets[t+1] (poff = the rows' exclusive
+ *     pair offsets; the last rank also takes rows at the very end); *rebalance = 1 when
+ *     max/mean > threshold; *total = global pairs.
+ *   gps_shard_recv: send_matrix[src*world + dst] = rows src sends to dst
+ *     (all-gathered); at[world] = row offset of src's block in this rank's receive
+ *     buffer (blocks in source-rank order); *total = rows received.
+ * Errors: GPS_EINVAL (world < 1, rank outside [0, world), NULL input). */
+GPS_API gps_status gps_shard_plan(int world, int rank, const uint64_t* pairs_all, float threshold,
+                                  uint64_t* local_targets, int* rebalance, uint64_t* total);
+GPS_API gps_status gps_shard_recv(int world, int rank, const uint64_t* send_matrix, uint64_t* at, uint64_t* total);
 
 /* In-process ranks on one device (threads sharing a hub): the same sharded path
  * with device-to-device copies instead of NCCL -- used to test sharding and

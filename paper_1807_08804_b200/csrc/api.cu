@@ -124,7 +124,7 @@ static void drop_workers(gps_ctx* c) {
 // (on_fail(lo, cnt, status)); the other slices are unaffected.
 static void run_sliced(gps_ctx* c, uint32_t nq, const std::function<void(gps_ctx*, uint32_t, uint32_t)>& body,
                        const std::function<void(uint32_t, uint32_t, gps_status)>& on_fail) {
-    if (c->comm && c->comm->world > 1) {   // SPMD ranks: every rank walks the batch in the same order
+    if (c->comm) {   // SPMD ranks: every rank walks the batch in the same order
         body(c, 0, nq);
         return;
     }
@@ -199,8 +199,9 @@ gps_status gps_create(const gps_ctx_opts* opts, gps_ctx** out) {
     return guarded([&] {
         if (!out) fail(GPS_EINVAL, "null out");
         int dev = opts ? opts->device : 0;
-        if (opts && opts->world > 1 && (opts->rank < 0 || opts->rank >= opts->world || !opts->nccl_comm))
-            fail(GPS_EINVAL, "world > 1 needs an nccl_comm and 0 <= rank < world");
+        if (opts && opts->world > 1 && !opts->nccl_comm) fail(GPS_EINVAL, "world > 1 needs an nccl_comm");
+        if (opts && opts->nccl_comm && (opts->world < 1 || opts->rank < 0 || opts->rank >= opts->world))
+            fail(GPS_EINVAL, "an nccl_comm needs world >= 1 and 0 <= rank < world");
         int ndev = 0;
         GPS_CK(cudaGetDeviceCount(&ndev));
         if (dev < 0 || dev >= ndev) fail(GPS_EINVAL, "bad device ordinal");
@@ -208,7 +209,7 @@ gps_status gps_create(const gps_ctx_opts* opts, gps_ctx** out) {
         gps_ctx* c = new gps_ctx();
         try {
             ctx_init(c, dev, opts ? (cudaStream_t)opts->stream : nullptr);
-            if (opts && opts->world > 1) c->comm = make_nccl_comm(opts->nccl_comm, opts->rank, opts->world);
+            if (opts && opts->nccl_comm) c->comm = make_nccl_comm(opts->nccl_comm, opts->rank, opts->world);
         } catch (...) {
             delete c;
             throw;
@@ -232,6 +233,26 @@ gps_status gps_result_global_rows(const gps_result* r, uint64_t* g) {
     if (!r || !g) return GPS_EINVAL;
     *g = r->global_rows;
     return GPS_OK;
+}
+
+gps_status gps_shard_plan(int world, int rank, const uint64_t* pairs_all, float threshold,
+                          uint64_t* local_targets, int* rebalance, uint64_t* total) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world || !pairs_all) fail(GPS_EINVAL, "bad shard plan arguments");
+        const ShardPlan sp = shard_plan(world, rank, pairs_all, threshold);
+        if (local_targets) std::copy(sp.local_targets.begin(), sp.local_targets.end(), local_targets);
+        if (rebalance) *rebalance = sp.rebalance ? 1 : 0;
+        if (total) *total = sp.total;
+    });
+}
+
+gps_status gps_shard_recv(int world, int rank, const uint64_t* send_matrix, uint64_t* at, uint64_t* total) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world || !send_matrix) fail(GPS_EINVAL, "bad shard recv arguments");
+        const ShardRecv r = shard_recv(world, rank, send_matrix);
+        if (at) std::copy(r.at.begin(), r.at.end(), at);
+        if (total) *total = r.total;
+    });
 }
 
 gps_status gps_local_comm_create(int world, gps_local_comm** out) {

@@ -1,6 +1,7 @@
 // comm.cu -- NCCL and in-process backends of the row-sharded join's collectives.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <string>
 
 #include "comm.h"
@@ -77,6 +78,40 @@ Comm* make_nccl_comm(void* c, int rank, int world) {
     x->rank = rank;
     x->world = world;
     return x;
+}
+
+// ------------------------------------------------------- shard arithmetic
+ShardPlan shard_plan(int world, int rank, const uint64_t* Pall, float thr) {
+    ShardPlan sp;
+    uint64_t S = 0, mx = 0;
+    for (int t = 0; t < world; t++) {
+        if (t < rank) S += Pall[t];
+        sp.total += Pall[t];
+        mx = std::max(mx, Pall[t]);
+    }
+    const double mean = (double)sp.total / world;
+    sp.rebalance = sp.total > 0 && (double)mx > (double)thr * mean;
+    sp.local_targets.resize(world + 1);
+    const uint64_t q = sp.total / world, rem = sp.total % world;
+    for (int t = 0; t <= world; t++) {
+        // global start of rank t's share = pairs_range(total, t, world).lo (t = world: total)
+        const uint64_t T = t == world ? sp.total : q * t + ((uint64_t)t < rem ? (uint64_t)t : rem);
+        // rows are assigned by their GLOBAL first pair g = S + poff[i] (T_t <= g < T_{t+1}, the
+        // last rank also takes g = total), so every rank cuts consistently; a share starting past
+        // this rank's pairs maps to pairs + 1 (no local row reaches it)
+        sp.local_targets[t] = T <= S ? 0 : std::min<uint64_t>(T - S, Pall[rank] + 1);
+    }
+    return sp;
+}
+
+ShardRecv shard_recv(int world, int rank, const uint64_t* send) {
+    ShardRecv r;
+    r.at.resize(world);
+    for (int src = 0; src < world; src++) {
+        r.at[src] = r.total;
+        r.total += send[(size_t)src * world + rank];
+    }
+    return r;
 }
 
 // ----------------------------------------------------------- in-process

@@ -35,6 +35,24 @@ struct Comm {
 
 Comm* make_nccl_comm(void* nccl_comm, int rank, int world);
 
+// Host arithmetic of the row-sharded join; pure functions of the
+// all-gathered counts, identical on every rank.
+struct ShardPlan {
+    bool rebalance = false;                 // max/mean pairs per rank > threshold
+    uint64_t total = 0;                     // global pairs of the step
+    std::vector<uint64_t> local_targets;    // [world+1]: rank t takes the local rows i with
+                                            // local_targets[t] <= poff[i] < local_targets[t+1]
+                                            // (clamped to [0, local pairs + 1])
+};
+// pairs_all[t] = rank t's local pairs; rank order is the global order.
+ShardPlan shard_plan(int world, int rank, const uint64_t* pairs_all, float threshold);
+struct ShardRecv {
+    std::vector<uint64_t> at;               // [world]: row offset of source t's block in the receive buffer
+    uint64_t total = 0;                     // rows received (own block included)
+};
+// send[src * world + dst] = rows src sends to dst (all-gathered matrix).
+ShardRecv shard_recv(int world, int rank, const uint64_t* send);
+
 // Shared state of in-process ranks.
 struct LocalHub {
     int world;

@@ -111,7 +111,7 @@ struct gps_ctx {
     gps::WorkerPool* pool = nullptr;
     uint32_t nworkers_req = 0;               // 0 = default (2)
     uint32_t slice = 0;                      // queries per worker hand-out (0 = default 64)
-    gps::Comm* comm = nullptr;               // row-sharded join across ranks (world > 1)
+    gps::Comm* comm = nullptr;               // row-sharded join across the ranks of a communicator
     // the previous run's filter-state arena, reused by the next run when large enough and no
     // result holds it (saves an allocation per batch slice)
     std::shared_ptr<gps::DevBlock> arena_cache;

@@ -822,33 +822,23 @@ static void allow_join_smem() {
     allow_smem((const void*)k_join_v, (int)join_v_smem(kMaxJobsPerLaunch, kStageW));
 }
 
-__global__ void k_rows_for_ranges(const uint64_t* __restrict__ poff, uint64_t R, const uint64_t* __restrict__ lohi,
-                                  uint32_t n, uint64_t* __restrict__ rows) {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const uint64_t lo = lohi[2 * t], hi = lohi[2 * t + 1];
-    if (lo >= hi || R == 0) {
-        rows[3 * t] = rows[3 * t + 1] = rows[3 * t + 2] = 0;
-        return;
+// out[i] = first j in [0, R] with poff[j] >= t[i] (poff non-decreasing, R+1 entries): the
+// row cuts of the row-sharded join (whole rows per rank).
+__global__ void k_lower_bound(const uint64_t* __restrict__ poff, uint64_t R, const uint64_t* __restrict__ t,
+                              uint32_t n, uint64_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t x = t[i];
+    uint64_t lo = 0, hi = R + 1;   // answer in [lo, hi)
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (poff[mid] < x) lo = mid + 1; else hi = mid;
     }
-    // i0 = largest row with poff[i0] <= lo; i1 = 1 + largest row with poff[i] <= hi - 1
-    auto find = [&](uint64_t p) {
-        uint64_t a = 0, b = R;
-        while (b - a > 1) {
-            uint64_t m = a + (b - a) / 2;
-            if (poff[m] <= p) a = m; else b = m;
-        }
-        return a;
-    };
-    const uint64_t i0 = find(lo);
-    rows[3 * t] = i0;
-    rows[3 * t + 1] = find(hi - 1) + 1;
-    rows[3 * t + 2] = poff[i0];
+    out[i] = lo > R ? R : lo;
 }
 
-void run_rows_for_ranges(gps_ctx* c, const uint64_t* poff, uint64_t R, const uint64_t* d_lohi, uint32_t n,
-                         uint64_t* d_rows) {
-    launch(c, GPS_K_JOIN_LEN, dim3((n + 63) / 64), dim3(64), 0, k_rows_for_ranges, poff, R, d_lohi, n, d_rows);
+void run_lower_bound(gps_ctx* c, const uint64_t* poff, uint64_t R, const uint64_t* d_t, uint32_t n, uint64_t* d_out) {
+    launch(c, GPS_K_JOIN_LEN, dim3((n + 63) / 64), dim3(64), 0, k_lower_bound, poff, R, d_t, n, d_out);
 }
 
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G) {

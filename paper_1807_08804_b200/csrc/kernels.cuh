@@ -170,11 +170,8 @@ struct JoinStep {
     uint32_t* imask = nullptr;
     uint64_t* woff = nullptr;
 };
-// Row-sharded join: for each target pair range [lo[t], hi[t]) of the local pair
-// space (poff[0..R]), the local row range [i0, i1) covering it and poff[i0]
-// (rows[3t .. 3t+2]).
-void run_rows_for_ranges(gps_ctx* c, const uint64_t* poff, uint64_t R, const uint64_t* d_lohi, uint32_t n,
-                         uint64_t* d_rows);
+// Row-sharded join: d_out[i] = first row j in [0, R] with poff[j] >= d_t[i] (row cuts).
+void run_lower_bound(gps_ctx* c, const uint64_t* poff, uint64_t R, const uint64_t* d_t, uint32_t n, uint64_t* d_out);
 void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (+ imask / aoff / woff / jobs[].total if fast)
 // fast steps: write pass over all P pairs (rows of count-only jobs are skipped)
 void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint64_t P);

@@ -439,185 +439,6 @@ CloseChk make_close(const Chunk& ch, const QS& q, int ci, int nv,
     return x;
 }
 
-// Row-sharded join of ONE query across the ranks of c->comm.  The
-// seed table is replicated, so its pair space is split evenly by pair index.  From
-// then on every rank extends its own rows; each step all-gathers the per-rank pair
-// counts and, when max/mean exceeds the threshold, moves rows so that rank r owns
-// the rows of the global pair range [r*P/N, (r+1)*P/N) (rows at a boundary are
-// sent to both sides; each side processes only its pair sub-range).  Global pair
-// order = rank order, so the shards in rank order are the global result.
-void join_sharded(Chunk& ch, QS* q, const uint32_t* ec_val, const std::function<const uint32_t*(int)>& ec_off_of,
-                  uint64_t* blk, bool count_only, float thr, QueryResult& r) {
-    gps_ctx* c = ch.c;
-    Comm* cm = c->comm;
-    const int N = cm->world, me = cm->rank;
-    const uint32_t G = (uint32_t)c->nsm * 4;
-    DevPtr coll(c, sizeof(uint64_t) * (4 * (size_t)N * N + 8 * N + 16));
-    uint64_t* d_send = coll.as<uint64_t>();
-    uint64_t* d_all = d_send + 4 * N;
-    Block cur;
-    const uint32_t* M = q->M;
-    uint64_t R = q->R;
-    bool replicated = true;
-    for (size_t s = 0; s < q->steps.size(); s++) {
-        const JoinStepPlan& st = q->steps[s];
-        const uint32_t w = (uint32_t)s + 1;
-        const bool last = s + 1 == q->steps.size();
-        DevPtr jt(c, sizeof(unsigned long long));
-        GPS_CK(cudaMemsetAsync(jt.p, 0, sizeof(unsigned long long), c->stream));
-        JoinJob j{};
-        j.row0 = 0;
-        j.Bx = ch.Bp(*q, st.key);
-        j.rpx = ch.rpp(*q, st.key);
-        j.ec_off = ec_off_of(q->ecjob[st.arc][st.key_dir]);
-        j.total = jt.as<unsigned long long>();
-        j.x_col = (uint32_t)q->col_of[st.key];
-        std::vector<CloseChk> cl;
-        for (int ci : st.closing) cl.push_back(make_close(ch, *q, ci, st.nv, ec_off_of));
-        j.nclose = (uint32_t)cl.size();
-        j.final_ = last ? 1u : 0u;
-        j.nowrite = (last && count_only) ? 1u : 0u;
-        if (last) {
-            for (uint32_t col = 0; col < w; col++) j.perm[col] = q->vert_of_col[col];
-            j.perm[w] = (uint8_t)st.nv;
-        }
-        JoinStep js{};
-        js.w = w;
-        js.wout = w + 1;
-        js.nj = 1;
-        js.cl = cl.empty() ? nullptr : upload(c, cl, ch.keep);
-        js.ec_val = ec_val;
-        js.ctl = PassCtl{blk, c->d_done, c->d_info};
-        DevPtr s0, poff;
-        auto segment = [&]() {   // s0 / pair offsets of the current local table
-            s0 = DevPtr(c, sizeof(uint32_t) * (R + 1));
-            poff = DevPtr(c, sizeof(uint64_t) * (R + 1));
-            j.M = M;
-            js.R = R;
-            js.jobs = upload(c, std::vector<JoinJob>{j}, ch.keep);
-            js.s0 = s0.as<uint32_t>();
-            js.poff = poff.as<uint64_t>();
-            if (R == 0) GPS_CK(cudaMemsetAsync(poff.p, 0, sizeof(uint64_t), c->stream));
-            else run_join_seg(c, js);
-        };
-        segment();
-        uint64_t lo = 0, hi = 0;
-        if (replicated) {
-            const uint64_t P = d2h_u64(c, js.poff + R, 1)[0];
-            pairs_range_host(P, (uint32_t)me, (uint32_t)N, lo, hi);
-        } else {
-            cm->allgather_u64(js.poff + R, d_all, 1, c->stream);
-            const std::vector<uint64_t> Pall = d2h_u64(c, d_all, N);
-            uint64_t PT = 0, S = 0, mx = 0;
-            for (int t = 0; t < N; t++) {
-                if (t < me) S += Pall[t];
-                PT += Pall[t];
-                mx = std::max(mx, Pall[t]);
-            }
-            const double mean = (double)PT / N;
-            if (PT > 0 && (double)mx > thr * mean) {
-                // ---- rebalance: rows of global pair range T_t go to rank t ----
-                std::vector<uint64_t> lohi(2 * N), T(2 * N);
-                for (int t = 0; t < N; t++) {
-                    pairs_range_host(PT, (uint32_t)t, (uint32_t)N, T[2 * t], T[2 * t + 1]);
-                    const uint64_t a = std::max(T[2 * t], S), b = std::min(T[2 * t + 1], S + Pall[me]);
-                    lohi[2 * t] = a < b ? a - S : 0;
-                    lohi[2 * t + 1] = a < b ? b - S : 0;
-                }
-                DevPtr drows(c, sizeof(uint64_t) * 3 * N);
-                run_rows_for_ranges(c, js.poff, R, upload(c, lohi, ch.keep), (uint32_t)N, drows.as<uint64_t>());
-                const std::vector<uint64_t> rows = d2h_u64(c, drows.as<uint64_t>(), 3 * N);
-                std::vector<uint64_t> sm(2 * N);
-                for (int t = 0; t < N; t++) {
-                    const bool any = lohi[2 * t] < lohi[2 * t + 1];
-                    sm[2 * t] = any ? rows[3 * t + 1] - rows[3 * t] : 0;
-                    sm[2 * t + 1] = any ? S + rows[3 * t + 2] : 0;
-                }
-                const uint64_t* dsm = upload(c, sm, ch.keep);
-                flush_uploads(c);   // a plain copy (not a launch) reads the staged array
-                GPS_CK(cudaMemcpyAsync(d_send, dsm, sizeof(uint64_t) * 2 * N, cudaMemcpyDeviceToDevice, c->stream));
-                cm->allgather_u64(d_send, d_all, 2 * N, c->stream);
-                const std::vector<uint64_t> all = d2h_u64(c, d_all, 2 * (size_t)N * N);
-                uint64_t newR = 0, A = ~0ull;
-                std::vector<uint64_t> at(N);
-                for (int src = 0; src < N; src++) {
-                    at[src] = newR;
-                    const uint64_t n = all[(size_t)src * 2 * N + 2 * me];
-                    if (n && A == ~0ull) A = all[(size_t)src * 2 * N + 2 * me + 1];
-                    newR += n;
-                }
-                Block nb = make_block(c, sizeof(uint32_t) * (newR * w + 1));
-                uint32_t* NBp = static_cast<uint32_t*>(nb->p);
-                std::vector<P2POp> ops;
-                for (int t = 0; t < N; t++) {
-                    const uint64_t nsend = sm[2 * t];
-                    const uint64_t nrecv = all[(size_t)t * 2 * N + 2 * me];
-                    const uint32_t* src = M + rows[3 * t] * w;
-                    if (t == me) {
-                        if (nsend)
-                            GPS_CK(cudaMemcpyAsync(NBp + at[me] * w, src, nsend * w * 4, cudaMemcpyDeviceToDevice,
-                                                   c->stream));
-                        continue;
-                    }
-                    if (nsend || nrecv)
-                        ops.push_back(P2POp{t, src, nsend * w * 4, NBp + at[t] * w, nrecv * w * 4});
-                }
-                cm->exchange(ops, c->stream);
-                cur = nb;
-                M = NBp;
-                R = newR;
-                segment();
-                lo = newR ? T[2 * me] - A : 0;
-                hi = newR ? T[2 * me + 1] - A : 0;
-            } else {
-                lo = 0;
-                hi = Pall[me];
-            }
-        }
-        js.plo = lo;
-        js.phi = hi;
-        run_join_count(c, js, G);
-        const uint64_t local = d2h_u64(c, (const uint64_t*)j.total, 1)[0];
-        const uint64_t writes = d2h_u64(c, c->d_info + 1, 1)[0];
-        GPS_CK(cudaMemcpyAsync(d_send, j.total, sizeof(uint64_t), cudaMemcpyDeviceToDevice, c->stream));
-        cm->allgather_u64(d_send, d_all, 1, c->stream);
-        const std::vector<uint64_t> totals = d2h_u64(c, d_all, N);
-        uint64_t global = 0;
-        for (uint64_t t : totals) global += t;
-        c->stats.k_bytes[GPS_K_JOIN_COUNT] += 4.0 * w * (double)R + 4.0 * (double)(hi - lo);
-        if (global == 0) {
-            r.rows = 0;
-            r.global_rows = 0;
-            return;
-        }
-        Block ob;
-        if (writes) {
-            ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
-            js.out = static_cast<uint32_t*>(ob->p);
-            run_join_write(c, js, G);
-            c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)(hi - lo) +
-                                                  4.0 * (w + 1) * (double)writes;
-        }
-        if (last) {
-            r.rows = local;
-            r.global_rows = global;
-            if (writes) {
-                r.block = ob;
-                r.data = static_cast<const uint32_t*>(ob->p);
-            }
-            return;
-        }
-        M = writes ? static_cast<const uint32_t*>(ob->p) : nullptr;
-        R = writes;
-        cur = ob;
-        replicated = false;
-        q->col_of[st.nv] = (int)w;
-        q->vert_of_col[w] = (uint8_t)st.nv;
-        c->stats.join_rows_max = std::max<uint64_t>(c->stats.join_rows_max, global);
-        c->stats.join_rows_total += local;
-    }
-}
-
 // Depth-first join of ONE query from step s on (reading R27): the step's
 // pair space is cut into ranges whose output fits the row budget; each range is
 // counted, written and carried through the remaining steps before the next range
@@ -829,7 +650,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         if (q->k == 1) {   // single-vertex query: the candidate set is the answer (reading R11)
             r.rows = q->C[0];
             r.global_rows = r.rows;
-            if (c->comm && c->comm->world > 1 && c->comm->rank != 0) r.rows = 0;   // one shard holds it
+            if (c->comm && c->comm->rank != 0) r.rows = 0;   // one shard holds it
             if (!count_only) {
                 r.block = make_block(c, (size_t)r.rows * 4);
                 GPS_CK(cudaMemcpyAsync(r.block->p, q->carr[0], (size_t)r.rows * 4, cudaMemcpyDeviceToDevice,
@@ -977,15 +798,12 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         q->M = q->carr[s0.key];
         q->R = q->C[s0.key];
     }
-    if (c->comm && c->comm->world > 1) {
-        for (QS* q : ch.qs) {
-            if (!q->live) continue;
-            join_sharded(ch, q, val.as<uint32_t>(), ec_off_of, blk.as<uint64_t>(), count_only,
-                         ch.rebalance, out[q->idx]);
-        }
-        return;
-    }
+    Comm* cm = c->comm;   // row-sharded join (one query)
+    DevPtr coll;
+    if (cm) coll = DevPtr(c, sizeof(uint64_t) * (4 * (size_t)cm->world * cm->world + 8 * cm->world + 16));
     Block cur;   // holds the previous step's output while its rows are read
+    Block recv;  // sharded: rows received by a rebalance
+    bool replicated = cm != nullptr;   // sharded: the seed table is the same on every rank
     for (size_t s = 0;; s++) {
         std::vector<QS*> act;
         for (QS* q : ch.qs)
@@ -996,62 +814,141 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         std::vector<CloseChk> cl;
         uint64_t R = 0;
         DevPtr jt(c, sizeof(unsigned long long) * act.size());
-        GPS_CK(cudaMemsetAsync(jt.p, 0, sizeof(unsigned long long) * act.size(), c->stream));
-        for (size_t i = 0; i < act.size(); i++) {
-            QS* q = act[i];
-            const JoinStepPlan& st = q->steps[s];
-            JoinJob j{};
-            j.row0 = R;
-            j.M = q->M;
-            j.Bx = ch.Bp(*q, st.key);
-            j.rpx = ch.rpp(*q, st.key);
-            j.ec_off = ec_off_of(q->ecjob[st.arc][st.key_dir]);
-            j.total = jt.as<unsigned long long>() + i;
-            j.x_col = (uint32_t)q->col_of[st.key];
-            j.close0 = (uint32_t)cl.size();
-            for (int ci : st.closing) cl.push_back(make_close(ch, *q, ci, st.nv, ec_off_of));
-            j.nclose = (uint32_t)st.closing.size();
-            const bool last = s + 1 == q->steps.size();
-            j.final_ = last ? 1u : 0u;
-            j.nowrite = (last && count_only) ? 1u : 0u;
-            if (last) {
-                for (uint32_t col = 0; col < w; col++) j.perm[col] = q->vert_of_col[col];
-                j.perm[w] = (uint8_t)st.nv;
-            }
-            for (uint32_t col = 0; col <= w && col < kJoinStageCols; col++)
-                j.perm_packed |= (last ? (uint32_t)j.perm[col] : col) << (4 * col);
-            jj.push_back(j);
-            R += q->R;
-        }
-        if (jj.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: join job list too long");
-        DevPtr s0(c, sizeof(uint32_t) * (R + 1));
-        DevPtr poff(c, sizeof(uint64_t) * (R + 1));
         JoinStep js{};
-        js.w = w;
-        js.wout = w + 1;
-        js.R = R;
-        js.jobs = upload(c, jj, ch.keep);
-        js.nj = (uint32_t)jj.size();
-        js.cl = cl.empty() ? nullptr : upload(c, cl, ch.keep);
-        js.ec_val = val.as<uint32_t>();
-        js.s0 = s0.as<uint32_t>();
-        js.poff = poff.as<uint64_t>();
-        js.ctl = PassCtl{blk.as<uint64_t>(), c->d_done, c->d_info};
-        bool any_write = false;
-        for (const JoinJob& x : jj) any_write |= !x.nowrite;
-        // closing-free step with narrow rows: the seg pass finds each row's own values in its
-        // segment, which fixes every output position -- no count pass, one sync
-        const bool fast = cl.empty() && w + 1 <= kJoinStageCols && std::getenv("GPS_NO_FAST_JOIN") == nullptr;
-        DevPtr imask, woff;
-        if (fast) {
-            imask = DevPtr(c, sizeof(uint32_t) * (R + 1));
-            woff = DevPtr(c, sizeof(uint64_t) * (R + 1));
-            js.fast = 1;
-            js.imask = imask.as<uint32_t>();
-            js.woff = woff.as<uint64_t>();
+        DevPtr s0, poff, imask, woff;
+        bool any_write = false, fast = false;
+        // job table + seg pass of the queries' current tables (q->M, q->R)
+        auto prepare = [&]() {
+            jj.clear();
+            cl.clear();
+            R = 0;
+            GPS_CK(cudaMemsetAsync(jt.p, 0, sizeof(unsigned long long) * act.size(), c->stream));
+            for (size_t i = 0; i < act.size(); i++) {
+                QS* q = act[i];
+                const JoinStepPlan& st = q->steps[s];
+                JoinJob j{};
+                j.row0 = R;
+                j.M = q->M;
+                j.Bx = ch.Bp(*q, st.key);
+                j.rpx = ch.rpp(*q, st.key);
+                j.ec_off = ec_off_of(q->ecjob[st.arc][st.key_dir]);
+                j.total = jt.as<unsigned long long>() + i;
+                j.x_col = (uint32_t)q->col_of[st.key];
+                j.close0 = (uint32_t)cl.size();
+                for (int ci : st.closing) cl.push_back(make_close(ch, *q, ci, st.nv, ec_off_of));
+                j.nclose = (uint32_t)st.closing.size();
+                const bool last = s + 1 == q->steps.size();
+                j.final_ = last ? 1u : 0u;
+                j.nowrite = (last && count_only) ? 1u : 0u;
+                if (last) {
+                    for (uint32_t col = 0; col < w; col++) j.perm[col] = q->vert_of_col[col];
+                    j.perm[w] = (uint8_t)st.nv;
+                }
+                for (uint32_t col = 0; col <= w && col < kJoinStageCols; col++)
+                    j.perm_packed |= (last ? (uint32_t)j.perm[col] : col) << (4 * col);
+                jj.push_back(j);
+                R += q->R;
+            }
+            if (jj.size() > kMaxJobsPerLaunch) fail(GPS_EINVAL, "internal: join job list too long");
+            s0 = DevPtr(c, sizeof(uint32_t) * (R + 1));
+            poff = DevPtr(c, sizeof(uint64_t) * (R + 1));
+            js = JoinStep{};
+            js.w = w;
+            js.wout = w + 1;
+            js.R = R;
+            js.jobs = upload(c, jj, ch.keep);
+            js.nj = (uint32_t)jj.size();
+            js.cl = cl.empty() ? nullptr : upload(c, cl, ch.keep);
+            js.ec_val = val.as<uint32_t>();
+            js.s0 = s0.as<uint32_t>();
+            js.poff = poff.as<uint64_t>();
+            js.ctl = PassCtl{blk.as<uint64_t>(), c->d_done, c->d_info};
+            any_write = false;
+            for (const JoinJob& x : jj) any_write |= !x.nowrite;
+            // closing-free step with narrow rows: the seg pass finds each row's own values in its
+            // segment, which fixes every output position -- no count pass, one sync
+            fast = cl.empty() && w + 1 <= kJoinStageCols && std::getenv("GPS_NO_FAST_JOIN") == nullptr;
+            imask = DevPtr();
+            woff = DevPtr();
+            if (fast) {
+                imask = DevPtr(c, sizeof(uint32_t) * (R + 1));
+                woff = DevPtr(c, sizeof(uint64_t) * (R + 1));
+                js.fast = 1;
+                js.imask = imask.as<uint32_t>();
+                js.woff = woff.as<uint64_t>();
+            }
+            if (R == 0) {   // a rank's share can be empty: the step's totals are 0
+                GPS_CK(cudaMemsetAsync(poff.p, 0, sizeof(uint64_t), c->stream));
+                if (fast) GPS_CK(cudaMemsetAsync(woff.p, 0, sizeof(uint64_t), c->stream));
+            }
+            run_join_seg(c, js);
+        };
+        prepare();
+        if (cm) {   // ---- row-sharded join: this rank's share of the step ----
+            QS* q = act[0];
+            if (replicated) {
+                // the seed table is replicated: rank r keeps the rows whose first pair lies in
+                // [r*P/N, (r+1)*P/N) (whole rows, so every local path applies unchanged)
+                const uint64_t P = d2h_u64(c, js.poff + R, 1)[0];
+                uint64_t lo, hi;
+                pairs_range_host(P, (uint32_t)cm->rank, (uint32_t)cm->world, lo, hi);
+                const uint64_t tg[2] = {lo, hi};
+                uint64_t* d_cut = coll.as<uint64_t>();
+                run_lower_bound(c, js.poff, R, upload(c, std::vector<uint64_t>(tg, tg + 2), ch.keep), 2, d_cut);
+                const std::vector<uint64_t> cut = d2h_u64(c, d_cut, 2);
+                const uint64_t i0 = cm->rank == 0 ? 0 : cut[0];
+                const uint64_t i1 = cm->rank + 1 == cm->world ? R : cut[1];
+                q->M = q->M + i0 * w;
+                q->R = i1 > i0 ? i1 - i0 : 0;
+                replicated = false;
+                prepare();
+            } else {
+                uint64_t* d_send = coll.as<uint64_t>();
+                uint64_t* d_all = d_send + 4 * cm->world;
+                cm->allgather_u64(js.poff + R, d_all, 1, c->stream);
+                const std::vector<uint64_t> Pall = d2h_u64(c, d_all, cm->world);
+                ShardPlan sp = shard_plan(cm->world, cm->rank, Pall.data(), ch.rebalance);
+                if (sp.rebalance) {
+                    // cut the local rows at the targets' pair boundaries (whole rows), all-gather
+                    // the send counts, then one grouped send/recv; received blocks in source-rank
+                    // order keep the global row order
+                    run_lower_bound(c, js.poff, R, upload(c, sp.local_targets, ch.keep), (uint32_t)cm->world + 1,
+                                    d_send);
+                    std::vector<uint64_t> cuts = d2h_u64(c, d_send, cm->world + 1);
+                    cuts[0] = 0;
+                    cuts[cm->world] = R;
+                    std::vector<uint64_t> cnt(cm->world);
+                    for (int t = 0; t < cm->world; t++) cnt[t] = cuts[t + 1] > cuts[t] ? cuts[t + 1] - cuts[t] : 0;
+                    const uint64_t* dc = upload(c, cnt, ch.keep);
+                    flush_uploads(c);
+                    GPS_CK(cudaMemcpyAsync(d_send, dc, sizeof(uint64_t) * cm->world, cudaMemcpyDeviceToDevice,
+                                           c->stream));
+                    cm->allgather_u64(d_send, d_all, cm->world, c->stream);
+                    const std::vector<uint64_t> mat = d2h_u64(c, d_all, (size_t)cm->world * cm->world);
+                    const ShardRecv rv = shard_recv(cm->world, cm->rank, mat.data());
+                    Block nb = make_block(c, sizeof(uint32_t) * (rv.total * w + 1));
+                    uint32_t* NBp = static_cast<uint32_t*>(nb->p);
+                    std::vector<P2POp> ops;
+                    for (int t = 0; t < cm->world; t++) {
+                        const uint64_t ns = cnt[t], nr = mat[(size_t)t * cm->world + cm->rank];
+                        const uint32_t* src = q->M + cuts[t] * w;
+                        if (t == cm->rank) {
+                            if (ns)
+                                GPS_CK(cudaMemcpyAsync(NBp + rv.at[t] * w, src, ns * w * 4, cudaMemcpyDeviceToDevice,
+                                                       c->stream));
+                            continue;
+                        }
+                        if (ns || nr) ops.push_back(P2POp{t, src, ns * w * 4, NBp + rv.at[t] * w, nr * w * 4});
+                    }
+                    cm->exchange(ops, c->stream);
+                    recv = nb;   // keeps the received rows; the old table (cur) may go
+                    q->M = NBp;
+                    q->R = rv.total;
+                    prepare();
+                }
+            }
         }
-        run_join_seg(c, js);
-        const uint64_t budget = step_budget(ch.budget_opt);
+        const uint64_t budget = cm ? ~0ull : step_budget(ch.budget_opt);   // sharded: no depth-first split
         // the step's tables exceed the row budget (or cannot be allocated): every query of the
         // step finishes depth-first, one pair range at a time (join_deep)
         auto go_deep = [&]() {
@@ -1120,7 +1017,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
                 try {
                     ob = make_block(c, sizeof(uint32_t) * writes * (w + 1));
                 } catch (const Error& e) {
-                    if (e.status != GPS_ENOMEM || all_final) throw;
+                    if (e.status != GPS_ENOMEM || all_final || cm) throw;
                     go_deep();
                     break;
                 }
@@ -1131,28 +1028,41 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
                                                       4.0 * (w + 1) * (double)writes;
             }
         }
+        // sharded: every rank learns the step's global size (one all-gather of the local total)
+        uint64_t global = tot.empty() ? 0 : tot[0];
+        if (cm) {
+            uint64_t* d_send = coll.as<uint64_t>();
+            uint64_t* d_all = d_send + 4 * cm->world;
+            GPS_CK(cudaMemcpyAsync(d_send, jt.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, c->stream));
+            cm->allgather_u64(d_send, d_all, 1, c->stream);
+            global = 0;
+            for (uint64_t x : d2h_u64(c, d_all, cm->world)) global += x;
+        }
         uint64_t off = 0;
         for (size_t i = 0; i < act.size(); i++) {
             QS* q = act[i];
             const JoinStepPlan& st = q->steps[s];
             QueryResult& r = out[q->idx];
             const uint64_t t = tot[i];
+            const uint64_t gt = cm ? global : t;
             const bool last = s + 1 == q->steps.size();
             const bool wrote = !(last && count_only);
             if (last) {
                 r.rows = t;
+                r.global_rows = gt;
                 if (wrote && t) {
                     r.block = ob;
                     r.data = static_cast<const uint32_t*>(ob->p) + off * (w + 1);
                 }
                 q->live = false;
-            } else if (t == 0) {
+            } else if (gt == 0) {
                 r.rows = 0;
+                r.global_rows = 0;
                 q->live = false;
             } else {
-                q->M = static_cast<const uint32_t*>(ob->p) + off * (w + 1);
+                q->M = t ? static_cast<const uint32_t*>(ob->p) + off * (w + 1) : nullptr;
                 q->R = t;
-                c->stats.join_rows_max = std::max<uint64_t>(c->stats.join_rows_max, t);
+                c->stats.join_rows_max = std::max<uint64_t>(c->stats.join_rows_max, gt);
                 c->stats.join_rows_total += t;
                 q->col_of[st.nv] = (int)w;
                 q->vert_of_col[w] = (uint8_t)st.nv;
@@ -1160,6 +1070,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             if (wrote) off += t;
         }
         cur = ob;   // the previous output block is released once no query reads it
+        recv.reset();
     }
 }
 
@@ -1196,7 +1107,7 @@ void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t n
         while (i < todo.size()) {
             QS* q = todo[i];
             size_t b = filter_bytes(*q, g->d.nws);
-            const size_t maxb = (c->comm && c->comm->world > 1) ? 1 : kMaxBatch;   // sharded: one query at a time
+            const size_t maxb = c->comm ? 1 : kMaxBatch;   // sharded: one query at a time
             if (!chunk.empty() && (chunk.size() >= maxb || bytes + b > kChunkBytes ||
                                    ecj + 2 * (size_t)std::max(q->E, 1) > kMaxJobsPerLaunch || vtx + q->k > kMaxJobsPerLaunch))
                 break;
@@ -1212,7 +1123,7 @@ void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t n
         todo.insert(todo.begin() + (std::ptrdiff_t)i, deferred.begin(), deferred.end());
         for (QS* q : deferred) q->live = true;
     }
-    const bool sharded = c->comm && c->comm->world > 1;
+    const bool sharded = c->comm != nullptr;
     for (uint32_t j = 0; j < nq; j++)
         if (out[j].status == GPS_OK) {
             if (!sharded) out[j].global_rows = out[j].rows;

@@ -107,6 +107,8 @@ def _load_lib():
         "gps_match_batch_host": (S, [P, P, P, ctypes.c_uint32, P, P, ctypes.c_uint64, P, P, P]),
         "gps_result_global_rows": (S, [P, P]),
         "gps_local_comm_create": (S, [ctypes.c_int, P]),
+        "gps_shard_plan": (S, [ctypes.c_int, ctypes.c_int, P, ctypes.c_float, P, P, P]),
+        "gps_shard_recv": (S, [ctypes.c_int, ctypes.c_int, P, P, P]),
         "gps_local_comm_destroy": (S, [P]),
         "gps_create_local_rank": (S, [P, P, ctypes.c_int, P]),
     }
@@ -123,7 +125,7 @@ EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_grap
             "gps_result_free", "gps_result_free_after", "gps_last_error", "gps_get_stats", "gps_reset_stats",
             "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates", "gps_match_batch",
             "gps_count_batch", "gps_set_workers", "gps_set_slice", "gps_match_batch_host",
-            "gps_result_global_rows", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
+            "gps_result_global_rows", "gps_shard_plan", "gps_shard_recv", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
 
 
 def _check(st: int):
@@ -321,6 +323,26 @@ class Graph:
             self.free()
         except Exception:
             pass
+
+
+def shard_plan(world: int, rank: int, pairs_all, threshold: float = 1.10):
+    """gps_shard_plan: (local_targets[world+1], rebalance, total)."""
+    p = np.ascontiguousarray(pairs_all, np.uint64)
+    lt = np.zeros(world + 1, np.uint64)
+    rb, tot = ctypes.c_int(), ctypes.c_uint64()
+    _check(lib.gps_shard_plan(int(world), int(rank), ctypes.c_void_p(p.ctypes.data), float(threshold),
+                              ctypes.c_void_p(lt.ctypes.data), ctypes.byref(rb), ctypes.byref(tot)))
+    return lt, bool(rb.value), int(tot.value)
+
+
+def shard_recv(world: int, rank: int, send_matrix):
+    """gps_shard_recv: (at[world], total)."""
+    m = np.ascontiguousarray(send_matrix, np.uint64).reshape(-1)
+    at = np.zeros(world, np.uint64)
+    tot = ctypes.c_uint64()
+    _check(lib.gps_shard_recv(int(world), int(rank), ctypes.c_void_p(m.ctypes.data), ctypes.c_void_p(at.ctypes.data),
+                              ctypes.byref(tot)))
+    return at, int(tot.value)
 
 
 class LocalComm:
