@@ -5,11 +5,15 @@ m = 1,500,000 labelled arcs, synth.config_graph(2), seed 8804) resident in HBM;
 one STEP = gps_match of the 100 stored six-vertex BFS tree queries
 (synth/data/cfg2_queries.json; embeddings stay in device memory).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config C] [--impl reference]
 
-Multi-GPU (torchrun): the graph is replicated, every rank runs its own batch of
-100 queries (weak scaling, no data-path collective); time = max over ranks of
-the device-timed region; value = all ranks' queries / that time.
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without a torchrun environment
+launches one itself).  Configs 2, 3 and 5: the graph is replicated and every rank
+runs its own batch (weak scaling, no data-path collective).  Config 4: every rank
+runs the SAME large cyclic queries and the partial-embedding tables are sharded by
+row across the ranks, with one NCCL all-gather per join step plus row rebalancing
+(strong scaling, SURVEY §8(e)).  Time = max over ranks of the device-timed region;
+value = queries completed / that time.
 """
 from __future__ import annotations
 
@@ -34,7 +38,8 @@ WORKLOADS = {
     3: f"cfg3: {GRAPH}, 30 cyclic 8/10/12-vertex queries (dense hub core) per step, device-resident results",
     5: f"cfg5: {GRAPH}, QA batch of 10000 3-5-vertex queries with a bound concept vertex per step",
     4: "cfg4: Chung-Lu graph n=20000000 m=100000000 labelled arcs (HBM-resident CSR); per step gps_match of "
-       "labelled out-star-2 / in-star-2 / 2-path (2.5e8 rows written) + gps_count of an out-star-3 (3.2e9)",
+       "the stored 6/7/8-vertex cyclic queries (synth/data/cfg4_queries.json, oracle BFS-prefix tables "
+       ">= 1e9 rows), rows sharded over the GPUs",
 }
 CONFIG = 2
 
@@ -42,11 +47,25 @@ CONFIG = 2
 def load_queries(cfg=None):
     from synth import Query
     cfg = CONFIG if cfg is None else cfg
-    if cfg == 4:   # closed-form-pinned large joins (tests/test_gpu_large.py); no stored oracle counts
-        from synth.large import CFG4
-        return [q for _, q, _ in CFG4], [None] * len(CFG4)
     data = json.load(open(os.path.join(ROOT, "synth", "data", f"cfg{cfg}_queries.json")))
     return [Query.from_json(d["query"]) for d in data["queries"]], [d["oracle_count"] for d in data["queries"]]
+
+
+def sample_order(n: int):
+    """A fixed pseudo-random order of the stored queries: CPU samples walk it (rotating by
+    step), so a bounded sample is not biased towards the first queries of the file."""
+    return np.random.default_rng(12345).permutation(n).tolist()
+
+
+def host_cpu() -> dict:
+    model, cores = None, os.cpu_count()
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"model": model, "cpus": cores}
 
 
 # ----------------------------------------------------------------- clocks
@@ -101,35 +120,78 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ reference arm
-def cpu_oracle_sample(graph, queries, budget_s: float):
-    """Time the CPU oracle (as it stands, 1 thread) on a bounded prefix of the query batch."""
+def cpu_oracle_sample(og, queries, order, start: int, budget_s: float, threads: int, max_q: int = 0):
+    """Time the CPU oracle (as it stands: oracle.c, `threads` OpenMP threads) on queries
+    taken from `order` starting at `start` (cyclic) until `budget_s` is used.  Each query is
+    the full enumeration (every embedding visited; count + multiset hash, rows not stored)."""
     from oracle import oracle
-    og = oracle.OracleGraph(graph)
     t0 = time.perf_counter()
     done, emb = 0, 0
-    for q in queries:
-        emb += oracle.match(og, q).shape[0]
+    while done < len(order) and (not max_q or done < max_q):
+        q = queries[order[(start + done) % len(order)]]
+        emb += oracle.run(og, q, threads=threads)["count"]
         done += 1
         if time.perf_counter() - t0 > budget_s:
             break
+    return done, emb, time.perf_counter() - t0
+
+
+def cpu_baseline(g, queries, budget_s: float) -> dict:
+    """Oracle on the host cores in both modes of SURVEY §8(d): 1 thread and all cores."""
+    from oracle import oracle
+    og = oracle.OracleGraph(g)
+    order = sample_order(len(queries))
+    nproc = os.cpu_count() or 1
+    d1, e1, t1 = cpu_oracle_sample(og, queries, order, 0, budget_s / 2, 1)
+    dn, en, tn = cpu_oracle_sample(og, queries, order, 0, budget_s / 2, nproc)
+    return {"value": dn / tn, "unit": "queries/s", "cores": nproc, "kind": "oracle",
+            "sample": f"cfg{CONFIG}: {dn} queries in a fixed seeded order (of {len(queries)}), oracle.c OpenMP "
+                      f"{nproc} threads, {en} embeddings in {tn:.1f} s",
+            "single_thread": {"value": d1 / t1, "cores": 1,
+                              "sample": f"{d1} queries of the same order, {e1} embeddings in {t1:.1f} s"},
+            "host": host_cpu()}
+
+
+def cfg4_cpu_baseline(g, queries, budget_s: float) -> dict:
+    """Config 4: one full oracle enumeration takes minutes, so the bounded sample is a
+    first-column partition (SURVEY §8(d) partitions) of each query in turn: the oracle
+    enumerates the embeddings whose first query vertex maps into [0, n/64); the rate is
+    reported as partitions/s / 64 (query-equivalents/s) with the partition stated."""
+    from oracle import oracle
+    og = oracle.OracleGraph(g)
+    nproc = os.cpu_count() or 1
+    part = 64
+    t0 = time.perf_counter()
+    done, emb = 0, 0
+    while time.perf_counter() - t0 < budget_s:
+        q = queries[done % len(queries)]
+        p = done // len(queries) % part
+        emb += oracle.run(og, q, threads=nproc, col0_range=(p * g.n // part, (p + 1) * g.n // part))["count"]
+        done += 1
     dt = time.perf_counter() - t0
-    return done, emb, dt
+    return {"value": done / part / dt, "unit": "queries/s", "cores": nproc, "kind": "oracle",
+            "sample": f"cfg4: {done} first-column partitions (1/{part} of the data ids each) of the stored "
+                      f"queries, oracle.c OpenMP {nproc} threads, {emb} embeddings in {dt:.1f} s; value = "
+                      f"partitions/s / {part}", "host": host_cpu()}
 
 
 def run_reference(args, rank, world):
     from synth import config_graph
+    from oracle import oracle
     if rank != 0:
         return
     queries, _ = load_queries()
-    g = config_graph(2)
+    g = config_graph(4 if CONFIG == 4 else 2)
+    og = oracle.OracleGraph(g)
+    order = sample_order(len(queries))
     per_step = max(1, args.ref_queries_per_step)
+    nproc = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_oracle_sample(g, queries[:1], 1e9)
+        cpu_oracle_sample(og, queries, order, 0, 0.0, nproc, 1)
     tot_q, tot_e, tot_t = 0, 0, 0.0
     for s in range(args.steps):
-        lo = (s * per_step) % len(queries)
-        qs = (queries[lo:] + queries[:lo])[:per_step]
-        d, e, t = cpu_oracle_sample(g, qs, 1e9)
+        d, e, t = cpu_oracle_sample(og, queries, order, (s * per_step) % len(order), args.ref_step_budget, nproc,
+                                    per_step)
         tot_q += d
         tot_e += e
         tot_t += t
@@ -138,9 +200,12 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic", "embeddings_per_s": tot_e / tot_t,
-            "config": {"workload": WORKLOADS[CONFIG], "sample": f"{per_step} queries per step (of {len(queries)})"},
-            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{tot_q} cfg{CONFIG} queries over {args.steps} steps"},
+            "config": {"workload": WORKLOADS[CONFIG],
+                       "sample": f"per step: queries of a fixed seeded order starting at step*{per_step}, "
+                                 f"until {args.ref_step_budget:.0f} s of oracle time"},
+            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": nproc, "kind": "oracle",
+                             "sample": f"{tot_q} cfg{CONFIG} queries over {args.steps} steps, oracle.c OpenMP "
+                                       f"{nproc} threads (full enumeration)", "host": host_cpu()},
             "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -165,6 +230,18 @@ def max_over_ranks(values, dist, device):
     return [float(x) for x in t.tolist()]
 
 
+def relaunch_under_torchrun(n: int) -> int:
+    """`--gpus N` outside a torchrun environment: launch one process per GPU ourselves."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -174,7 +251,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
                     help="BASELINE.json configs[N-1]; the driver's line is config 2")
     ap.add_argument("--ref-queries-per-step", type=int, default=10)
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-step-budget", type=float, default=8.0, help="reference arm: oracle seconds per step")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--workers", type=int, default=3, help="library batch workers (0 = one query at a time)")
@@ -184,9 +262,14 @@ def main():
     global CONFIG
     CONFIG = args.config
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -201,33 +284,34 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.Stream(device=dev)
-    ctx = gpsense.Context(local, stream=stream)
+    sharded = CONFIG == 4 and world > 1   # row-sharded join of the same queries (strong scaling)
+    if sharded:
+        comm = dist.group.WORLD._get_backend(dev)._comm_ptr()
+        ctx = gpsense.Context(local, stream=stream, nccl_comm=comm, rank=rank, world=world)
+    else:
+        ctx = gpsense.Context(local, stream=stream)
     g = config_graph(4 if CONFIG == 4 else 2)
     G = ctx.load_graph(g)
     queries, counts = load_queries()
-    if CONFIG == 4:
-        args.no_cpu_baseline = True   # the oracle on 10^8 arcs / 10^9 embeddings is far outside a bounded sample
-        from synth.large import CFG4
-    queries, counts = rank_batch(queries, counts, rank)
-    qbatch = gpsense.QueryBatch(queries) if CONFIG != 4 else None   # marshalled once (host descriptors)
+    if CONFIG != 4:
+        queries, counts = rank_batch(queries, counts, rank)
+    qbatch = gpsense.QueryBatch(queries)   # marshalled once (host descriptors)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    batch_api = args.workers and not sharded   # sharded ranks walk queries one at a time (SPMD)
 
-    if args.workers:
+    if batch_api:
         ctx.set_workers(args.workers)
         ctx.set_slice(args.slice)
 
     def step():
-        if CONFIG == 4:
+        if CONFIG == 4:   # each query's rows stay on the device (sharded: this rank's shard)
             emb = 0
-            for (name, q, mode) in CFG4:
-                if mode == "count":
-                    emb += ctx.count(G, q)
-                else:
-                    br = ctx.match_batch_raw(G, [q])
-                    emb += int(br.rows().sum())
-                    br.free()
+            for q in queries:
+                br = ctx.match_batch_raw(G, [q])
+                emb += int(br.rows().sum())
+                br.free()
             return emb
-        if args.workers:
+        if batch_api:
             br = ctx.match_batch_raw(G, qbatch)        # device-resident results, freed after the step
             emb = int(br.rows().sum())
             br.free()
@@ -244,7 +328,7 @@ def main():
         # class event-timed (concurrent streams would blur per-launch event times)
         for _ in range(max(args.warmup, 1)):
             step()
-        if args.workers:   # the timed region's slices, serialised on one stream
+        if batch_api:   # the timed region's slices, serialised on one stream
             ctx.set_workers(1)
             ctx.set_slice(args.slice)
         ctx.set_profiling(gpsense.KERNEL_CLASSES)
@@ -256,7 +340,7 @@ def main():
         dominant = max(ms, key=ms.get)
         kd_iso = iso[dominant]
         total_iso = sum(ms.values())
-        if args.workers:   # fresh worker contexts: warm them again (scratch growth, first launches;
+        if batch_api:   # fresh worker contexts: warm them again (scratch growth, first launches;
             ctx.set_workers(args.workers)   # their first steps can stall on driver allocations)
             ctx.set_slice(args.slice)
             for _ in range(max(args.warmup, 10)):
@@ -290,38 +374,47 @@ def main():
         st = ctx.stats()
 
         # e2e: the same step through the C-ABI with a HOST result buffer (copies inside the region)
-        if CONFIG == 4:   # sizes of the written results (untimed counts), for the pinned buffer
-            counts = [ctx.count(G, q) if mode == "match" else 0 for (_, q, mode) in CFG4]
-            total_words = max(c * q.k for c, q in zip(counts, queries))
+        local_rows = counts if not sharded else [None] * len(queries)
+        if CONFIG == 4:   # every query's (local) rows into one pinned buffer, one query at a time
+            local_rows = [int(ctx.count(G, q)) if not sharded else None for q in queries]
+            if sharded:
+                local_rows = []
+                for q in queries:
+                    a = ctx.match_batch_raw(G, [q])
+                    local_rows.append(int(a.rows().sum()))
+                    a.free()
+            total_words = max(c * q.k for c, q in zip(local_rows, queries))
         else:
-            total_words = sum(c * q.k for c, q in zip(counts, queries))
+            total_words = sum(c * q.k for c, q in zip(local_rows, queries))
         pinned = torch.empty(int(total_words * 1.05) + 1024, dtype=torch.int32, pin_memory=True)
         h2d = sum(query_bytes(q) for q in queries)
-        d2h = sum(c * q.k * 4 for c, q in zip(counts, queries))
+        d2h = sum(c * q.k * 4 for c, q in zip(local_rows, queries))
         e2e_ms = 0.0
-        for s in range(max(1, args.steps // 2)):
+        e2e_steps = max(1, args.steps // 2)
+        for s in range(e2e_steps):
             if flush is not None:
                 flush.fill_(s & 0xff)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             if CONFIG == 4:
-                for (_, q, mode) in CFG4:
-                    if mode == "count":
-                        ctx.count(G, q)
-                    else:
-                        ctx.match_host(G, q, pinned)
-            elif args.workers:
+                for q in queries:
+                    ctx.match_host(G, q, pinned)
+            elif batch_api:
                 ctx.match_batch_host(G, qbatch, pinned)     # library copies every result into `pinned`
             else:
                 for q in queries:
                     ctx.match_host(G, q, pinned)
             e2e_ms += 1000 * (time.perf_counter() - t0)
-        e2e_steps = max(1, args.steps // 2)
 
     max_ms, e2e_step_ms = max_over_ranks([total_ms, e2e_ms / e2e_steps], dist, dev)
-    nq = len(queries) * args.steps * world
-    value = nq / (max_ms / 1000)
-    emb_per_s = emb_total * world / (max_ms / 1000)
+    nq_step = len(queries) if sharded else len(queries) * world   # sharded: all ranks serve the same queries
+    value = nq_step * args.steps / (max_ms / 1000)
+    emb_step_local = emb_total
+    if world > 1:
+        t = torch.tensor([emb_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        emb_step_local = int(t.item())
+    emb_per_s = emb_step_local / (max_ms / 1000)
 
     kd = st["kernels"][dominant]
     achieved = kd["bytes"] / (kd["ms"] / 1000) / 1e9 if kd["ms"] > 0 else None
@@ -331,42 +424,50 @@ def main():
     except Exception:
         pass
     peak = peaks.get("hbm_gbs", 6650.0)
-    traffic = None
+    traffic, l2_hit = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        tj = json.load(open(tpath))   # ncu DRAM bytes per launch of the class (config 2; others prefixed)
-        traffic = tj.get(dominant) if CONFIG == 2 else tj.get(f"cfg{CONFIG}:{dominant}")
+        tj = json.load(open(tpath))   # ncu per-launch DRAM bytes / L2 hit rate of the class, per config
+        key = f"cfg{CONFIG}:{dominant}"
+        traffic = tj.get(key)
+        l2_hit = tj.get(f"{key}:l2_hit_pct")
 
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "embeddings_per_s": emb_per_s,
         "config": {"workload": WORKLOADS[CONFIG], "queries_per_step_per_gpu": len(queries),
-                   "embeddings_per_step_per_gpu": emb_total // args.steps,
-                   "parallelism": f"graph replicated, queries sharded over {world} GPU(s); "
-                                  f"gps_match_batch: {args.workers} worker streams x {args.slice}-query "
-                                  f"batch-synchronous slices per GPU" if args.workers else
-                                  f"graph replicated, queries sharded over {world} GPU(s); one query at a time",
-                   "l2": "flushed between timed steps (256 MiB write outside the events); the 15 MB graph "
-                         "is L2-resident within a step" if flush is not None else "not flushed"},
+                   "embeddings_per_step": emb_step_local // args.steps,
+                   "parallelism": (f"graph replicated on {world} GPU(s), partial-embedding rows sharded "
+                                   f"(NCCL all-gather per join step + row rebalancing)") if sharded else
+                                  (f"graph replicated, queries sharded over {world} GPU(s); "
+                                   f"gps_match_batch: {args.workers} worker streams x {args.slice}-query "
+                                   f"batch-synchronous slices per GPU" if batch_api else
+                                   f"graph replicated, queries over {world} GPU(s); one query at a time"),
+                   "l2": "flushed between timed steps (256 MiB write outside the events)" +
+                         ("; the 15 MB graph is L2-resident within a step" if CONFIG != 4 else "")
+                         if flush is not None else "not flushed"},
         "gpu_launches": st["launches"] // args.steps * args.steps,
         "launches_per_query": st["launches"] / (len(queries) * args.steps),
         "join_rows_max": st["join_rows_max"], "join_rows_per_step": st["join_rows_total"] // args.steps,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "l2_hit_pct": l2_hit,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else
                      "fallback 6650 GB/s",
                      "kernel_ms_share_of_step": kd["ms"] / max_ms if max_ms else None,
                      "note": "achieved = algorithmic bytes / CUDA-event time of every launch of this class in "
-                             "the timed region (concurrent worker streams: per-launch times include sharing)",
+                             "the timed region (concurrent worker streams: per-launch times include sharing); "
+                             "traffic / l2_hit_pct: per-launch ncu --set full capture of this class "
+                             "(profiles/traffic.json)",
                      "algorithmic_bytes_per_launch": kd["bytes"] / max(kd["timed"], 1),
                      "isolated": {"achieved": (kd_iso["bytes"] / (kd_iso["ms"] / 1000) / 1e9) if kd_iso["ms"] else None,
                                   "share_of_kernel_time": kd_iso["ms"] / total_iso if total_iso else None,
-                                  "how": "one pass of the same batch and slices serialised on one stream "
+                                  "how": "one pass of the same step serialised on one stream "
                                          "(the dominant class has the most event time there)"}},
         "clocks": clocks,
-        "e2e": {"value": len(queries) / (e2e_step_ms / 1000) * world, "unit": "queries/s",
+        "e2e": {"value": nq_step / (e2e_step_ms / 1000), "unit": "queries/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
     }
     if CONFIG == 5:
@@ -383,10 +484,10 @@ def main():
         line["latency_ms"] = {"p50": lat[len(lat) // 2], "p99": lat[int(len(lat) * 0.99)],
                               "how": "host wall clock of single-query gps_match calls (500 queries)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        done, emb, dt = cpu_oracle_sample(g, queries, args.cpu_budget)
-        line["cpu_baseline"] = {"value": done / dt, "unit": "queries/s", "cores": 1, "kind": "oracle",
-                                "sample": f"first {done} of the {len(queries)} cfg{CONFIG} queries, oracle.c 1 thread, "
-                                          f"{emb} embeddings in {dt:.1f} s"}
+        if CONFIG == 4:
+            line["cpu_baseline"] = cfg4_cpu_baseline(g, queries, args.cpu_budget)
+        else:
+            line["cpu_baseline"] = cpu_baseline(g, queries, args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -57,6 +57,7 @@ typedef enum {
 #define GPS_FREE (-1)        /* unbound query vertex (variable node P:592) */
 #define GPS_MAX_QV 32        /* max query vertices */
 #define GPS_MAX_QE 64        /* max query arcs */
+#define GPS_REFINE_UNTIL_STABLE 0xFFFFFFFFu   /* gps_match_opts.refine_rounds: refine to the fixpoint */
 
 /* gps_csr_desc.flags */
 #define GPS_DIRECTED 0u
@@ -113,7 +114,9 @@ typedef struct {
 
 /* Knobs of the method (NULL = defaults from gps_default_opts). */
 typedef struct {
-    uint32_t refine_rounds;      /* refinement rounds after initialisation; default 1 */
+    uint32_t refine_rounds;      /* refinement rounds after initialisation; default 1;
+                                    GPS_REFINE_UNTIL_STABLE = rounds until no candidate set shrinks
+                                    ("the refinement function until convergence") */
     int32_t reverse_refine;      /* refine in reversed visit order; default 1 */
     uint32_t lowconn_threshold;  /* query degree <= this is "low connectivity"; default 1 */
     int32_t result_on_device;    /* gps_match: 1 = rows stay in device memory (default), 0 = host copy */

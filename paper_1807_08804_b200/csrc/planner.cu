@@ -159,7 +159,9 @@ Plan make_plan(const gps_query* q, uint32_t n, bool undirected, const std::vecto
     uint32_t kept = 0;
     for (uint32_t u = 0; u < k; u++)
         if (p.bound[u] >= 0 || p.deg[u] > o.lowconn_threshold) kept |= 1u << u;
-    for (uint32_t r = 0; r < o.refine_rounds; r++) {
+    p.until_stable = o.refine_rounds == GPS_REFINE_UNTIL_STABLE;
+    const uint32_t rounds = p.until_stable ? 1u : o.refine_rounds;
+    for (uint32_t r = 0; r < rounds; r++) {
         std::vector<int> seq = p.discovery;
         if (o.reverse_refine) std::reverse(seq.begin(), seq.end());
         for (int u : seq) {

@@ -50,6 +50,7 @@ struct Plan {
     std::vector<int> tparent;      // parent in T (-1 for the root)
     std::vector<FilterStep> init_steps;
     std::vector<FilterStep> refine_steps;
+    bool until_stable = false;     // refine_steps is ONE round, repeated until no set shrinks
 };
 
 // Throws gps::Error (GPS_EINVAL / GPS_EDISCONNECTED).

@@ -117,6 +117,7 @@ struct QS {                       // one query of a chunk
     uint32_t C[GPS_MAX_QV];
     uint32_t P[GPS_MAX_QV][2];    // out / in pair-space size of C(u) (sum of degrees)
     bool live = true;
+    bool stable = false;          // GPS_REFINE_UNTIL_STABLE: the last round removed no candidate
     int ecjob[GPS_MAX_QE][2];
     std::vector<JoinStepPlan> steps;
     int col_of[GPS_MAX_QV];
@@ -183,30 +184,40 @@ void carve_all(Chunk& ch, Carve& cv) {
 // next collect launch of the same vertex (CollectJob.xs); the last step's updates
 // are returned in *pending (the caller folds them into its final collect) or, if
 // pending is null, applied by a post-only collect launch.
-void filter_phase(Chunk& ch, int stage, std::vector<CollectJob>* pending = nullptr) {
+// refine_only: one more refinement round of the queries with mask[qi] != 0 on their current
+// bitmaps (every vertex collected by the previous final collect): the fixpoint version of
+// P:1008 (GPS_REFINE_UNTIL_STABLE).
+void filter_phase(Chunk& ch, int stage, std::vector<CollectJob>* pending = nullptr, bool refine_only = false,
+                  const std::vector<char>* mask = nullptr) {
     gps_ctx* c = ch.c;
     const DevGraph& d = ch.g->d;
-    std::vector<ChkQV> qv;
-    for (QS* q : ch.qs)
-        for (int u = 0; u < q->k; u++) {
-            ChkQV x{};
-            x.lab = q->plan.vlab[u];
-            x.bound = q->plan.bound[u];
-            x.qout = q->plan.qout[u];
-            x.qin = q->plan.qin[u];
-            x.B = q->B + (size_t)u * d.nws;
-            qv.push_back(x);
-        }
-    run_check(c, d, upload(c, qv, ch.keep), (uint32_t)qv.size());
-    if (stage < 1) return;
+    if (!refine_only) {
+        std::vector<ChkQV> qv;
+        for (QS* q : ch.qs)
+            for (int u = 0; u < q->k; u++) {
+                ChkQV x{};
+                x.lab = q->plan.vlab[u];
+                x.bound = q->plan.bound[u];
+                x.qout = q->plan.qout[u];
+                x.qin = q->plan.qin[u];
+                x.B = q->B + (size_t)u * d.nws;
+                qv.push_back(x);
+            }
+        run_check(c, d, upload(c, qv, ch.keep), (uint32_t)qv.size());
+        if (stage < 1) return;
+    }
+    auto in_mask = [&](size_t qi) { return !mask || (*mask)[qi]; };
+    auto n_init = [&](const QS* q) { return refine_only ? (size_t)0 : q->plan.init_steps.size(); };
     size_t S = 0;
-    for (QS* q : ch.qs) {
-        size_t s = q->plan.init_steps.size() + (stage >= 2 ? q->plan.refine_steps.size() : 0);
+    for (size_t qi = 0; qi < ch.qs.size(); qi++) {
+        if (!in_mask(qi)) continue;
+        const QS* q = ch.qs[qi];
+        size_t s = n_init(q) + (stage >= 2 ? q->plan.refine_steps.size() : 0);
         S = std::max(S, s);
     }
     // vertices whose candidate array exists (collected by an earlier step: a superset of
     // the current set); a side without one cannot be walked
-    std::vector<uint32_t> have(ch.qs.size(), 0u);
+    std::vector<uint32_t> have(ch.qs.size(), refine_only ? 0xffffffffu : 0u);
     auto job = [&](size_t qi, int A, int Sv, const Constraint& cs, int dir, uint32_t* X) {
         QS* q = ch.qs[qi];
         ExploreJob e{};
@@ -279,9 +290,10 @@ void filter_phase(Chunk& ch, int stage, std::vector<CollectJob>* pending = nullp
         std::vector<P> post1, post2;
         std::vector<uint32_t*> xs;
         for (size_t qi = 0; qi < ch.qs.size(); qi++) {
+            if (!in_mask(qi)) continue;
             QS* q = ch.qs[qi];
             const Plan& p = q->plan;
-            const size_t ni = p.init_steps.size();
+            const size_t ni = n_init(q);
             const size_t nr = stage >= 2 ? p.refine_steps.size() : 0;
             if (s >= ni + nr) continue;
             const FilterStep& st = s < ni ? p.init_steps[s] : p.refine_steps[s - ni];
@@ -408,6 +420,72 @@ void setup_chunk(Chunk& ch) {
     const char* x1 = reinterpret_cast<const char*>(ch.qs.back()->X) + (size_t)std::max(ch.qs.back()->E, 1) * ch.nws * 4;
     GPS_CK(cudaMemsetAsync((void*)x0, 0, (size_t)(x1 - x0), c->stream));
     (void)xbytes;
+}
+
+// Final collect of every query vertex of the chunk (+ the pending posts of the last filter
+// step), then one sync: |C(u)| and the out/in pair-space sizes of every vertex to the host.
+void final_collect(Chunk& ch, const std::vector<CollectJob>& pend) {
+    gps_ctx* c = ch.c;
+    const DevGraph& d = ch.g->d;
+    std::vector<CollectJob> cj;
+    for (size_t i = 0; i < ch.qs.size(); i++) {
+        QS* q = ch.qs[i];
+        for (int u = 0; u < q->k; u++)
+            cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0],
+                                    q->seg[u][1], ch.cnt_all + ch.ncnt + 2 * (ch.cnt_base[i] + u)});
+    }
+    for (const CollectJob& p : pend) {   // every vertex is collected here: each post finds its job
+        auto it = std::find_if(cj.begin(), cj.end(), [&](const CollectJob& y) { return y.B == p.B && y.x1 == y.x0; });
+        if (it == cj.end()) {
+            cj.push_back(p);
+        } else {
+            it->xs = p.xs;
+            it->x0 = p.x0;
+            it->x1 = p.x1;
+        }
+    }
+    run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
+    const size_t nc = ch.ncnt;
+    size_t got = 0;
+    uint32_t* h = static_cast<uint32_t*>(pinned_alloc(c, nc * 12, &got));
+    GPS_CK(cudaMemcpyAsync(h, ch.cnt_all, nc * 12, cudaMemcpyDeviceToHost, c->stream));
+    ctx_sync(c);
+    for (size_t i = 0; i < ch.qs.size(); i++) {
+        QS* q = ch.qs[i];
+        for (int u = 0; u < q->k; u++) {
+            const size_t x = ch.cnt_base[i] + u;
+            q->C[u] = h[x];
+            q->P[u][0] = h[nc + 2 * x];
+            q->P[u][1] = h[nc + 2 * x + 1];
+        }
+    }
+    pinned_release(c, h, got);
+}
+
+// GPS_REFINE_UNTIL_STABLE (the first two versions): further refinement rounds of the
+// queries whose candidate sets still shrank, until none does.
+void refine_to_fixpoint(Chunk& ch) {
+    for (int round = 0; round < 1024; round++) {
+        std::vector<char> m(ch.qs.size(), 0);
+        std::vector<std::vector<uint32_t>> prev(ch.qs.size());
+        bool any = false;
+        for (size_t i = 0; i < ch.qs.size(); i++) {
+            QS* q = ch.qs[i];
+            if (!q->plan.until_stable || q->stable || q->plan.refine_steps.empty()) continue;
+            bool empty = false;
+            for (int u = 0; u < q->k; u++) empty |= q->C[u] == 0;
+            if (empty) continue;
+            m[i] = 1;
+            prev[i].assign(q->C, q->C + q->k);
+            any = true;
+        }
+        if (!any) break;
+        std::vector<CollectJob> pend2;
+        filter_phase(ch, 2, &pend2, true, &m);
+        final_collect(ch, pend2);
+        for (size_t i = 0; i < ch.qs.size(); i++)
+            if (m[i]) ch.qs[i]->stable = std::equal(prev[i].begin(), prev[i].end(), ch.qs[i]->C);
+    }
 }
 
 // Host copy of n u64 that a collective left in device memory (stream-ordered + sync).
@@ -605,41 +683,8 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
     tr.mark("filter enqueued");
 
     // ---- final collect of every query vertex (+ the last filter step's posts), sync #1 ----
-    {
-        std::vector<CollectJob> cj;
-        for (size_t i = 0; i < ch.qs.size(); i++) {
-            QS* q = ch.qs[i];
-            for (int u = 0; u < q->k; u++)
-                cj.push_back(CollectJob{ch.Bp(*q, u), ch.rpp(*q, u), q->carr[u], q->cnt + u, q->seg[u][0],
-                                        q->seg[u][1], ch.cnt_all + ch.ncnt + 2 * (ch.cnt_base[i] + u)});
-        }
-        for (const CollectJob& p : pend) {   // every vertex is collected here: each post finds its job
-            auto it = std::find_if(cj.begin(), cj.end(), [&](const CollectJob& y) { return y.B == p.B && y.x1 == y.x0; });
-            if (it == cj.end()) {
-                cj.push_back(p);
-            } else {
-                it->xs = p.xs;
-                it->x0 = p.x0;
-                it->x1 = p.x1;
-            }
-        }
-        run_collect(c, d, upload(c, cj, ch.keep), (uint32_t)cj.size());
-        const size_t nc = ch.ncnt;
-        size_t got = 0;
-        uint32_t* h = static_cast<uint32_t*>(pinned_alloc(c, nc * 12, &got));
-        GPS_CK(cudaMemcpyAsync(h, ch.cnt_all, nc * 12, cudaMemcpyDeviceToHost, c->stream));
-        ctx_sync(c);
-        for (size_t i = 0; i < ch.qs.size(); i++) {
-            QS* q = ch.qs[i];
-            for (int u = 0; u < q->k; u++) {
-                const size_t x = ch.cnt_base[i] + u;
-                q->C[u] = h[x];
-                q->P[u][0] = h[nc + 2 * x];
-                q->P[u][1] = h[nc + 2 * x + 1];
-            }
-        }
-        pinned_release(c, h, got);
-    }
+    final_collect(ch, pend);
+    refine_to_fixpoint(ch);
     tr.mark("sync1 (|C(u)|)");
     for (QS* q : ch.qs) {
         QueryResult& r = out[q->idx];
@@ -1121,7 +1166,10 @@ void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t n
         run_chunk(c, g, chunk, count_only, o.rebalance_threshold, o.row_budget_bytes, out, deferred);
         // a deferred query starts the next chunk (where it is first, so it never defers again)
         todo.insert(todo.begin() + (std::ptrdiff_t)i, deferred.begin(), deferred.end());
-        for (QS* q : deferred) q->live = true;
+        for (QS* q : deferred) {
+            q->live = true;
+            q->stable = false;
+        }
     }
     const bool sharded = c->comm != nullptr;
     for (uint32_t j = 0; j < nq; j++)
@@ -1145,7 +1193,14 @@ void run_filter_debug(gps_ctx* c, const gps_graph* g, const gps_query* q, const 
     ch.g = g;
     ch.qs = {&one};
     setup_chunk(ch);
-    filter_phase(ch, stage);
+    if (stage == 2 && one.plan.until_stable) {
+        std::vector<CollectJob> pend;
+        filter_phase(ch, stage, &pend);
+        final_collect(ch, pend);
+        refine_to_fixpoint(ch);
+    } else {
+        filter_phase(ch, stage);
+    }
     GPS_CK(cudaMemcpy2DAsync(host_bitmaps, sizeof(uint32_t) * g->d.nw, one.B, sizeof(uint32_t) * ch.nws,
                              sizeof(uint32_t) * g->d.nw, one.k, cudaMemcpyDeviceToHost, c->stream));
     ctx_sync(c);

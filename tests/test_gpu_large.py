@@ -2,9 +2,14 @@
 per direction on the device) and joins of 10^7..10^9 embeddings.
 
 Pins (independent of oracle and CUDA path): closed-form counts of labelled stars
-and 2-paths (tests/closed_forms.py).  Written rows are checked on a random sample
-against the data arcs and labels, and for pairwise-distinct vertices.
+and 2-paths (tests/closed_forms.py); every written row is checked against the data
+arcs and labels, for injectivity and for distinctness (tests/rowcheck.py).  The cyclic
+config-4 queries (synth/data/cfg4_queries.json) are checked against the oracle's stored
+count and multiset hash.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -13,6 +18,7 @@ from synth import config_graph
 from synth.large import CFG4
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module")
@@ -50,23 +56,54 @@ def test_cfg4_counts_closed_form(env, i):
     assert ctx.count(G, q) == _closed(g, keys, name)
 
 
-@pytest.mark.parametrize("i", [0, 2])
-def test_cfg4_rows_valid_sample(env, i):
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_cfg4_rows_all_valid_distinct(env, i):
+    """Every written row of the closed-form joins (10^7..10^8 rows) is a valid embedding and
+    no row repeats; with the closed-form count this is the full set."""
     import torch
+    import rowcheck
     ctx, g, G, keys = env
     name, q, mode = CFG4[i]
     t = ctx.match(G, q)
     assert t.shape[0] == _closed(g, keys, name)
-    rng = np.random.default_rng(i)
-    idx = torch.as_tensor(rng.choice(t.shape[0], 4096, replace=False), device=t.device)
-    rows = t.view(torch.int32)[idx].cpu().numpy().astype(np.int64)
-    for u in range(q.k):
-        if q.vlabels[u] >= 0:
-            assert (g.vlab[rows[:, u]] == q.vlabels[u]).all()
-        for v in range(u + 1, q.k):
-            assert (rows[:, u] != rows[:, v]).all()
-    for a, b, _ in q.edges:
-        kk = rows[:, a] * g.n + rows[:, b]
-        pos = np.minimum(np.searchsorted(keys, kk), keys.shape[0] - 1)
-        assert (keys[pos] == kk).all()
-    del t
+    x = t.view(torch.int32)
+    assert rowcheck.all_distinct(x)
+    assert rowcheck.all_valid(x, _ga(env, t.device), q)
+    del t, x
+
+
+def _ga(env, device):
+    import rowcheck
+    if not hasattr(_ga, "v"):
+        _ga.v = rowcheck.GraphArrays(env[1], device)
+    return _ga.v
+
+
+def _cyclic():
+    p = os.path.join(ROOT, "synth", "data", "cfg4_queries.json")
+    return json.load(open(p))["queries"] if os.path.exists(p) else []
+
+
+@pytest.mark.parametrize("i", range(len(_cyclic())))
+def test_cfg4_cyclic_parity(env, i):
+    """BASELINE configs[3] cyclic queries (oracle BFS-prefix tables >= 10^9 rows): gps_count
+    equals the oracle's count (scripts/gen_queries_cfg4.py, OpenMP oracle on the GPU host);
+    the gps_match rows have the oracle's multiset hash, are all valid embeddings and all
+    distinct -- the oracle's set."""
+    import torch
+    import rowcheck
+    from synth import Query
+    ctx, g, G, keys = env
+    d = _cyclic()[i]
+    q = Query.from_json(d["query"])
+    assert ctx.count(G, q) == d["oracle_count"]
+    ctx.reset_stats()
+    t = ctx.match(G, q)
+    st = ctx.stats()
+    assert t.shape == (d["oracle_count"], q.k)
+    x = t.view(torch.int32)
+    assert rowcheck.multiset_hash(x) == int(d["oracle_hash"])
+    assert rowcheck.all_distinct(x)
+    assert rowcheck.all_valid(x, _ga(env, t.device), q)
+    print(f"cfg4 cyclic {i}: {d['oracle_count']} rows, join_rows_max {st['join_rows_max']}")
+    del t, x

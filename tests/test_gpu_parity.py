@@ -144,9 +144,20 @@ def test_filter_sets_equal_reference(gps, ctx, seed):
         o = gps.default_opts(refine_rounds=rounds, reverse_refine=rev, lowconn_threshold=low)
         want = filter_ref.candidates(g, q, 2, refine_rounds=rounds, reverse_refine=bool(rev), lowconn_threshold=low)
         assert np.array_equal(ctx.candidates(G, q, 2, o), want), (rounds, rev, low)
+    # the fixpoint version ("until convergence"): equal to the reference refined for so
+    # many rounds that it no longer changes
+    for rev in (1, 0):
+        o = gps.default_opts(refine_rounds=UNTIL_STABLE, reverse_refine=rev)
+        want = filter_ref.candidates(g, q, 2, refine_rounds=48, reverse_refine=bool(rev))
+        assert np.array_equal(want, filter_ref.candidates(g, q, 2, refine_rounds=49, reverse_refine=bool(rev)))
+        assert np.array_equal(ctx.candidates(G, q, 2, o), want), ("fixpoint", rev)
 
 
-@pytest.mark.parametrize("rounds,rev,low", [(0, 1, 1), (1, 0, 1), (3, 1, 1), (1, 1, 0), (2, 0, 2)])
+UNTIL_STABLE = 0xFFFFFFFF   # GPS_REFINE_UNTIL_STABLE
+
+
+@pytest.mark.parametrize("rounds,rev,low", [(0, 1, 1), (1, 0, 1), (3, 1, 1), (1, 1, 0), (2, 0, 2),
+                                            (UNTIL_STABLE, 1, 1), (UNTIL_STABLE, 0, 1)])
 def test_refinement_variants_same_result(gps, ctx, rounds, rev, low):
     """P:997-1008 refinement variants change work, never the result."""
     for seed in (3, 11, 22, 40):

@@ -56,8 +56,8 @@ def test_bench_multirank_gloo(tmp_path):
 def test_reference_arm_rank1_exits_quietly(tmp_path):
     """--impl reference under torchrun: rank 0 alone prints; other ranks exit 0 without work."""
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
-    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0"],
-                       capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert p.returncode == 0 and p.stdout.strip() == ""
 
 
@@ -146,3 +146,12 @@ def test_shard_arithmetic_gloo(tmp_path, world):
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     for r in range(world):
         assert (tmp_path / f"shard{r}").exists()
+
+
+def test_bench_gpus_mismatch_fails_loudly():
+    """A torchrun environment whose world size differs from --gpus is an error, never a
+    silent single-rank run."""
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "4", "--steps", "1"], capture_output=True,
+                       text=True, timeout=120, cwd=ROOT, env=env)
+    assert p.returncode == 2 and "WORLD_SIZE" in p.stderr
