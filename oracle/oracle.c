@@ -170,6 +170,7 @@ typedef struct {
     uint32_t *rows;
     volatile int over;
     uint64_t slot;                /* next free row of `rows` (atomic) */
+    uint64_t emitted;             /* rows emitted by all searchers, in blocks of 1024 (atomic) */
 } orc_shared;
 
 /* One searcher (one per thread). */
@@ -221,6 +222,11 @@ static void emit(orc_state *s) {
     }
     s->hash += row_hash(s->f, p->k);
     s->count++;
+    /* the limit is on the total over all searchers: each publishes its count in blocks */
+    if (sh->limit && (s->count & 1023) == 0) {
+        uint64_t tot = __atomic_add_fetch(&sh->emitted, 1024, __ATOMIC_RELAXED);
+        if (tot > sh->limit) sh->over = 1;
+    }
     if (sh->limit && s->count > sh->limit) sh->over = 1;
 }
 
@@ -482,6 +488,7 @@ void oracle_run(const og_graph *g, uint32_t k, const int32_t *qvlab, const int64
         res->threads = threads;
     }
     if (sh.over == 1 && res->count >= 0) res->count = ORC_ELIMIT;
+    if (limit && res->count > (int64_t)limit) res->count = ORC_ELIMIT;
     free(s0.used);
     free(p);
 }
