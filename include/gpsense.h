@@ -126,8 +126,9 @@ typedef struct {
                                     at once (reading R27, "intermediate results ... a key
                                     challenge"): a step whose output exceeds it is split into pair
                                     ranges and each piece runs the remaining steps depth-first (the
-                                    result set does not depend on it).  0 (default) = one third of the
-                                    device memory free at the time of the step.  gps_count never
+                                    result set does not depend on it).  0 (default) = a quarter of the
+                                    device memory; a table that cannot be allocated below the budget
+                                    also goes depth-first.  gps_count never
                                     materialises its last level, so it never fails for lack of
                                     memory on the tables; gps_match returns GPS_ENOMEM only when the
                                     final rows themselves cannot be allocated. */

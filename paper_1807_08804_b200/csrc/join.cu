@@ -340,17 +340,47 @@ __device__ __forceinline__ bool seg_contains(const uint32_t* __restrict__ val, u
     return false;
 }
 
+// Closing arcs keyed by a column of the input row (the arc's other endpoint is the new
+// vertex) have the SAME candidate segment for every pair of the row: the window staging
+// looks up the first kHoist of them once per row (rank + two offsets) and the pairs only
+// search their segment.  Arcs keyed by the new vertex need its rank per pair.
+constexpr uint32_t kHoist = 3;
+
+__device__ __forceinline__ uint2 close_seg(const CloseChk& cl, uint32_t key) {
+    const uint32_t rk = bit_rank(cl.Bk, cl.rpk, key);
+    return make_uint2(__ldg(cl.off + rk), __ldg(cl.off + rk + 1));
+}
+
+// Per-row part: seg[ci] for the hoisted closing arcs (ci < kHoist, keyed by a row column).
+__device__ __forceinline__ void hoist_close(const JoinStep& a, const JoinJob& J, const uint32_t* __restrict__ row,
+                                            uint2 (&seg)[kHoist]) {
+#pragma unroll
+    for (uint32_t ci = 0; ci < kHoist; ci++) {
+        seg[ci] = make_uint2(0u, 0u);
+        if (ci < J.nclose) {
+            const CloseChk& cl = a.cl[J.close0 + ci];
+            if (!cl.key_new) seg[ci] = close_seg(cl, __ldg(row + cl.key_col));
+        }
+    }
+}
+
 // Injectivity (Def. 2 "injective") + every fused closing arc (P:818 case 1).
 __device__ __forceinline__ bool pair_ok(const JoinStep& a, const JoinJob& J, const uint32_t* __restrict__ row,
-                                        uint32_t cand) {
+                                        uint32_t cand, const uint2 (&seg)[kHoist]) {
     for (uint32_t c = 0; c < a.w; c++)
         if (__ldg(row + c) == cand) return false;
     for (uint32_t ci = 0; ci < J.nclose; ci++) {
         const CloseChk& cl = a.cl[J.close0 + ci];
-        const uint32_t key = cl.key_new ? cand : __ldg(row + cl.key_col);
         const uint32_t tgt = cl.tgt_new ? cand : __ldg(row + cl.tgt_col);
-        const uint32_t rk = bit_rank(cl.Bk, cl.rpk, key);
-        if (!seg_contains(a.ec_val, __ldg(cl.off + rk), __ldg(cl.off + rk + 1), tgt)) return false;
+        uint2 sg = make_uint2(0u, 0u);
+        if (!cl.key_new && ci < kHoist) {
+#pragma unroll
+            for (uint32_t h = 0; h < kHoist; h++)   // select, not index: stays in registers
+                if (h == ci) sg = seg[h];
+        } else {
+            sg = close_seg(cl, cl.key_new ? cand : __ldg(row + cl.key_col));
+        }
+        if (!seg_contains(a.ec_val, sg.x, sg.y, tgt)) return false;
     }
     return true;
 }
@@ -359,6 +389,7 @@ struct JMeta {              // one input row of a join step
     const uint32_t* rowp;   // its w values
     uint32_t s0;            // start of its EC segment in ec_val
     uint32_t job;
+    uint2 cseg[kHoist];     // hoisted closing segments (hoist_close)
 };
 using JoinSmem = PairSmem<JMeta, kPT, kPI, kJW, 1>;
 
@@ -402,6 +433,7 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
         const JoinJob& J = a.jobs[m.job];
         m.rowp = J.M + (r - J.row0) * a.w;
         m.s0 = __ldg(a.s0 + r);
+        hoist_close(a, J, m.rowp, m.cseg);
         return m;
     };
     const uint64_t plo = a.plo, phi = a.phi == ~0ull ? offs(a.R) : a.phi;
@@ -434,7 +466,7 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
             writes[it] = false;
             if (v[it]) {
                 const JoinJob& J = a.jobs[m[it].job];
-                valid[it] = pair_ok(a, J, m[it].rowp, cand[it]);
+                valid[it] = pair_ok(a, J, m[it].rowp, cand[it], m[it].cseg);
                 writes[it] = valid[it] && !J.nowrite;
             }
         }
@@ -508,16 +540,16 @@ struct JVMeta {
     uint32_t perm;          // output column of input column c (nibble c), of the new value (nibble w)
     uint32_t flags;         // bit 0: count only, bit 1: has closing arcs
     uint32_t val[kStageW];  // the row's w values, unused slots 0xffffffff (never a vertex id)
+    uint2 cseg[kHoist];     // hoisted closing segments (hoist_close)
 };
 using JVSmem = PairSmem<JVMeta, kPT, kPI, kJVW, 1>;
 
-__device__ __forceinline__ bool close_ok(const JoinStep& a, const JoinJob& J, const uint32_t* val, uint32_t cand) {
+__device__ __forceinline__ bool close_ok(const JoinStep& a, const JoinJob& J, const JVMeta& m, uint32_t cand) {
     for (uint32_t ci = 0; ci < J.nclose; ci++) {
         const CloseChk& cl = a.cl[J.close0 + ci];
-        const uint32_t key = cl.key_new ? cand : val[cl.key_col];
-        const uint32_t tgt = cl.tgt_new ? cand : val[cl.tgt_col];
-        const uint32_t rk = bit_rank(cl.Bk, cl.rpk, key);
-        if (!seg_contains(a.ec_val, __ldg(cl.off + rk), __ldg(cl.off + rk + 1), tgt)) return false;
+        const uint32_t tgt = cl.tgt_new ? cand : m.val[cl.tgt_col];
+        const uint2 sg = (!cl.key_new && ci < kHoist) ? m.cseg[ci] : close_seg(cl, cl.key_new ? cand : m.val[cl.key_col]);
+        if (!seg_contains(a.ec_val, sg.x, sg.y, tgt)) return false;
     }
     return true;
 }
@@ -548,6 +580,7 @@ __global__ void __launch_bounds__(kPT) k_join_v(const __grid_constant__ JoinStep
         m.perm = perm;
         m.flags = (J.nowrite ? 1u : 0u) | (J.nclose ? 2u : 0u);
         m.s0 = __ldg(a.s0 + r);
+        hoist_close(a, J, rowp, m.cseg);
         return m;
     };
     const uint64_t P = a.phi == ~0ull ? offs(a.R) - a.plo : a.phi - a.plo;
@@ -568,7 +601,7 @@ __global__ void __launch_bounds__(kPT) k_join_v(const __grid_constant__ JoinStep
             bool ok = v[it];
 #pragma unroll
             for (uint32_t c = 0; c < kStageW; c++) ok = ok && m.val[c] != cand[it];   // injectivity (Def. 2)
-            if (ok && (m.flags & 2u)) ok = close_ok(a, a.jobs[m.job], m.val, cand[it]);
+            if (ok && (m.flags & 2u)) ok = close_ok(a, a.jobs[m.job], m, cand[it]);
             valid[it] = ok;
             writes[it] = ok && !(m.flags & 1u);
             mine += writes[it] ? 1u : 0u;

@@ -19,6 +19,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <numeric>
 
 #include "comm.h"
@@ -48,16 +50,26 @@ uint64_t ec_pair_limit() {
     return e && *e ? std::min<uint64_t>(lim, std::strtoull(e, nullptr, 10)) : lim;
 }
 
-// Row budget of a join step (gps_match_opts.row_budget_bytes; 0 = one third of the
-// device memory free now, reading R27).
+// Row budget of a join step (gps_match_opts.row_budget_bytes; 0 = a quarter of the device
+// memory, reading R27; a table that fails to allocate below it also goes depth-first).
+// The device size is read once per device (cudaMemGetInfo is far too slow per step).
 uint64_t step_budget(uint64_t opt) {
     if (opt) return opt;
-    size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
-        (void)cudaGetLastError();
-        return 1ull << 30;
+    static std::mutex mu;
+    static std::map<int, uint64_t> total;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = total.find(dev);
+    if (it == total.end()) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+            (void)cudaGetLastError();
+            tot = 4ull << 30;
+        }
+        it = total.emplace(dev, (uint64_t)tot).first;
     }
-    return std::max<uint64_t>(fr / 3, 64ull << 20);
+    return std::max<uint64_t>(it->second / 4, 64ull << 20);
 }
 
 struct Carve {
@@ -464,7 +476,9 @@ void final_collect(Chunk& ch, const std::vector<CollectJob>& pend) {
 
 // GPS_REFINE_UNTIL_STABLE (the first two versions): further refinement rounds of the
 // queries whose candidate sets still shrank, until none does.
-void refine_to_fixpoint(Chunk& ch) {
+// stop_on_empty: a query with an empty candidate set has no match -- stop refining it (the
+// debug entry point refines on, to show the sets the fixpoint reaches).
+void refine_to_fixpoint(Chunk& ch, bool stop_on_empty = true) {
     for (int round = 0; round < 1024; round++) {
         std::vector<char> m(ch.qs.size(), 0);
         std::vector<std::vector<uint32_t>> prev(ch.qs.size());
@@ -474,7 +488,7 @@ void refine_to_fixpoint(Chunk& ch) {
             if (!q->plan.until_stable || q->stable || q->plan.refine_steps.empty()) continue;
             bool empty = false;
             for (int u = 0; u < q->k; u++) empty |= q->C[u] == 0;
-            if (empty) continue;
+            if (empty && stop_on_empty) continue;
             m[i] = 1;
             prev[i].assign(q->C, q->C + q->k);
             any = true;
@@ -504,7 +518,10 @@ std::vector<uint64_t> d2h_u64(gps_ctx* c, const uint64_t* d, size_t n) {
 CloseChk make_close(const Chunk& ch, const QS& q, int ci, int nv,
                     const std::function<const uint32_t*(int)>& ec_off_of) {
     const QArc& a = q.plan.arcs[ci];
-    const int dir = q.ecjob[ci][0] >= 0 ? 0 : 1;
+    // prefer the direction keyed by the endpoint visited before this step (its segment is a
+    // per-row constant the join kernels look up once per row)
+    const int pref = a.a == nv ? 1 : 0;
+    const int dir = q.ecjob[ci][pref] >= 0 ? pref : 1 - pref;
     const int key = dir ? a.b : a.a, tgt = dir ? a.a : a.b;
     CloseChk x{};
     x.key_new = key == nv;
@@ -826,8 +843,19 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         }
         if (!q->live) continue;
         q->steps = make_join_order(q->plan, cnts, mdir);
-        for (const JoinStepPlan& st : q->steps)
+        for (const JoinStepPlan& st : q->steps) {
             if (q->ecjob[st.arc][st.key_dir] < 0) add_ec(q, st.arc, st.key_dir);
+            // a closing arc is checked fastest keyed by its endpoint visited earlier (one segment
+            // per input row instead of a rank lookup per pair): build that direction too unless
+            // it costs much more than the one built
+            for (int ci : st.closing) {
+                const QArc& a = q->plan.arcs[ci];
+                const int dir = a.a == st.nv ? 1 : 0;
+                if (q->ecjob[ci][dir] >= 0 || std::getenv("GPS_NO_CLOSE_DIR")) continue;
+                const int key = dir ? a.b : a.a, okey = dir ? a.a : a.b;
+                if ((uint64_t)q->P[key][dir] <= 2ull * q->P[okey][1 - dir] + 65536) add_ec(q, ci, dir);
+            }
+        }
     }
     if (ej.size() > nj1) launch_ec(nj1, ec_values);
     auto ec_off_of = [&](int job) { return ecoff.as<uint32_t>() + kc_off[job]; };
@@ -1197,7 +1225,7 @@ void run_filter_debug(gps_ctx* c, const gps_graph* g, const gps_query* q, const 
         std::vector<CollectJob> pend;
         filter_phase(ch, stage, &pend);
         final_collect(ch, pend);
-        refine_to_fixpoint(ch);
+        refine_to_fixpoint(ch, false);
     } else {
         filter_phase(ch, stage);
     }
