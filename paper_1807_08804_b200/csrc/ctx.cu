@@ -72,7 +72,7 @@ static void fault_injection() {
 
 // The library's own stream-ordered memory pool per device (never the device's default
 // pool, whose attributes other users of the process own).  Freed blocks stay cached
-// up to GPS_POOL_KEEP_BYTES (default 16 GiB) across synchronisations, so a steady
+// up to GPS_POOL_KEEP_BYTES (default 64 GiB) across synchronisations, so a steady
 // stream of same-sized queries reuses memory without driver calls; anything above is
 // returned to the driver at the next synchronisation.
 cudaMemPool_t device_pool(int dev) {
@@ -89,7 +89,7 @@ cudaMemPool_t device_pool(int dev) {
     cudaMemPool_t pool;
     GPS_CK(cudaMemPoolCreate(&pool, &props));
     const char* e = std::getenv("GPS_POOL_KEEP_BYTES");
-    uint64_t keep = (e && *e) ? std::strtoull(e, nullptr, 10) : (16ull << 30);
+    uint64_t keep = (e && *e) ? std::strtoull(e, nullptr, 10) : (64ull << 30);
     GPS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     pools[dev] = pool;
     return pool;

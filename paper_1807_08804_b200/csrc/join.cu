@@ -157,6 +157,65 @@ void run_ec(gps_ctx* c, const DevGraph& g, const ECJob* d_jobs, uint32_t nj, uin
 }
 
 // ------------------------------------------------------------ a8 join step
+// Closing arcs keyed by a column of the input row (the arc's other endpoint is the new
+// vertex) have the SAME candidate segment for every pair of the row: the window staging
+// looks up the first kHoist of them once per row (rank + two offsets) and the pairs only
+// search their segment.  Arcs keyed by the new vertex need its rank per pair.
+constexpr uint32_t kHoist = 3;
+
+__device__ __forceinline__ uint2 close_seg(const CloseChk& cl, uint32_t key) {
+    const uint32_t rk = bit_rank(cl.Bk, cl.rpk, key);
+    return make_uint2(__ldg(cl.off + rk), __ldg(cl.off + rk + 1));
+}
+
+// Per-row part: seg[ci] for the hoisted closing arcs (ci < kHoist, keyed by a row column).
+__device__ __forceinline__ void hoist_close(const JoinStep& a, const JoinJob& J, const uint32_t* __restrict__ row,
+                                            uint2 (&seg)[kHoist]) {
+#pragma unroll
+    for (uint32_t ci = 0; ci < kHoist; ci++) {
+        seg[ci] = make_uint2(0u, 0u);
+        if (ci < J.nclose) {
+            const CloseChk& cl = a.cl[J.close0 + ci];
+            if (!cl.key_new) seg[ci] = close_seg(cl, __ldg(row + cl.key_col));
+        }
+    }
+}
+
+// The row's DRIVER list: of the extension segment and the hoisted closing segments -- all
+// sorted lists the new vertex must belong to -- the shortest (first on ties).  The row's
+// pairs walk the driver and test membership in the others, so a row costs min(|S|, |T_i|)
+// pairs instead of |S| (sorted-list intersection, "closing edges" + the north star's
+// "intersect").  The seg pass and the pair kernels compute it the same way.
+struct RowLists {
+    uint2 ext;                // extension segment [x, y) in ec_val
+    uint2 cseg[kHoist];       // hoisted closing segments (0, 0 when not hoisted)
+    uint32_t drv;             // 0: extension, 1 + ci: hoisted closing arc ci
+};
+__device__ __forceinline__ void row_lists(const JoinStep& a, const JoinJob& J, const uint32_t* __restrict__ row,
+                                          RowLists& L) {
+    const uint32_t rk = bit_rank(J.Bx, J.rpx, __ldg(row + J.x_col));
+    L.ext = make_uint2(__ldg(J.ec_off + rk), __ldg(J.ec_off + rk + 1));
+    hoist_close(a, J, row, L.cseg);
+    L.drv = 0;
+    uint32_t best = L.ext.y - L.ext.x;
+#pragma unroll
+    for (uint32_t ci = 0; ci < kHoist; ci++) {
+        if (ci >= J.nclose || a.cl[J.close0 + ci].key_new) continue;
+        const uint32_t n = L.cseg[ci].y - L.cseg[ci].x;
+        if (n < best) {
+            best = n;
+            L.drv = 1 + ci;
+        }
+    }
+}
+__device__ __forceinline__ uint2 driver_seg(const RowLists& L) {
+    uint2 d = L.ext;
+#pragma unroll
+    for (uint32_t ci = 0; ci < kHoist; ci++)
+        if (L.drv == 1 + ci) d = L.cseg[ci];
+    return d;
+}
+
 // rows per thread (4 rows amortise the scan; the FAST pass interleaves their searches)
 // (FAST: 2 rows per thread on small tables -- more threads, shorter chains; 4 on large ones --
 // more searches in flight per thread; measured on configs 2 and 4)
@@ -196,10 +255,18 @@ __global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinSt
             while (jb + 1 < a.nj && s_jr[jb + 1] <= r) jb++;
             const JoinJob& J = a.jobs[jb];
             rowp[i] = J.M + (r - J.row0) * a.w;
-            const uint32_t key = __ldg(rowp[i] + J.x_col);
-            const uint32_t rk = bit_rank(J.Bx, J.rpx, key);
-            sst[i] = __ldg(J.ec_off + rk);
-            len[i] = __ldg(J.ec_off + rk + 1) - sst[i];
+            if (FAST || J.nclose == 0) {
+                const uint32_t key = __ldg(rowp[i] + J.x_col);
+                const uint32_t rk = bit_rank(J.Bx, J.rpx, key);
+                sst[i] = __ldg(J.ec_off + rk);
+                len[i] = __ldg(J.ec_off + rk + 1) - sst[i];
+            } else {   // closing arcs: the row's pairs walk its shortest list
+                RowLists L;
+                row_lists(a, J, rowp[i], L);
+                const uint2 d = driver_seg(L);
+                sst[i] = d.x;
+                len[i] = d.y - d.x;
+            }
             nowr[i] = J.nowrite;
             jrow[i] = jb;
             a.s0[r] = sst[i];
@@ -340,36 +407,15 @@ __device__ __forceinline__ bool seg_contains(const uint32_t* __restrict__ val, u
     return false;
 }
 
-// Closing arcs keyed by a column of the input row (the arc's other endpoint is the new
-// vertex) have the SAME candidate segment for every pair of the row: the window staging
-// looks up the first kHoist of them once per row (rank + two offsets) and the pairs only
-// search their segment.  Arcs keyed by the new vertex need its rank per pair.
-constexpr uint32_t kHoist = 3;
-
-__device__ __forceinline__ uint2 close_seg(const CloseChk& cl, uint32_t key) {
-    const uint32_t rk = bit_rank(cl.Bk, cl.rpk, key);
-    return make_uint2(__ldg(cl.off + rk), __ldg(cl.off + rk + 1));
-}
-
-// Per-row part: seg[ci] for the hoisted closing arcs (ci < kHoist, keyed by a row column).
-__device__ __forceinline__ void hoist_close(const JoinStep& a, const JoinJob& J, const uint32_t* __restrict__ row,
-                                            uint2 (&seg)[kHoist]) {
-#pragma unroll
-    for (uint32_t ci = 0; ci < kHoist; ci++) {
-        seg[ci] = make_uint2(0u, 0u);
-        if (ci < J.nclose) {
-            const CloseChk& cl = a.cl[J.close0 + ci];
-            if (!cl.key_new) seg[ci] = close_seg(cl, __ldg(row + cl.key_col));
-        }
-    }
-}
-
-// Injectivity (Def. 2 "injective") + every fused closing arc (P:818 case 1).
+// Injectivity (Def. 2 "injective") + membership in every list of the row but its driver:
+// the extension segment and every fused closing arc (P:818 case 1).
 __device__ __forceinline__ bool pair_ok(const JoinStep& a, const JoinJob& J, const uint32_t* __restrict__ row,
-                                        uint32_t cand, const uint2 (&seg)[kHoist]) {
+                                        uint32_t cand, const uint2 (&seg)[kHoist], uint2 ext, uint32_t drv) {
     for (uint32_t c = 0; c < a.w; c++)
         if (__ldg(row + c) == cand) return false;
+    if (drv != 0 && !seg_contains(a.ec_val, ext.x, ext.y, cand)) return false;
     for (uint32_t ci = 0; ci < J.nclose; ci++) {
+        if (drv == 1 + ci) continue;   // cand was taken from this list
         const CloseChk& cl = a.cl[J.close0 + ci];
         const uint32_t tgt = cl.tgt_new ? cand : __ldg(row + cl.tgt_col);
         uint2 sg = make_uint2(0u, 0u);
@@ -387,9 +433,11 @@ __device__ __forceinline__ bool pair_ok(const JoinStep& a, const JoinJob& J, con
 
 struct JMeta {              // one input row of a join step
     const uint32_t* rowp;   // its w values
-    uint32_t s0;            // start of its EC segment in ec_val
+    uint32_t s0;            // start of its driver list in ec_val
     uint32_t job;
     uint2 cseg[kHoist];     // hoisted closing segments (hoist_close)
+    uint2 ext;              // extension segment
+    uint32_t drv;           // driver list (RowLists)
 };
 using JoinSmem = PairSmem<JMeta, kPT, kPI, kJW, 1>;
 
@@ -433,7 +481,16 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
         const JoinJob& J = a.jobs[m.job];
         m.rowp = J.M + (r - J.row0) * a.w;
         m.s0 = __ldg(a.s0 + r);
-        hoist_close(a, J, m.rowp, m.cseg);
+        if (J.nclose) {
+            RowLists L;
+            row_lists(a, J, m.rowp, L);
+#pragma unroll
+            for (uint32_t h = 0; h < kHoist; h++) m.cseg[h] = L.cseg[h];
+            m.ext = L.ext;
+            m.drv = L.drv;
+        } else {
+            m.drv = 0;
+        }
         return m;
     };
     const uint64_t plo = a.plo, phi = a.phi == ~0ull ? offs(a.R) : a.phi;
@@ -466,7 +523,7 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
             writes[it] = false;
             if (v[it]) {
                 const JoinJob& J = a.jobs[m[it].job];
-                valid[it] = pair_ok(a, J, m[it].rowp, cand[it], m[it].cseg);
+                valid[it] = pair_ok(a, J, m[it].rowp, cand[it], m[it].cseg, m[it].ext, m[it].drv);
                 writes[it] = valid[it] && !J.nowrite;
             }
         }
@@ -541,11 +598,15 @@ struct JVMeta {
     uint32_t flags;         // bit 0: count only, bit 1: has closing arcs
     uint32_t val[kStageW];  // the row's w values, unused slots 0xffffffff (never a vertex id)
     uint2 cseg[kHoist];     // hoisted closing segments (hoist_close)
+    uint2 ext;              // extension segment
+    uint32_t drv;           // driver list (RowLists)
 };
 using JVSmem = PairSmem<JVMeta, kPT, kPI, kJVW, 1>;
 
 __device__ __forceinline__ bool close_ok(const JoinStep& a, const JoinJob& J, const JVMeta& m, uint32_t cand) {
+    if (m.drv != 0 && !seg_contains(a.ec_val, m.ext.x, m.ext.y, cand)) return false;
     for (uint32_t ci = 0; ci < J.nclose; ci++) {
+        if (m.drv == 1 + ci) continue;   // cand was taken from this list
         const CloseChk& cl = a.cl[J.close0 + ci];
         const uint32_t tgt = cl.tgt_new ? cand : m.val[cl.tgt_col];
         const uint2 sg = (!cl.key_new && ci < kHoist) ? m.cseg[ci] : close_seg(cl, cl.key_new ? cand : m.val[cl.key_col]);
@@ -580,7 +641,16 @@ __global__ void __launch_bounds__(kPT) k_join_v(const __grid_constant__ JoinStep
         m.perm = perm;
         m.flags = (J.nowrite ? 1u : 0u) | (J.nclose ? 2u : 0u);
         m.s0 = __ldg(a.s0 + r);
-        hoist_close(a, J, rowp, m.cseg);
+        if (J.nclose) {
+            RowLists L;
+            row_lists(a, J, rowp, L);
+#pragma unroll
+            for (uint32_t h = 0; h < kHoist; h++) m.cseg[h] = L.cseg[h];
+            m.ext = L.ext;
+            m.drv = L.drv;
+        } else {
+            m.drv = 0;
+        }
         return m;
     };
     const uint64_t P = a.phi == ~0ull ? offs(a.R) - a.plo : a.phi - a.plo;

@@ -1071,6 +1071,10 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             pinned_release(c, h, got);
         }
         tr.mark(fast ? "join step synced (fast)" : single ? "join step synced (single pass)" : "join step synced");
+        if (tr.on)
+            std::fprintf(stderr, "[gps]     step %zu: %zu queries, w=%u, rows %llu, pairs %llu, written %llu, closing %zu\n",
+                         s, act.size(), w, (unsigned long long)R, (unsigned long long)P, (unsigned long long)writes,
+                         cl.size());
         if (!single && writes && (double)writes * 4.0 * (w + 1) > (double)budget) {
             bool fin = true;   // a step whose written rows are all final results is never split
             for (QS* q : act) fin = fin && s + 1 == q->steps.size();

@@ -1,10 +1,11 @@
 """Generate the config-4 cyclic query set (calls only synth/ and oracle/).
 
 BASELINE configs[3] / SURVEY §8(d): on the 20M-vertex / 100M-arc graph, 6/7/8-vertex
-CYCLIC queries (BFS from a top-1% seed expanding the highest-degree neighbours first,
-every induced arc, wildcard edge labels) whose intermediate tables are large: starting
+CYCLIC queries (BFS from a top-10% seed expanding the highest-degree neighbours first,
+every induced arc with its relation label) whose intermediate tables are large: starting
 from the fully labelled query, vertex labels are replaced by '*' one at a time in a
-seeded order (a replacement that makes the oracle exceed its limits is undone) until
+seeded order (a replacement that makes the oracle exceed its limits is undone; the
+fully labelled query is tried first) until
 the oracle's largest BFS-prefix table (#embeddings of the sub-query induced on a BFS
 prefix, oracle.run levels) reaches PEAK rows; accepted iff that happens with
 #Emb <= 10^8.  Every oracle run uses the OpenMP variant on all host cores.  Stored with
@@ -12,8 +13,9 @@ the oracle's count, multiset hash and per-depth table sizes; the file is rewritt
 after every acceptance, so a run cut short keeps what it found.
 
 Usage: python scripts/gen_queries_cfg4.py OUT.json [n_queries] [seconds] [peak]
-(the driver-side run: gpurun on the 16-core GPU host, then commit OUT.json as
-synth/data/cfg4_queries.json).  Never touches the CUDA path.
+(writes synth/data/cfg4_queries.json when OUT.json is that path).  The peak used for the
+stored set is 10^8: with wildcard edge labels (or a 10^9 peak) no hub-core query of this
+graph finished within the oracle's work limit.  Never touches the CUDA path.
 """
 import json
 import os
@@ -28,8 +30,8 @@ sys.path.insert(0, ROOT)
 from synth import Query, bfs_query, config_graph  # noqa: E402
 from oracle import oracle  # noqa: E402
 
-RECIPE = dict(cfg=4, k=(6, 7, 8), seed0=4000, induced=True, max_children=2, keep_elabels=False,
-              prefer_hubs=True, top_fraction=0.01, hi=10**8, work_per_thread=400_000_000)
+RECIPE = dict(cfg=4, k=(6, 7, 8), seed0=4000, induced=True, max_children=2, keep_elabels=True,
+              prefer_hubs=True, top_fraction=0.1, hi=10**8, work_per_thread=200_000_000)
 
 
 def main():
@@ -56,6 +58,13 @@ def main():
         ts = time.time()
         got = None
         trace = []
+        res = oracle.run(og, q, threads=threads, limit=r["hi"])   # the fully labelled query first
+        trace.append((-1, res["count"], max(res["levels"]) if res["count"] >= 0 else -1))
+        if res["count"] >= 0 and max(res["levels"]) >= r["peak"]:
+            got = (q, res)
+            perm = []
+        elif res["count"] < 0:
+            perm = []
         for u in perm:
             trial = list(vl)
             trial[int(u)] = -1

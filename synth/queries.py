@@ -130,7 +130,7 @@ def bfs_query(g: DataGraph, k: int, seed: int, induced: bool = False,
               keep_vlabels: bool = True, keep_elabels: bool = True,
               p_wild_v: float = 0.0, bind_seed: bool = False,
               top_fraction: float = 0.1, max_children: int = 0, prefer_hubs: bool = False,
-              max_extra: int = -1) -> Query:
+              max_extra: int = -1, max_vertex_degree: int = 0) -> Query:
     """BFS-extracted query ("picking a node ... following breadth-first
     search ... nodes in the dense area").
 
@@ -149,6 +149,8 @@ def bfs_query(g: DataGraph, k: int, seed: int, induced: bool = False,
     rng = np.random.default_rng(seed)
     sk = _skeleton(g)
     order = np.argsort(-sk.deg, kind="stable")
+    if max_vertex_degree > 0:
+        order = order[sk.deg[order] <= max_vertex_degree]
     top = order[: max(1, int(g.n * top_fraction))]
     for _attempt in range(64):
         root = int(rng.choice(top))
@@ -170,6 +172,8 @@ def bfs_query(g: DataGraph, k: int, seed: int, induced: bool = False,
                     break
                 y = int(sk.nb[e])
                 if y == x or y in pos:
+                    continue
+                if max_vertex_degree > 0 and sk.deg[y] > max_vertex_degree:
                     continue
                 pos[y] = len(chosen)
                 chosen.append(y)

@@ -80,15 +80,16 @@ def test_cfg3_cyclic_sets(env, i):
     if d["oracle_count"] <= 300_000:
         assert np.array_equal(_rows(t), oracle.match(og, q))
     # one first-column partition, row by row: [lo, hi) chosen around the median image of vertex 0
-    col0 = t[:, 0].to(torch.int64) & 0xFFFFFFFF
+    x = t.view(torch.int32)
+    col0 = x[:, 0].to(torch.int64) & 0xFFFFFFFF
     if col0.numel():
         mid = int(col0.median().item())
         lo, hi = max(0, mid - 200), mid + 200
-        sel = t[(col0 >= lo) & (col0 < hi)]
+        sel = x[(col0 >= lo) & (col0 < hi)]
         r = oracle.run(og, q, col0_range=(lo, hi), rows=True, cap=max(1, sel.shape[0]) + 1, threads=os.cpu_count())
         assert r["count"] == sel.shape[0]
         assert np.array_equal(_rows(sel), r["rows"])
-    del t
+    del t, x
 
 
 def test_cfg5_qa_batch_counts(env):
