@@ -36,6 +36,7 @@ constexpr uint32_t kStageW = kJoinStageCols;   // join: stage rows of width <= 8
 // the keys whose first pair it holds.  Values of a key therefore come out sorted
 // and contiguous, and the count pass + scan of the two-step scheme disappear.
 constexpr uint32_t kTile = kPT * kPI;      // pairs per chunk (and per join tile)
+static_assert(kTile == kJoinTilePairs, "host and device join tiling differ");
 constexpr uint32_t kEcTile = 4 * kTile;     // pairs per EC tile: a few chunks amortise the tile's set-up latency
 static_assert(kEcTile == kEcPairTile, "host and device EC tiling differ");
 
@@ -407,28 +408,75 @@ __device__ __forceinline__ bool seg_contains(const uint32_t* __restrict__ val, u
     return false;
 }
 
-// Injectivity (Def. 2 "injective") + membership in every list of the row but its driver:
-// the extension segment and every fused closing arc (P:818 case 1).
-__device__ __forceinline__ bool pair_ok(const JoinStep& a, const JoinJob& J, const uint32_t* __restrict__ row,
-                                        uint32_t cand, const uint2 (&seg)[kHoist], uint2 ext, uint32_t drv) {
-    for (uint32_t c = 0; c < a.w; c++)
-        if (__ldg(row + c) == cand) return false;
-    if (drv != 0 && !seg_contains(a.ec_val, ext.x, ext.y, cand)) return false;
-    for (uint32_t ci = 0; ci < J.nclose; ci++) {
-        if (drv == 1 + ci) continue;   // cand was taken from this list
-        const CloseChk& cl = a.cl[J.close0 + ci];
-        const uint32_t tgt = cl.tgt_new ? cand : __ldg(row + cl.tgt_col);
-        uint2 sg = make_uint2(0u, 0u);
-        if (!cl.key_new && ci < kHoist) {
-#pragma unroll
-            for (uint32_t h = 0; h < kHoist; h++)   // select, not index: stays in registers
-                if (h == ci) sg = seg[h];
-        } else {
-            sg = close_seg(cl, cl.key_new ? cand : __ldg(row + cl.key_col));
-        }
-        if (!seg_contains(a.ec_val, sg.x, sg.y, tgt)) return false;
+// First index in [lo, hi) with val[i] >= t (val sorted ascending).
+__device__ __forceinline__ uint32_t seg_lower(const uint32_t* __restrict__ val, uint32_t lo, uint32_t hi, uint32_t t) {
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(val + mid) < t) lo = mid + 1; else hi = mid;
     }
-    return true;
+    return lo;
+}
+// Same, knowing val[i] < t for every i < lo: doubling probes from lo, then a binary search
+// of the last gap -- O(log distance) when consecutive searches land close together.
+__device__ __forceinline__ uint32_t seg_gallop(const uint32_t* __restrict__ val, uint32_t lo, uint32_t hi, uint32_t t) {
+    uint32_t step = 1, b = lo;
+    while (b < hi && __ldg(val + b) < t) {
+        lo = b + 1;
+        b = lo + step;
+        step <<= 1;
+    }
+    return seg_lower(val, lo, b < hi ? b : hi, t);
+}
+
+// Membership of a thread's candidates in the lists of their rows, list by list: the
+// extension segment (when it is not the driver) and the hoisted closing segments.  A
+// thread's items are consecutive pairs; items of one row carry increasing candidates (the
+// driver is sorted), so each search after the first of a row gallops from the previous
+// position instead of restarting (a merge-like intersection of the row's lists).  Closing
+// arcs that are not hoisted (keyed by the new vertex, or beyond kHoist) are checked per item
+// with their own rank lookup.  ok[] holds the injectivity results on entry.
+template <int IPT, typename MetaAt, typename RowVal>
+__device__ __forceinline__ void lists_check(const JoinStep& a, const uint32_t (&wi)[IPT], const uint32_t (&cand)[IPT],
+                                            bool (&ok)[IPT], MetaAt meta_of, RowVal rowval) {
+#pragma unroll 1
+    for (uint32_t l = 0; l <= kHoist; l++) {
+        uint32_t prow = 0xffffffffu, ppos = 0;
+#pragma unroll
+        for (int it = 0; it < IPT; it++) {
+            if (!ok[it]) continue;
+            const auto& m = meta_of(wi[it]);
+            const JoinJob& J = a.jobs[m.job];
+            if (J.nclose == 0) continue;
+            uint2 sg = m.ext;
+            bool use = m.drv != 0;
+            if (l > 0) {
+                const uint32_t ci = l - 1;
+                use = ci < J.nclose && m.drv != l && !a.cl[J.close0 + ci].key_new;
+#pragma unroll
+                for (uint32_t h = 0; h < kHoist; h++)
+                    if (h == ci) sg = m.cseg[h];
+            }
+            if (!use) continue;
+            const uint32_t pos = wi[it] == prow ? seg_gallop(a.ec_val, max(ppos, sg.x), sg.y, cand[it])
+                                                : seg_lower(a.ec_val, sg.x, sg.y, cand[it]);
+            ok[it] = pos < sg.y && __ldg(a.ec_val + pos) == cand[it];
+            prow = wi[it];
+            ppos = pos;
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        if (!ok[it]) continue;
+        const auto& m = meta_of(wi[it]);
+        const JoinJob& J = a.jobs[m.job];
+        for (uint32_t ci = 0; ci < J.nclose && ok[it]; ci++) {
+            const CloseChk& cl = a.cl[J.close0 + ci];
+            if (!cl.key_new && ci < kHoist) continue;   // done above
+            const uint32_t tgt = cl.tgt_new ? cand[it] : rowval(m, cl.tgt_col);
+            const uint2 sg = close_seg(cl, cl.key_new ? cand[it] : rowval(m, cl.key_col));
+            ok[it] = seg_contains(a.ec_val, sg.x, sg.y, tgt);
+        }
+    }
 }
 
 struct JMeta {              // one input row of a join step
@@ -518,15 +566,14 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
         for (int it = 0; it < kPI; it++) cand[it] = v[it] ? __ldg(a.ec_val + m[it].s0 + j[it]) : 0u;
         bool valid[kPI], writes[kPI];
 #pragma unroll
-        for (int it = 0; it < kPI; it++) {
-            valid[it] = false;
-            writes[it] = false;
-            if (v[it]) {
-                const JoinJob& J = a.jobs[m[it].job];
-                valid[it] = pair_ok(a, J, m[it].rowp, cand[it], m[it].cseg, m[it].ext, m[it].drv);
-                writes[it] = valid[it] && !J.nowrite;
-            }
+        for (int it = 0; it < kPI; it++) {   // injectivity (Def. 2 "injective")
+            valid[it] = v[it];
+            for (uint32_t c = 0; c < a.w && valid[it]; c++) valid[it] = __ldg(m[it].rowp + c) != cand[it];
         }
+        lists_check<kPI>(a, wi, cand, valid, [&](uint32_t w_) -> const JMeta& { return sm[w_]; },
+                         [&](const JMeta& mm, uint32_t col) { return __ldg(mm.rowp + col); });
+#pragma unroll
+        for (int it = 0; it < kPI; it++) writes[it] = valid[it] && !a.jobs[m[it].job].nowrite;
         if (MODE != 1) {   // per-job output totals
             uint32_t key[kPI], one[kPI];
 #pragma unroll
@@ -578,7 +625,8 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
         }
         __syncthreads();
         const uint64_t pre = s_prefix;
-        copy_out(a.out + pre * a.wout, s_out, lc * a.wout);
+        const uint64_t n = pre >= a.cap ? 0 : (lc < a.cap - pre ? lc : a.cap - pre);   // rows below the capacity
+        copy_out(a.out + (a.out_base + pre) * a.wout, s_out, (uint32_t)n * a.wout);
         if (t == ntiles - 1 && threadIdx.x == 0) {
             a.ctl.info[0] = P;
             a.ctl.info[1] = pre + lc;
@@ -602,18 +650,6 @@ struct JVMeta {
     uint32_t drv;           // driver list (RowLists)
 };
 using JVSmem = PairSmem<JVMeta, kPT, kPI, kJVW, 1>;
-
-__device__ __forceinline__ bool close_ok(const JoinStep& a, const JoinJob& J, const JVMeta& m, uint32_t cand) {
-    if (m.drv != 0 && !seg_contains(a.ec_val, m.ext.x, m.ext.y, cand)) return false;
-    for (uint32_t ci = 0; ci < J.nclose; ci++) {
-        if (m.drv == 1 + ci) continue;   // cand was taken from this list
-        const CloseChk& cl = a.cl[J.close0 + ci];
-        const uint32_t tgt = cl.tgt_new ? cand : m.val[cl.tgt_col];
-        const uint2 sg = (!cl.key_new && ci < kHoist) ? m.cseg[ci] : close_seg(cl, cl.key_new ? cand : m.val[cl.key_col]);
-        if (!seg_contains(a.ec_val, sg.x, sg.y, tgt)) return false;
-    }
-    return true;
-}
 
 __global__ void __launch_bounds__(kPT) k_join_v(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
                                                 uint32_t epoch) {
@@ -671,9 +707,13 @@ __global__ void __launch_bounds__(kPT) k_join_v(const __grid_constant__ JoinStep
             bool ok = v[it];
 #pragma unroll
             for (uint32_t c = 0; c < kStageW; c++) ok = ok && m.val[c] != cand[it];   // injectivity (Def. 2)
-            if (ok && (m.flags & 2u)) ok = close_ok(a, a.jobs[m.job], m, cand[it]);
             valid[it] = ok;
-            writes[it] = ok && !(m.flags & 1u);
+        }
+        lists_check<kPI>(a, wi, cand, valid, [&](uint32_t w_) -> const JVMeta& { return sm[w_]; },
+                         [&](const JVMeta& mm, uint32_t col) { return mm.val[col]; });
+#pragma unroll
+        for (int it = 0; it < kPI; it++) {
+            writes[it] = valid[it] && !(sm[wi[it]].flags & 1u);
             mine += writes[it] ? 1u : 0u;
         }
         {   // per-job output totals: warp-wide when the warp's items share one job, else per run
@@ -719,7 +759,8 @@ __global__ void __launch_bounds__(kPT) k_join_v(const __grid_constant__ JoinStep
     }
     __syncthreads();
     const uint64_t pre = s_prefix;
-    copy_out(a.out + pre * wout, s_out, lc * wout);
+    const uint64_t n = pre >= a.cap ? 0 : (lc < a.cap - pre ? lc : a.cap - pre);   // rows below the capacity
+    copy_out(a.out + (a.out_base + pre) * wout, s_out, (uint32_t)n * wout);
     if (t == ntiles - 1 && threadIdx.x == 0) {
         a.ctl.info[0] = P;
         a.ctl.info[1] = pre + lc;
@@ -952,19 +993,41 @@ void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G) {
     allow_join_smem();
     launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kPT), join_smem(s.nj, 1, s.wout), k_join<1>, s, LbScratch{}, 0u, 0u);
 }
-void run_join_tiles(gps_ctx* c, const JoinStep& s, uint64_t P) {
-    if (P == 0) return;
+uint32_t run_join_tiles(gps_ctx* c, const JoinStep& s, uint64_t P) {
+    if (P == 0) return 0;
     const uint64_t nt = (P + kTile - 1) / kTile;
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join pair space too large");
     if (s.wout > GPS_MAX_QV) fail(GPS_EINVAL, "internal: join row too wide");
     allow_join_smem();
     LbScratch lb = lb_scratch(c, 1, (uint32_t)nt);
+    const uint32_t ep = lb_next_epoch(c);
     if (s.wout <= kStageW)
         launch(c, GPS_K_JOIN_WRITE, dim3((uint32_t)nt), dim3(kPT), join_v_smem(s.nj, s.wout), k_join_v, s, lb,
-               (uint32_t)nt, lb_next_epoch(c));
+               (uint32_t)nt, ep);
     else
         launch(c, GPS_K_JOIN_WRITE, dim3((uint32_t)nt), dim3(kPT), join_smem(s.nj, 2, s.wout), k_join<2>, s, lb,
-               (uint32_t)nt, lb_next_epoch(c));
+               (uint32_t)nt, ep);
+    return ep;
+}
+
+// After a capped single pass (epoch ep, nt tiles, look-back words in slot 0): the first tile
+// whose rows reach past row `cap` and its exclusive output prefix -> out[0], out[1].
+__global__ void k_cap_tile(const uint64_t* __restrict__ status, uint32_t nt, uint64_t cap, uint64_t* out) {
+    if (threadIdx.x != 0) return;
+    auto incl = [&](uint32_t t) { return status[t] & kLbValueMask; };
+    uint32_t lo = 0, hi = nt;   // first t with incl(t) > cap
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (incl(mid) > cap) hi = mid; else lo = mid + 1;
+    }
+    out[0] = lo;
+    out[1] = lo == 0 ? 0 : incl(lo - 1);
+}
+
+void run_cap_tile(gps_ctx* c, uint64_t P, uint64_t cap, uint64_t* d_out) {
+    const uint64_t nt = (P + kTile - 1) / kTile;
+    LbScratch lb = lb_scratch(c, 1, (uint32_t)nt);
+    launch(c, GPS_K_JOIN_LEN, dim3(1), dim3(32), 0, k_cap_tile, (const uint64_t*)lb.status, (uint32_t)nt, cap, d_out);
 }
 
 }  // namespace gps

@@ -160,7 +160,9 @@ struct JoinStep {
     uint64_t* poff;        // [R+1] exclusive scan of segment lengths (pair space)
     PassCtl ctl;
     uint32_t* out;         // output rows of the writing jobs, job order
-    uint64_t plo = 0, phi = ~0ull;   // pair sub-range to process (row-sharded join); phi == ~0: all pairs
+    uint64_t plo = 0, phi = ~0ull;   // pair sub-range to process; phi == ~0: all pairs
+    uint64_t cap = ~0ull;            // single pass: output rows the buffer holds (rows past it are not written)
+    uint64_t out_base = 0;           // single pass: output row of the first row this launch produces
     // closing-free steps (every job): validity is injectivity only, so a row's outputs are its
     // segment minus the row's own values.  imask[r] = which of row r's values occur in its
     // segment (binary searches in the seg pass); woff = exclusive scan of written
@@ -177,8 +179,13 @@ void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (+ imask / a
 void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint64_t P);
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G);
 void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G);
-// Single pass (no count pass): P = pairs of the step (poff[R]); out must hold P rows
-// (an upper bound); per-job totals via jobs[].total, info[0] = P, info[1] = rows written.
-void run_join_tiles(gps_ctx* c, const JoinStep& s, uint64_t P);
+// Single pass (no count pass): P = pairs of the step's range [plo, phi); out holds cap rows
+// (rows of the step past cap are produced but not written); per-job totals via
+// jobs[].total, info[0] = P, info[1] = rows produced.  Returns the look-back epoch.
+uint32_t run_join_tiles(gps_ctx* c, const JoinStep& s, uint64_t P);
+// After a capped run_join_tiles of P pairs: d_out[0] = first tile not fully written,
+// d_out[1] = its first output row (the tail is rerun from there).
+void run_cap_tile(gps_ctx* c, uint64_t P, uint64_t cap, uint64_t* d_out);
+constexpr uint32_t kJoinTilePairs = 1024;   // pairs per single-pass tile (join.cu kTile)
 
 }  // namespace gps

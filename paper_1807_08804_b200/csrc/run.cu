@@ -35,11 +35,12 @@ namespace {
 constexpr size_t kAlign = 256;
 constexpr uint32_t kMaxBatch = 512;            // queries per chunk
 constexpr size_t kChunkBytes = size_t(6) << 30;  // filter arena budget per chunk
-// Largest upper-bound output block (P rows) a join step may allocate to run as one
-// pass; GPS_SINGLE_PASS_BYTES overrides (0 forces count -> write everywhere).
+// Output buffer of a single-pass join step: at most this many bytes (and at most the
+// step's pairs, an upper bound on its rows); rows past it are produced by a rerun of the
+// tail into an exact buffer.  GPS_SINGLE_PASS_BYTES overrides (0 forces count -> write).
 double single_pass_bytes() {
     const char* e = std::getenv("GPS_SINGLE_PASS_BYTES");
-    return e && *e ? std::atof(e) : 24.0 * (1ull << 30);
+    return e && *e ? std::atof(e) : 8.0 * (1ull << 30);
 }
 
 // Limit on the candidate-edge pairs of one chunk (32-bit value positions); GPS_EC_PAIR_LIMIT
@@ -1030,22 +1031,25 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
         };
         Block ob;
         bool single = false;
+        uint64_t P0 = 0;
         if (fast) {
             GPS_CK(cudaMemcpyAsync(c->d_info, js.poff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
             GPS_CK(cudaMemcpyAsync(c->d_info + 1, js.woff + R, 8, cudaMemcpyDeviceToDevice, c->stream));
         } else {
-            const uint64_t P0 = d2h_u64(c, js.poff + R, 1)[0];
-            // single pass when an output block of P0 rows (an upper bound) is affordable: no
-            // count pass; else count -> exact allocation -> write
-            single = !any_write ||
-                     (double)P0 * 4.0 * (w + 1) <= std::min<double>(single_pass_bytes(), (double)budget);
+            P0 = d2h_u64(c, js.poff + R, 1)[0];
+            // single pass (no count pass) into a buffer of min(P0 rows (an upper bound), the
+            // single-pass byte cap): a step whose rows overflow it reruns only its tail
+            const double rowb = 4.0 * (w + 1);
+            const double cap_bytes = std::min<double>(single_pass_bytes(), (double)budget);
+            single = !any_write || cap_bytes > 0;
             if (single) {
-                if (any_write && P0) {
+                js.cap = any_write ? std::min<uint64_t>(P0, (uint64_t)(cap_bytes / rowb)) : 0;
+                if (js.cap) {
                     try {
-                        ob = make_block(c, sizeof(uint32_t) * P0 * (w + 1));
+                        ob = make_block(c, sizeof(uint32_t) * js.cap * (w + 1));
                     } catch (const Error& e) {
                         if (e.status != GPS_ENOMEM) throw;
-                        single = false;   // no room for the upper bound: count first
+                        single = false;   // no room for the buffer: count first
                     }
                     if (ob) js.out = static_cast<uint32_t*>(ob->p);
                 }
@@ -1054,6 +1058,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
                 if (P0) run_join_tiles(c, js, P0);
                 else GPS_CK(cudaMemsetAsync(c->d_info, 0, 16, c->stream));
             } else {
+                js.cap = ~0ull;
                 run_join_count(c, js, G);
             }
         }
@@ -1075,13 +1080,31 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
             std::fprintf(stderr, "[gps]     step %zu: %zu queries, w=%u, rows %llu, pairs %llu, written %llu, closing %zu\n",
                          s, act.size(), w, (unsigned long long)R, (unsigned long long)P, (unsigned long long)writes,
                          cl.size());
-        if (!single && writes && (double)writes * 4.0 * (w + 1) > (double)budget) {
+        if (writes && (double)writes * 4.0 * (w + 1) > (double)budget && (!single || writes > js.cap)) {
             bool fin = true;   // a step whose written rows are all final results is never split
             for (QS* q : act) fin = fin && s + 1 == q->steps.size();
             if (!fin) {
                 go_deep();
                 break;
             }
+        }
+        if (single && writes > js.cap) {
+            // the rows overflowed the single-pass buffer: keep the first cap rows, rerun the
+            // tail (from the first tile not fully written) into an exact buffer
+            Block nb = make_block(c, sizeof(uint32_t) * writes * (w + 1));
+            if (js.cap)
+                GPS_CK(cudaMemcpyAsync(nb->p, ob->p, sizeof(uint32_t) * js.cap * (w + 1), cudaMemcpyDeviceToDevice,
+                                       c->stream));
+            run_cap_tile(c, P0, js.cap, c->d_info + 2);
+            const std::vector<uint64_t> tp = d2h_u64(c, c->d_info + 2, 2);
+            JoinStep rt = js;
+            rt.plo = tp[0] * kJoinTilePairs;
+            rt.out = static_cast<uint32_t*>(nb->p);
+            rt.out_base = tp[1];
+            rt.cap = ~0ull;
+            run_join_tiles(c, rt, P0 - rt.plo);   // per-job totals are already on the host
+            ob = nb;
+            c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * (double)(P0 - rt.plo) + 4.0 * (w + 1) * (double)(writes - tp[1]);
         }
         if (single) {
             c->stats.k_bytes[GPS_K_JOIN_WRITE] += 4.0 * w * (double)R + 4.0 * (double)P + 4.0 * (w + 1) * (double)writes;

@@ -89,11 +89,14 @@ def test_random_corpus(ctx, seed):
     _check(ctx, ctx.load_graph(g), og, q)
 
 
-@pytest.mark.parametrize("env", ["GPS_SINGLE_PASS_BYTES=0", "GPS_NO_FAST_JOIN=1"])
+@pytest.mark.parametrize("env", ["GPS_SINGLE_PASS_BYTES=0", "GPS_NO_FAST_JOIN=1", "GPS_SINGLE_PASS_BYTES=256",
+                                 "GPS_NO_CLOSE_DIR=1"])
 @pytest.mark.parametrize("seed", range(0, 200, 5))
 def test_random_corpus_other_join_paths(ctx, seed, env, monkeypatch):
     """Same corpus with the closing-free fast path off (GPS_NO_FAST_JOIN: look-back tiles) and
-    additionally the single pass off (GPS_SINGLE_PASS_BYTES=0: count -> exact allocation -> write)."""
+    additionally: the single pass off (GPS_SINGLE_PASS_BYTES=0: count -> exact allocation ->
+    write); a 256-byte single-pass buffer (nearly every step overflows it and reruns its tail);
+    closing arcs only in the direction built first (GPS_NO_CLOSE_DIR: per-pair rank lookups)."""
     monkeypatch.setenv("GPS_NO_FAST_JOIN", "1")
     k, v = env.split("=")
     monkeypatch.setenv(k, v)
