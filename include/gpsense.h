@@ -58,6 +58,8 @@ typedef enum {
 #define GPS_MAX_QV 32        /* max query vertices */
 #define GPS_MAX_QE 64        /* max query arcs */
 #define GPS_REFINE_UNTIL_STABLE 0xFFFFFFFFu   /* gps_match_opts.refine_rounds: refine to the fixpoint */
+#define GPS_PLAN_RANKING 0                    /* gps_match_opts.plan_mode */
+#define GPS_PLAN_COMMONSENSE 1
 
 /* gps_csr_desc.flags */
 #define GPS_DIRECTED 0u
@@ -122,6 +124,9 @@ typedef struct {
     int32_t result_on_device;    /* gps_match: 1 = rows stay in device memory (default), 0 = host copy */
     float rebalance_threshold;   /* row-sharded join: exchange rows when max/mean pairs per rank exceeds
                                     this (default 1.10; 0 = always, very large = never) */
+    int32_t plan_mode;           /* visit order O: GPS_PLAN_RANKING (default, f(u) = deg/freq) or
+                                    GPS_PLAN_COMMONSENSE (concept node of max degree first, then the
+                                    neighbour with the most unordered neighbours) */
     uint64_t row_budget_bytes;   /* largest partial-embedding table (bytes) a join step may materialise
                                     at once (reading R27, "intermediate results ... a key
                                     challenge"): a step whose output exceeds it is split into pair
@@ -229,6 +234,26 @@ typedef struct gps_local_comm gps_local_comm;
 GPS_API gps_status gps_local_comm_create(int world, gps_local_comm** out);
 GPS_API gps_status gps_local_comm_destroy(gps_local_comm* comm);
 GPS_API gps_status gps_create_local_rank(const gps_ctx_opts* opts, gps_local_comm* comm, int rank, gps_ctx** out);
+
+/* ---- f2: commonsense query semantics -----------------------
+ * gps_load_triples: a knowledge base given as (subject, relation, object) triples is the
+ *   labelled data graph directly ("direct transformation": concepts -> vertices,
+ *   relations -> labelled arcs subject -> object).  subject/object [n_triples] < n_vertices,
+ *   relation [n_triples] (NULL = all 0), vertex_labels as for gps_csr_desc (NULL = all 0,
+ *   P:528).  flags as gps_csr_desc.flags.  Same errors as gps_load_data_graph.
+ * gps_match_project: the matches of the PROJECTION ("a subset of variable
+ *   nodes, termed projection"): the set of distinct tuples (f(project[0]), ...,
+ *   f(project[n_project-1])) over all embeddings f, in lexicographic order; rows x n_project
+ *   in the result.  GPS_EINVAL if n_project is 0 or > 32 or a vertex is out of range;
+ *   GPS_EUNSUPPORTED with a row-sharded ctx or more than 2^32 embeddings.
+ * gps_count_project: the number of such tuples. */
+GPS_API gps_status gps_load_triples(gps_ctx* ctx, uint32_t n_vertices, uint64_t n_triples, const uint32_t* subject,
+                                    const uint16_t* relation, const uint32_t* object, const uint16_t* vertex_labels,
+                                    uint32_t flags, gps_graph** out);
+GPS_API gps_status gps_match_project(gps_ctx* ctx, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
+                                     uint32_t n_project, const int32_t* project, gps_result** out);
+GPS_API gps_status gps_count_project(gps_ctx* ctx, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
+                                     uint32_t n_project, const int32_t* project, uint64_t* count);
 
 /* rows, cols (= k), data (device or host pointer, owned by the result), on_device. */
 GPS_API gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols,

@@ -190,6 +190,7 @@ gps_status gps_default_opts(gps_match_opts* o) {
     o->result_on_device = 1;
     o->rebalance_threshold = 1.10f;
     o->row_budget_bytes = 0;
+    o->plan_mode = GPS_PLAN_RANKING;
     return GPS_OK;
 }
 
@@ -490,6 +491,71 @@ gps_status gps_count_batch(gps_ctx* c, const gps_graph* g, const gps_query* qs, 
             if (st[i] != GPS_OK && first == GPS_OK) first = st[i];
         }
         if (first != GPS_OK) fail(first, "some queries of the batch failed (see statuses)");
+    });
+}
+
+gps_status gps_load_triples(gps_ctx* c, uint32_t n, uint64_t m, const uint32_t* subj, const uint16_t* rel,
+                            const uint32_t* obj, const uint16_t* vlab, uint32_t flags, gps_graph** out) {
+    return guarded([&] {
+        if (!c || !out) fail(GPS_EINVAL, "null ctx/out");
+        if (m && (!subj || !obj)) fail(GPS_EINVAL, "null subject/object");
+        // counting sort by subject on the host (input marshalling; the device load sorts and
+        // de-duplicates every row)
+        std::vector<uint64_t> off((size_t)n + 1, 0);
+        for (uint64_t i = 0; i < m; i++) {
+            if (subj[i] >= n || obj[i] >= n) fail(GPS_EINVAL, "triple endpoint >= n_vertices");
+            off[subj[i] + 1]++;
+        }
+        for (uint32_t v = 0; v < n; v++) off[v + 1] += off[v];
+        std::vector<uint32_t> tgt(m);
+        std::vector<uint16_t> lab(rel ? m : 0);
+        std::vector<uint64_t> at(off.begin(), off.end() - 1);
+        for (uint64_t i = 0; i < m; i++) {
+            const uint64_t j = at[subj[i]]++;
+            tgt[j] = obj[i];
+            if (rel) lab[j] = rel[i];
+        }
+        gps_csr_desc d{n, m, off.data(), tgt.data(), rel ? lab.data() : nullptr, vlab, flags};
+        const gps_status st = gps_load_data_graph(c, &d, out);
+        if (st != GPS_OK) fail(st, last_error());
+    });
+}
+
+static void project_call(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts* opts, uint32_t kp,
+                         const int32_t* cols, gps_result** out, uint64_t* count) {
+    check_args(c, g);
+    if (!q) fail(GPS_EINVAL, "null query");
+    if (kp && !cols) fail(GPS_EINVAL, "null projection");
+    if (c->comm) fail(GPS_EUNSUPPORTED, "projection with a row-sharded ctx");
+    DeviceGuard dg(c->device);
+    const gps_match_opts o = resolve_opts(opts);
+    std::vector<QueryResult> qr;
+    run_queries(c, g, q, 1, o, false, qr);
+    if (qr[0].status != GPS_OK) fail(qr[0].status, qr[0].error);
+    QueryResult pr;
+    pr.cols = kp;
+    pr.rows = project_unique(c, qr[0].data, qr[0].rows, qr[0].cols, cols, kp, out ? &pr.block : nullptr);
+    pr.global_rows = pr.rows;
+    if (pr.block) pr.data = static_cast<const uint32_t*>(pr.block->p);
+    qr.clear();
+    if (count) *count = pr.rows;
+    if (out) *out = wrap_result(c, pr, o.result_on_device != 0);
+    ctx_sync(c);
+}
+
+gps_status gps_match_project(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
+                             uint32_t kp, const int32_t* cols, gps_result** out) {
+    return guarded([&] {
+        if (!out) fail(GPS_EINVAL, "null out");
+        project_call(c, g, q, opts, kp, cols, out, nullptr);
+    });
+}
+
+gps_status gps_count_project(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
+                             uint32_t kp, const int32_t* cols, uint64_t* count) {
+    return guarded([&] {
+        if (!count) fail(GPS_EINVAL, "null count");
+        project_call(c, g, q, opts, kp, cols, nullptr, count);
     });
 }
 

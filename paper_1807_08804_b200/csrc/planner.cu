@@ -109,6 +109,40 @@ Plan make_plan(const gps_query* q, uint32_t n, bool undirected, const std::vecto
         p.order.push_back(0);
         p.discovery.push_back(0);
         inT = 1u;
+    } else if (o.plan_mode == GPS_PLAN_COMMONSENSE) {
+        // P:937-939 (commonsense queries): the concept (bound) node of maximum degree first (no
+        // concept node: the vertex of maximum degree); then, among the vertices adjacent to the
+        // order, the one with the most neighbours not yet in the order; until the order's edges
+        // cover the query graph.  Ties -> lowest id.
+        int u = -1;
+        for (int x = 0; x < (int)k; x++) {
+            const bool cx = p.bound[x] >= 0, cu = u >= 0 && p.bound[u] >= 0;
+            if (u < 0 || (cx && !cu) || (cx == cu && p.deg[x] > p.deg[u])) u = x;
+        }
+        uint32_t inO = 1u << u;
+        p.order.push_back(u);
+        p.discovery.push_back(u);
+        inT |= 1u << u;
+        add_vertex_edges(u);
+        auto covered = [&]() {
+            for (const QArc& a : p.arcs)
+                if (!(inO >> a.a & 1u) && !(inO >> a.b & 1u)) return false;
+            return true;
+        };
+        while (!covered()) {
+            int pick = -1, best = -1;
+            for (int x = 0; x < (int)k; x++) {
+                if ((inO >> x & 1u) || !(inT >> x & 1u)) continue;
+                const int outside = __builtin_popcount(adj[x] & ~inO);
+                if (outside > best) {
+                    best = outside;
+                    pick = x;
+                }
+            }
+            inO |= 1u << pick;
+            p.order.push_back(pick);
+            add_vertex_edges(pick);
+        }
     } else {
         int best_a = -1, best_b = -1;
         Rat best{0, 1};

@@ -22,6 +22,8 @@ GPS_OK, GPS_EINVAL, GPS_EDISCONNECTED, GPS_ENOMEM, GPS_ECUDA, GPS_ENCCL, GPS_EOV
 GPS_ANY = -1
 GPS_FREE = -1
 GPS_DIRECTED, GPS_UNDIRECTED = 0, 1
+GPS_REFINE_UNTIL_STABLE = 0xFFFFFFFF
+GPS_PLAN_RANKING, GPS_PLAN_COMMONSENSE = 0, 1
 KERNEL_CLASSES = ["check", "collect", "explore", "bitand", "ec_count", "ec_write", "scan", "join_len",
                   "join_count", "join_write", "load", "propagate", "clear"]
 NK = len(KERNEL_CLASSES)
@@ -63,7 +65,8 @@ class QueryDesc(ctypes.Structure):
 class MatchOpts(ctypes.Structure):
     _fields_ = [("refine_rounds", ctypes.c_uint32), ("reverse_refine", ctypes.c_int32),
                 ("lowconn_threshold", ctypes.c_uint32), ("result_on_device", ctypes.c_int32),
-                ("rebalance_threshold", ctypes.c_float), ("row_budget_bytes", ctypes.c_uint64)]
+                ("rebalance_threshold", ctypes.c_float), ("plan_mode", ctypes.c_int32),
+                ("row_budget_bytes", ctypes.c_uint64)]
 
 
 class Stats(ctypes.Structure):
@@ -108,6 +111,9 @@ def _load_lib():
         "gps_result_global_rows": (S, [P, P]),
         "gps_local_comm_create": (S, [ctypes.c_int, P]),
         "gps_shard_plan": (S, [ctypes.c_int, ctypes.c_int, P, ctypes.c_float, P, P, P]),
+        "gps_load_triples": (S, [P, ctypes.c_uint32, ctypes.c_uint64, P, P, P, P, ctypes.c_uint32, P]),
+        "gps_match_project": (S, [P, P, P, P, ctypes.c_uint32, P, P]),
+        "gps_count_project": (S, [P, P, P, P, ctypes.c_uint32, P, P]),
         "gps_shard_recv": (S, [ctypes.c_int, ctypes.c_int, P, P, P]),
         "gps_local_comm_destroy": (S, [P]),
         "gps_create_local_rank": (S, [P, P, ctypes.c_int, P]),
@@ -125,7 +131,8 @@ EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_grap
             "gps_result_free", "gps_result_free_after", "gps_last_error", "gps_get_stats", "gps_reset_stats",
             "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates", "gps_match_batch",
             "gps_count_batch", "gps_set_workers", "gps_set_slice", "gps_match_batch_host",
-            "gps_result_global_rows", "gps_shard_plan", "gps_shard_recv", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
+            "gps_result_global_rows", "gps_shard_plan", "gps_shard_recv", "gps_load_triples",
+            "gps_match_project", "gps_count_project", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
 
 
 def _check(st: int):
@@ -147,7 +154,7 @@ def default_opts(**kw) -> MatchOpts:
 
 def _with_device(o: MatchOpts, on_device: bool) -> MatchOpts:
     return MatchOpts(o.refine_rounds, o.reverse_refine, o.lowconn_threshold, 1 if on_device else 0,
-                     o.rebalance_threshold, o.row_budget_bytes)
+                     o.rebalance_threshold, o.plan_mode, o.row_budget_bytes)
 
 
 class _QueryArrays:
@@ -417,6 +424,43 @@ class Context:
         """From a synth.DataGraph-like object (n, to_csr(), vlab, undirected)."""
         off, tgt, el = g.to_csr()
         return self.load_graph_csr(g.n, off, tgt, el, g.vlab, g.undirected)
+
+    def load_triples(self, n, subject, relation, obj, vertex_labels=None, undirected=False) -> Graph:
+        """A knowledge base as (subject, relation, object) triples (f2)."""
+        su = np.ascontiguousarray(subject, np.uint32)
+        ob = np.ascontiguousarray(obj, np.uint32)
+        rl = None if relation is None else np.ascontiguousarray(relation, np.uint16)
+        vl = None if vertex_labels is None else np.ascontiguousarray(vertex_labels, np.uint16)
+        h = ctypes.c_void_p()
+        _check(lib.gps_load_triples(self._h, int(n), int(su.shape[0]), _addr(su), _addr(rl), _addr(ob), _addr(vl),
+                                    GPS_UNDIRECTED if undirected else GPS_DIRECTED, ctypes.byref(h)))
+        return Graph(self, h)
+
+    def match_project(self, graph: Graph, q, project, opts: Optional[MatchOpts] = None) -> np.ndarray:
+        """Distinct projections of the embeddings onto the query vertices `project` (f2, P:826,
+        P:937), lexicographically sorted, as a (rows, len(project)) uint32 numpy array."""
+        qa = _QueryArrays(q)
+        pj = np.ascontiguousarray(project, np.int32)
+        o = _with_device(opts if opts is not None else default_opts(), False)
+        res = ctypes.c_void_p()
+        _check(lib.gps_match_project(self._h, graph.handle, ctypes.byref(qa.desc), ctypes.byref(o), pj.shape[0],
+                                     _addr(pj), ctypes.byref(res)))
+        rows, cols, ptr, ondev = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_void_p(), ctypes.c_int()
+        lib.gps_result_info(res, ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(ptr), ctypes.byref(ondev))
+        a = np.zeros((rows.value, cols.value), np.uint32)
+        if rows.value:
+            ctypes.memmove(a.ctypes.data, ptr.value, rows.value * cols.value * 4)
+        lib.gps_result_free(res)
+        return a
+
+    def count_project(self, graph: Graph, q, project, opts: Optional[MatchOpts] = None) -> int:
+        qa = _QueryArrays(q)
+        pj = np.ascontiguousarray(project, np.int32)
+        c = ctypes.c_uint64()
+        _check(lib.gps_count_project(self._h, graph.handle, ctypes.byref(qa.desc),
+                                     ctypes.byref(opts) if opts is not None else None, pj.shape[0], _addr(pj),
+                                     ctypes.byref(c)))
+        return int(c.value)
 
     # ---- queries ----
     def match(self, graph: Graph, q, opts: Optional[MatchOpts] = None, device: bool = True):

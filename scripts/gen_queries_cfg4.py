@@ -7,7 +7,7 @@ from the fully labelled query, vertex labels are replaced by '*' one at a time i
 seeded order (a replacement that makes the oracle exceed its limits is undone; the
 fully labelled query is tried first) until
 the oracle's largest BFS-prefix table (#embeddings of the sub-query induced on a BFS
-prefix, oracle.run levels) reaches PEAK rows; accepted iff that happens with
+prefix of >= 2 vertices, oracle.run levels[1:]) reaches PEAK rows; accepted iff that happens with
 #Emb <= 10^8.  Every oracle run uses the OpenMP variant on all host cores.  Stored with
 the oracle's count, multiset hash and per-depth table sizes; the file is rewritten
 after every acceptance, so a run cut short keeps what it found.
@@ -32,6 +32,12 @@ from oracle import oracle  # noqa: E402
 
 RECIPE = dict(cfg=4, k=(6, 7, 8), seed0=4000, induced=True, max_children=2, keep_elabels=True,
               prefer_hubs=True, top_fraction=0.1, hi=10**8, work_per_thread=200_000_000)
+
+
+def peak_of(res) -> int:
+    """Largest BFS-prefix table of 2+ vertices (the first level is just the root's candidates:
+    all n data vertices when the root is a wildcard)."""
+    return max(res["levels"][1:]) if len(res["levels"]) > 1 else 0
 
 
 def main():
@@ -59,8 +65,8 @@ def main():
         got = None
         trace = []
         res = oracle.run(og, q, threads=threads, limit=r["hi"])   # the fully labelled query first
-        trace.append((-1, res["count"], max(res["levels"]) if res["count"] >= 0 else -1))
-        if res["count"] >= 0 and max(res["levels"]) >= r["peak"]:
+        trace.append((-1, res["count"], peak_of(res) if res["count"] >= 0 else -1))
+        if res["count"] >= 0 and peak_of(res) >= r["peak"]:
             got = (q, res)
             perm = []
         elif res["count"] < 0:
@@ -70,11 +76,11 @@ def main():
             trial[int(u)] = -1
             qt = Query(q.k, trial, q.bound, q.edges)
             res = oracle.run(og, qt, threads=threads, limit=r["hi"])
-            trace.append((int(u), res["count"], max(res["levels"]) if res["count"] >= 0 else -1))
+            trace.append((int(u), res["count"], peak_of(res) if res["count"] >= 0 else -1))
             if res["count"] < 0:
                 continue
             vl = trial
-            if max(res["levels"]) >= r["peak"]:
+            if peak_of(res) >= r["peak"]:
                 got = (qt, res)
                 break
             if time.time() - t0 > budget_s:

@@ -131,10 +131,15 @@ def main():
                       f"{g('launch__registers_per_thread'):.0f} | "
                       f"{g('smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio'):.2f} | "
                       f"{g('smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio'):.2f} |")
-            per[klass(e["kernel"])].append(e.get("dram__bytes_read.sum", 0) + e.get("dram__bytes_write.sum", 0))
+            per[klass(e["kernel"])].append((e.get("dram__bytes_read.sum", 0) + e.get("dram__bytes_write.sum", 0),
+                                           e.get("lts__t_sector_hit_rate.pct", float("nan")),
+                                           e.get("gpu__time_duration.sum", 0.0)))
         pre = os.environ.get("TRAFFIC_PREFIX", "")
         for c, v in per.items():
-            traffic[pre + c] = sum(v) / len(v)
+            traffic[pre + c] = sum(x[0] for x in v) / len(v)   # DRAM bytes per launch
+            tw = sum(x[2] for x in v)
+            if tw > 0:   # duration-weighted L2 hit rate of the class
+                traffic[pre + c + ":l2_hit_pct"] = sum(x[1] * x[2] for x in v if x[1] == x[1]) / tw
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     open(os.path.join(prof, f"{rnd}_summary.md"), "w").write("\n".join(md) + "\n")
     print("\n".join(md[:40]))
