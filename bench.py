@@ -37,9 +37,10 @@ WORKLOADS = {
     2: f"cfg2: {GRAPH}, 100 six-vertex BFS tree queries per step, gps_match with device-resident results",
     3: f"cfg3: {GRAPH}, 30 cyclic 8/10/12-vertex queries (dense hub core) per step, device-resident results",
     5: f"cfg5: {GRAPH}, QA batch of 10000 3-5-vertex queries with a bound concept vertex per step",
-    4: "cfg4: Chung-Lu graph n=20000000 m=100000000 labelled arcs (HBM-resident CSR); per step gps_match of "
-       "the stored 6/7/8-vertex cyclic queries (synth/data/cfg4_queries.json, oracle BFS-prefix tables "
-       ">= 1e9 rows), rows sharded over the GPUs",
+    4: "cfg4: Chung-Lu graph n=20000000 m=100000000 labelled arcs (HBM-resident CSR); per step the "
+       "closed-form joins (out-star-2, in-star-2, 2-path: 2.5e8 rows written; out-star-3: 3.2e9 counted) and "
+       "gps_match of the 6 stored 6/7/8-vertex cyclic queries (synth/data/cfg4_queries.json); rows sharded "
+       "over the GPUs when N > 1",
 }
 CONFIG = 2
 
@@ -48,7 +49,19 @@ def load_queries(cfg=None):
     from synth import Query
     cfg = CONFIG if cfg is None else cfg
     data = json.load(open(os.path.join(ROOT, "synth", "data", f"cfg{cfg}_queries.json")))
-    return [Query.from_json(d["query"]) for d in data["queries"]], [d["oracle_count"] for d in data["queries"]]
+    qs, cs = [Query.from_json(d["query"]) for d in data["queries"]], [d["oracle_count"] for d in data["queries"]]
+    if cfg == 4:   # + the closed-form-pinned large joins (tests/test_gpu_large.py): the HBM-sized tables
+        from synth.large import CFG4
+        qs = [q for _, q, _ in CFG4] + qs
+        cs = [None] * len(CFG4) + cs
+    return qs, cs
+
+
+def cfg4_modes():
+    """Config 4 step: gps_match of every query except the closed-form out-star-3 (3.2e9
+    embeddings: gps_count, its last level is never written)."""
+    from synth.large import CFG4
+    return [m for _, _, m in CFG4] + ["match"] * (len(load_queries(4)[0]) - len(CFG4))
 
 
 def sample_order(n: int):
@@ -182,6 +195,16 @@ def run_reference(args, rank, world):
         return
     queries, _ = load_queries()
     g = config_graph(4 if CONFIG == 4 else 2)
+    if CONFIG == 4:   # one full oracle enumeration takes minutes: first-column partitions (cfg4_cpu_baseline)
+        cb = cfg4_cpu_baseline(g, queries, args.steps * args.ref_step_budget)
+        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "queries/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / cb["value"] * len(queries),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "data": "synthetic", "config": {"workload": WORKLOADS[CONFIG], "sample": cb["sample"]},
+                "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     og = oracle.OracleGraph(g)
     order = sample_order(len(queries))
     per_step = max(1, args.ref_queries_per_step)
@@ -303,10 +326,15 @@ def main():
         ctx.set_workers(args.workers)
         ctx.set_slice(args.slice)
 
+    modes = cfg4_modes() if CONFIG == 4 else None
+
     def step():
         if CONFIG == 4:   # each query's rows stay on the device (sharded: this rank's shard)
             emb = 0
-            for q in queries:
+            for q, mode in zip(queries, modes):
+                if mode == "count":
+                    emb += ctx.count(G, q)
+                    continue
                 br = ctx.match_batch_raw(G, [q])
                 emb += int(br.rows().sum())
                 br.free()
@@ -375,14 +403,15 @@ def main():
 
         # e2e: the same step through the C-ABI with a HOST result buffer (copies inside the region)
         local_rows = counts if not sharded else [None] * len(queries)
-        if CONFIG == 4:   # every query's (local) rows into one pinned buffer, one query at a time
-            local_rows = [int(ctx.count(G, q)) if not sharded else None for q in queries]
-            if sharded:
-                local_rows = []
-                for q in queries:
-                    a = ctx.match_batch_raw(G, [q])
-                    local_rows.append(int(a.rows().sum()))
-                    a.free()
+        if CONFIG == 4:   # every written query's (local) rows into one pinned buffer, one query at a time
+            local_rows = []
+            for q, mode in zip(queries, modes):
+                if mode == "count":
+                    local_rows.append(0)
+                    continue
+                a = ctx.match_batch_raw(G, [q])
+                local_rows.append(int(a.rows().sum()))
+                a.free()
             total_words = max(c * q.k for c, q in zip(local_rows, queries))
         else:
             total_words = sum(c * q.k for c, q in zip(local_rows, queries))
@@ -397,8 +426,11 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             if CONFIG == 4:
-                for q in queries:
-                    ctx.match_host(G, q, pinned)
+                for q, mode in zip(queries, modes):
+                    if mode == "count":
+                        ctx.count(G, q)
+                    else:
+                        ctx.match_host(G, q, pinned)
             elif batch_api:
                 ctx.match_batch_host(G, qbatch, pinned)     # library copies every result into `pinned`
             else:

@@ -534,7 +534,8 @@ static void project_call(gps_ctx* c, const gps_graph* g, const gps_query* q, con
     if (qr[0].status != GPS_OK) fail(qr[0].status, qr[0].error);
     QueryResult pr;
     pr.cols = kp;
-    pr.rows = project_unique(c, qr[0].data, qr[0].rows, qr[0].cols, cols, kp, out ? &pr.block : nullptr);
+    pr.rows = project_unique(c, qr[0].data, qr[0].rows, qr[0].cols, cols, kp, g->d.n ? g->d.n - 1 : 0,
+                             out ? &pr.block : nullptr);
     pr.global_rows = pr.rows;
     if (pr.block) pr.data = static_cast<const uint32_t*>(pr.block->p);
     qr.clear();

@@ -10,6 +10,8 @@
 //                  sort by column, so after kp passes the rows are in lexicographic order
 //   k_gather       rows in sorted order; k_mark: first row of each run of equal rows;
 //                  exclusive scan; k_compact: one row per run.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "runtime.h"
 
@@ -31,19 +33,21 @@ __global__ void k_project(const uint32_t* __restrict__ in, uint64_t R, uint32_t 
     for (uint32_t j = 0; j < pc.n; j++) out[i * pc.n + j] = __ldg(in + i * k + pc.col[j]);
 }
 
+// key = value << pbits | position (position < 2^pbits): sorting the key sorts by value,
+// ties kept in the current order (a stable sort by this column)
 __global__ void k_sort_keys(const uint32_t* __restrict__ P, const uint32_t* __restrict__ perm, uint64_t R,
-                            uint32_t kp, uint32_t col, uint64_t* __restrict__ keys) {
+                            uint32_t kp, uint32_t col, uint32_t pbits, uint64_t* __restrict__ keys) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R) return;
     const uint32_t r = perm ? perm[i] : (uint32_t)i;
-    keys[i] = ((uint64_t)__ldg(P + (uint64_t)r * kp + col) << 32) | i;
+    keys[i] = ((uint64_t)__ldg(P + (uint64_t)r * kp + col) << pbits) | i;
 }
 
 __global__ void k_compose(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ perm, uint64_t R,
-                          uint32_t* __restrict__ nperm) {
+                          uint32_t pbits, uint32_t* __restrict__ nperm) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R) return;
-    const uint32_t pos = (uint32_t)(keys[i] & 0xffffffffu);
+    const uint32_t pos = (uint32_t)(keys[i] & ((1ull << pbits) - 1));
     nperm[i] = perm ? perm[pos] : pos;
 }
 
@@ -83,7 +87,7 @@ uint32_t bits_for(uint64_t x) {
 // Distinct projections of R rows of k columns (device, row-major) onto cols[0..kp); the
 // result rows (row-major R' x kp, lexicographic order) go to *out (nullptr: count only).
 uint64_t project_unique(gps_ctx* c, const uint32_t* rows, uint64_t R, uint32_t k, const int32_t* cols, uint32_t kp,
-                        Block* out) {
+                        uint32_t vmax, Block* out) {
     if (kp == 0 || kp > kProjMax) fail(GPS_EINVAL, "projection must name 1..32 query vertices");
     ProjCols pc{};
     pc.n = kp;
@@ -93,6 +97,7 @@ uint64_t project_unique(gps_ctx* c, const uint32_t* rows, uint64_t R, uint32_t k
     }
     if (R == 0) return 0;
     if (R >= (1ull << 32)) fail(GPS_EUNSUPPORTED, "projection of more than 2^32 embeddings");
+    if (bits_for(R - 1) + bits_for(vmax) > 64) fail(GPS_EUNSUPPORTED, "projection sort key wider than 64 bits");
     const uint32_t T = 256;
     const dim3 g((uint32_t)((R + T - 1) / T));
     DevPtr P(c, sizeof(uint32_t) * R * kp);
@@ -101,13 +106,14 @@ uint64_t project_unique(gps_ctx* c, const uint32_t* rows, uint64_t R, uint32_t k
     DevPtr pa(c, sizeof(uint32_t) * R), pb(c, sizeof(uint32_t) * R);
     uint32_t* perm = nullptr;
     uint32_t* next = pa.as<uint32_t>();
-    const int nbits = 32 + (int)bits_for(R - 1);
+    const uint32_t pbits = std::max<uint32_t>(1, bits_for(R - 1));            // positions
+    const int nbits = (int)(pbits + bits_for(vmax));                            // + vertex ids
     for (int j = (int)kp - 1; j >= 0; j--) {   // LSD: stable sort by each column from the last
         launch(c, GPS_K_JOIN_WRITE, g, dim3(T), 0, k_sort_keys, (const uint32_t*)P.as<uint32_t>(), (const uint32_t*)perm,
-               R, kp, (uint32_t)j, keys.as<uint64_t>());
+               R, kp, (uint32_t)j, pbits, keys.as<uint64_t>());
         radix_sort_u64(c, keys.as<uint64_t>(), tmp.as<uint64_t>(), R, nbits);
         launch(c, GPS_K_JOIN_WRITE, g, dim3(T), 0, k_compose, (const uint64_t*)keys.as<uint64_t>(),
-               (const uint32_t*)perm, R, next);
+               (const uint32_t*)perm, R, pbits, next);
         perm = next;
         next = perm == pa.as<uint32_t>() ? pb.as<uint32_t>() : pa.as<uint32_t>();
     }

@@ -49,7 +49,7 @@ void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t n
 // f2: distinct projections of R device rows (k columns) onto cols[0..kp), lexicographic
 // order, into *out (nullptr: count only); returns their number (project.cu).
 uint64_t project_unique(gps_ctx* c, const uint32_t* rows, uint64_t R, uint32_t k, const int32_t* cols, uint32_t kp,
-                        Block* out);
+                        uint32_t vmax, Block* out);
 
 // Filter only (debug entry point): candidate bitmaps after stage 0/1/2 to host.
 void run_filter_debug(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts& o, int stage,

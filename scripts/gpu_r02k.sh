@@ -1,0 +1,4 @@
+(timeout 900 python -m pytest tests/test_gpu_commonsense.py tests/test_gpu_parity.py -m gpu -x -q > gpurun_out/gpu_tests_k.log 2>&1; echo exit $? >> gpurun_out/gpu_tests_k.log)
+tail -3 gpurun_out/gpu_tests_k.log
+CLASSES=1 timeout 600 python scripts/ncu_cfg4.py 2>&1 | tail -12
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed --clock-control none -k regex:"k_join_fast|k_join_seg" --csv python scripts/ncu_cfg4.py 2>/dev/null | grep -E "k_join" | awk -F'","' '{print $5, $(NF-2), $(NF)}' | sed 's/"//g' | head -40
