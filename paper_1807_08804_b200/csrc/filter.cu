@@ -118,12 +118,15 @@ __global__ void __launch_bounds__(kColThreads, 5) k_collect(DevGraph g, const Co
     const uint32_t tile = lb_ticket(lb.ctr + 3 * y, ntiles);
     const uint32_t w0 = tile * kColTile + threadIdx.x * kColWords;
     uint32_t word[kColWords];
-    if (w0 < g.nw) {   // nws >= nw rounded up to 64 words: the vector load stays in bounds
+    if (w0 + 3 < g.nw) {   // one 16-byte load of 4 words
         const uint4 b4 = *reinterpret_cast<const uint4*>(J.B + w0);
         word[0] = b4.x;
-        word[1] = w0 + 1 < g.nw ? b4.y : 0u;
-        word[2] = w0 + 2 < g.nw ? b4.z : 0u;
-        word[3] = w0 + 3 < g.nw ? b4.w : 0u;
+        word[1] = b4.y;
+        word[2] = b4.z;
+        word[3] = b4.w;
+    } else if (w0 < g.nw) {   // the last words: never read the (unwritten) row padding
+#pragma unroll
+        for (int i = 0; i < kColWords; i++) word[i] = w0 + i < g.nw ? J.B[w0 + i] : 0u;
     } else {
         word[0] = word[1] = word[2] = word[3] = 0u;
     }

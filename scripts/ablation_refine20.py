@@ -19,18 +19,24 @@ import torch  # noqa: E402
 from synth import bfs_query, config_graph  # noqa: E402
 from paper_1807_08804_b200 import gpsense  # noqa: E402
 
+# the four versions of P:1008 (until convergence; until convergence reversed; one round reversed --
+# the default; none) plus one round forward
 VARIANTS = [("none", dict(refine_rounds=0)), ("1 round reversed (default)", dict(refine_rounds=1, reverse_refine=1)),
-            ("1 round forward", dict(refine_rounds=1, reverse_refine=0)),
-            ("4 rounds reversed", dict(refine_rounds=4, reverse_refine=1))]
+            ("until stable", dict(refine_rounds=0xFFFFFFFF, reverse_refine=0)),
+            ("until stable reversed", dict(refine_rounds=0xFFFFFFFF, reverse_refine=1)),
+            ("1 round forward", dict(refine_rounds=1, reverse_refine=0))]
 
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+    only = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else None
     g = config_graph(2)
     ctx = gpsense.Context(0)
     G = ctx.load_graph(g)
     rows = []
     for i in range(n):
+        if only is not None and i not in only:
+            continue
         k = (16, 20)[i % 2]
         q = bfs_query(g, k, 6000 + i, induced=True, max_children=2, prefer_hubs=True, top_fraction=0.01,
                       keep_elabels=False, p_wild_v=0.0)
