@@ -72,9 +72,10 @@ static void fault_injection() {
 
 // The library's own stream-ordered memory pool per device (never the device's default
 // pool, whose attributes other users of the process own).  Freed blocks stay cached
-// up to GPS_POOL_KEEP_BYTES (default 64 GiB) across synchronisations, so a steady
-// stream of same-sized queries reuses memory without driver calls; anything above is
-// returned to the driver at the next synchronisation.
+// up to GPS_POOL_KEEP_BYTES (default three quarters of the device memory) across
+// synchronisations, so a steady stream of queries reuses memory without driver calls;
+// anything above is returned to the driver at the next synchronisation, and all of it
+// when the process ends.
 cudaMemPool_t device_pool(int dev) {
     static std::mutex mu;
     static std::map<int, cudaMemPool_t> pools;
@@ -89,7 +90,18 @@ cudaMemPool_t device_pool(int dev) {
     cudaMemPool_t pool;
     GPS_CK(cudaMemPoolCreate(&pool, &props));
     const char* e = std::getenv("GPS_POOL_KEEP_BYTES");
-    uint64_t keep = (e && *e) ? std::strtoull(e, nullptr, 10) : (64ull << 30);
+    uint64_t keep = 64ull << 30;
+    if (e && *e) {
+        keep = std::strtoull(e, nullptr, 10);
+    } else {   // three quarters of the device: trimming below the working set of a large join
+        size_t fr = 0, tot = 0;   // re-maps tens of GB on the next step (0.3-0.7 s stalls, config 3)
+        int prev = -1;
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) keep = (uint64_t)tot / 4 * 3;
+        else (void)cudaGetLastError();
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
     GPS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     pools[dev] = pool;
     return pool;
