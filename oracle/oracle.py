@@ -185,3 +185,47 @@ def row_hash_py(row) -> int:
 
 def multiset_hash_py(rows) -> int:
     return sum(row_hash_py(r) for r in rows) & _M64
+
+
+def match_named(g, og: OracleGraph, q, edge_var, project=None) -> np.ndarray:
+    """Named variable edges (f2; "each variable-edge name as a binding reported in
+    output, with equal names constrained equal"; DESIGN reading R32).  edge_var[e] >= 0 names
+    query edge e (its label must be ANY), -1 leaves it unnamed.
+
+    Plain definition: the set of tuples (f(project...), beta(v_0), beta(v_1), ...) -- the
+    variables v_i in increasing id order -- over every embedding f (Def. 2, with the
+    named edges as variable edges) and every assignment beta of labels to the variables
+    such that each edge e = (a, b) named v has an arc f(a) -> f(b) labelled beta(v).  Rows are
+    distinct and lexicographically sorted.  The arc labels come from the raw edge list g."""
+    import itertools
+    edges = [tuple(e) for e in q.edges]
+    if len(edge_var) != len(edges):
+        raise ValueError("edge_var needs one entry per query edge")
+    names = sorted({int(v) for v in edge_var if v >= 0})
+    for e, v in zip(edges, edge_var):
+        if v >= 0 and e[2] != -1:
+            raise ValueError("a named edge must be a variable (ANY) edge")
+    proj = list(range(q.k)) if project is None else [int(x) for x in project]
+    labels = {}   # (a, b) -> set of arc labels, from the raw edge list
+    el = np.zeros(len(g.src), np.int64) if g.elab is None else np.asarray(g.elab, np.int64)
+    for s, d, l in zip(np.asarray(g.src, np.int64), np.asarray(g.dst, np.int64), el):
+        labels.setdefault((int(s), int(d)), set()).add(int(l))
+        if g.undirected:
+            labels.setdefault((int(d), int(s)), set()).add(int(l))
+    out = set()
+    for f in match(og, q):
+        choices = []
+        for v in names:
+            s = None
+            for (a, b, _), ev in zip(edges, edge_var):
+                if ev == v:
+                    ls = labels.get((int(f[a]), int(f[b])), set())
+                    s = set(ls) if s is None else s & ls
+            choices.append(sorted(s))
+        head = tuple(int(f[c]) for c in proj)
+        for beta in itertools.product(*choices):
+            out.add(head + beta)
+    width = len(proj) + len(names)
+    if not out:
+        return np.zeros((0, width), np.uint32)
+    return np.array(sorted(out), np.uint32).reshape(-1, width)

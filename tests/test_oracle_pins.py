@@ -309,3 +309,77 @@ def test_closed_forms_large_families_vs_oracle(seed):
         assert oracle.count(og, out_star(k, la, lb)) == cf.out_star(g, keys, k, la, lb)
         assert oracle.count(og, in_star(k, la, lb)) == cf.in_star(g, keys, k, la, lb)
         assert oracle.count(og, path2(la, lb, lc)) == cf.path2(g, keys, la, lb, lc)
+
+
+# ---------------------------------------------------------------- f2 named variable edges
+def brute_force_named(g: DataGraph, q: Query, edge_var, project):
+    """Every injective map V_q -> V_g and every assignment of present labels to the named
+    variables, kept when Def. 2 holds with each named edge carrying its variable's label."""
+    arcs, pairs = set(), set()
+    lab = g.elab if g.elab is not None else np.zeros(g.m, np.uint16)
+    for s, d, l in zip(g.src.tolist(), g.dst.tolist(), lab.tolist()):
+        arcs.add((s, d, l)); pairs.add((s, d))
+        if g.undirected:
+            arcs.add((d, s, l)); pairs.add((d, s))
+    present = sorted(set(lab.tolist())) or [0]
+    names = sorted({v for v in edge_var if v >= 0})
+    vl = g.vlab.tolist() if g.vlab is not None else [0] * g.n
+    out = set()
+    for f in itertools.permutations(range(g.n), q.k):
+        if any(q.vlabels[u] != -1 and q.vlabels[u] != vl[f[u]] for u in range(q.k)):
+            continue
+        if any(q.bound[u] != -1 and q.bound[u] != f[u] for u in range(q.k)):
+            continue
+        for beta in itertools.product(present, repeat=len(names)):
+            ok = True
+            for (a, b, l), v in zip(q.edges, edge_var):
+                if v >= 0:
+                    ok = (f[a], f[b], beta[names.index(v)]) in arcs
+                elif l == -1:
+                    ok = (f[a], f[b]) in pairs
+                else:
+                    ok = (f[a], f[b], l) in arcs
+                if not ok:
+                    break
+            if ok:
+                out.add(tuple(f[p] for p in project) + tuple(beta))
+    w = len(project) + len(names)
+    return np.array(sorted(out), np.uint32).reshape(-1, w)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_oracle_named_edges_equal_brute_force(seed):
+    rng = np.random.default_rng(5000 + seed)
+    n = int(rng.integers(4, 7))
+    g = random_multigraph(n, int(rng.integers(2 * n, 4 * n)), n_elabels=3, n_vlabels=2,
+                          seed=seed, undirected=seed % 4 == 0, dup_prob=0.4)
+    k = int(rng.integers(2, min(4, n) + 1))
+    q = random_connected_query(rng, k, extra=int(rng.integers(0, 2)), n_elabels=3, n_vlabels=2,
+                               p_wild_v=0.6, p_wild_e=0.8)
+    # name some of the variable edges, from a pool of 2 names (so names repeat)
+    ev = [int(rng.integers(0, 2)) if (l == -1 and rng.random() < 0.7) else -1 for (_, _, l) in q.edges]
+    proj = sorted(rng.choice(k, size=int(rng.integers(1, k + 1)), replace=False).tolist())
+    got = oracle.match_named(g, oracle.OracleGraph(g), q, ev, proj)
+    want = brute_force_named(g, q, ev, proj)
+    assert _eq(got, want), (seed, got.shape, want.shape)
+
+
+def test_oracle_named_edges_worked_example():
+    """Hand-worked (P:592-594 reading): data arcs person -eats(1)-> bread, person -eats(1)-> soup,
+    person -likes(2)-> soup, cook -makes(3)-> soup, cook -makes(3)-> bread.  Query ?p -?x-> ?f <-?y- ?c
+    with ?x, ?y distinct names: ?p = person (0), ?c = cook (3):  f = soup: x in {eats, likes},
+    y = makes; f = bread: x = eats, y = makes.  With ?x = ?y (one name) nothing matches (no label
+    both eats/likes and makes).  Projection onto ?f only: (bread, 1, 3), (soup, 1, 3), (soup, 2, 3)."""
+    person, bread, soup, cook = 0, 1, 2, 3
+    src = np.array([person, person, person, cook, cook], np.uint32)
+    dst = np.array([bread, soup, soup, soup, bread], np.uint32)
+    el = np.array([1, 1, 2, 3, 3], np.uint16)
+    g = DataGraph(4, src, dst, el, None, False)
+    q = Query(3, [-1, -1, -1], [person, -1, cook], [(0, 1, -1), (2, 1, -1)])
+    og = oracle.OracleGraph(g)
+    rows = oracle.match_named(g, og, q, [0, 1])
+    assert rows.tolist() == [[person, bread, cook, 1, 3], [person, soup, cook, 1, 3], [person, soup, cook, 2, 3]]
+    assert oracle.match_named(g, og, q, [0, 0]).shape == (0, 4)
+    assert oracle.match_named(g, og, q, [0, 1], [1]).tolist() == [[bread, 1, 3], [soup, 1, 3], [soup, 2, 3]]
+    # one named edge, one plain variable edge: the plain one binds nothing
+    assert oracle.match_named(g, og, q, [-1, 7], [1]).tolist() == [[bread, 3], [soup, 3]]
