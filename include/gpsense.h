@@ -254,6 +254,27 @@ GPS_API gps_status gps_match_project(gps_ctx* ctx, const gps_graph* g, const gps
                                      uint32_t n_project, const int32_t* project, gps_result** out);
 GPS_API gps_status gps_count_project(gps_ctx* ctx, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
                                      uint32_t n_project, const int32_t* project, uint64_t* count);
+/* gps_match_named: NAMED variable edges ("query edges are also categorized into variable
+ *   and labeled edges", "2 variable edges: ?x, ?y"; "each variable-edge name as a
+ *   binding reported in output, with equal names constrained equal"; DESIGN reading R32).
+ *   edge_var [q->n_edges] (host): a name id >= 0 for a variable edge (its label must be
+ *   GPS_ANY), -1 for an edge without a name.  Let v_0 < v_1 < ... < v_{V-1} be the distinct
+ *   ids.  The result is the set of distinct tuples (f(project[0]), ..., f(project[n_project-1]),
+ *   beta(v_0), ..., beta(v_{V-1})) over every embedding f (Def. 2) and every assignment beta of
+ *   edge labels to the names such that each edge e = (a, b) named v has an arc f(a) -> f(b)
+ *   labelled beta(v); lexicographic order, (n_project or k) + V columns (n_project = 0 and
+ *   project = NULL: all k query vertices).  Computed on the device by instantiating the query
+ *   for every assignment of the labels present in g (one batch) and deduplicating.
+ *   Errors: GPS_EINVAL (named edge with a label, projected vertex out of range, more than 32
+ *   columns), GPS_EUNSUPPORTED (V > 8, more than 65536 assignments, row-sharded ctx, more than
+ *   2^32 rows before deduplication), plus gps_match's.
+ * gps_count_named: the number of such tuples. */
+GPS_API gps_status gps_match_named(gps_ctx* ctx, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
+                                   const int32_t* edge_var, uint32_t n_project, const int32_t* project,
+                                   gps_result** out);
+GPS_API gps_status gps_count_named(gps_ctx* ctx, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
+                                   const int32_t* edge_var, uint32_t n_project, const int32_t* project,
+                                   uint64_t* count);
 
 /* rows, cols (= k), data (device or host pointer, owned by the result), on_device. */
 GPS_API gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols,

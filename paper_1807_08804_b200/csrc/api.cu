@@ -560,6 +560,48 @@ gps_status gps_count_project(gps_ctx* c, const gps_graph* g, const gps_query* q,
     });
 }
 
+static void named_call(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
+                       const int32_t* edge_var, uint32_t kp, const int32_t* cols, gps_result** out, uint64_t* count) {
+    check_args(c, g);
+    if (!q) fail(GPS_EINVAL, "null query");
+    if (kp && !cols) fail(GPS_EINVAL, "null projection");
+    if (c->comm) fail(GPS_EUNSUPPORTED, "named edges with a row-sharded ctx");
+    DeviceGuard dg(c->device);
+    const gps_match_opts o = resolve_opts(opts);
+    QueryResult pr;
+    uint32_t V = 0;
+    {
+        std::vector<int32_t> ids;
+        for (uint32_t e = 0; e < q->n_edges && edge_var; e++)
+            if (edge_var[e] >= 0) ids.push_back(edge_var[e]);
+        std::sort(ids.begin(), ids.end());
+        V = (uint32_t)(std::unique(ids.begin(), ids.end()) - ids.begin());
+    }
+    pr.cols = (kp ? kp : q->n_vertices) + V;
+    pr.rows = named_unique(c, g, q, o, edge_var, kp, cols, out ? &pr.block : nullptr);
+    pr.global_rows = pr.rows;
+    if (pr.block) pr.data = static_cast<const uint32_t*>(pr.block->p);
+    if (count) *count = pr.rows;
+    if (out) *out = wrap_result(c, pr, o.result_on_device != 0);
+    ctx_sync(c);
+}
+
+gps_status gps_match_named(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
+                           const int32_t* edge_var, uint32_t kp, const int32_t* cols, gps_result** out) {
+    return guarded([&] {
+        if (!out) fail(GPS_EINVAL, "null out");
+        named_call(c, g, q, opts, edge_var, kp, cols, out, nullptr);
+    });
+}
+
+gps_status gps_count_named(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts* opts,
+                           const int32_t* edge_var, uint32_t kp, const int32_t* cols, uint64_t* count) {
+    return guarded([&] {
+        if (!count) fail(GPS_EINVAL, "null count");
+        named_call(c, g, q, opts, edge_var, kp, cols, nullptr, count);
+    });
+}
+
 gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols, const uint32_t** data,
                            int* on_device) {
     if (!r) return GPS_EINVAL;

@@ -124,7 +124,8 @@ void allow_smem(const void* func, int bytes) {
 void* dmalloc(gps_ctx* c, size_t bytes) {
     fault_injection();
     void* p = nullptr;
-    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, c->pool_mem, c->stream);
+    // +16 bytes: bulk copies (bulk.cuh) round staged ranges out to 16-byte boundaries
+    cudaError_t e = cudaMallocFromPoolAsync(&p, ((bytes + 15) & ~size_t(15)) + 16, c->pool_mem, c->stream);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
         fail(GPS_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed");

@@ -125,6 +125,7 @@ struct gps_graph {
     bool undirected = false;
     uint32_t n_vlabels = 1;
     std::vector<uint64_t> lab_hist;   // freq(label)
+    std::vector<uint32_t> elabels;    // edge labels carried by at least one stored arc, ascending
     void* mem[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 

@@ -934,6 +934,7 @@ static void launch_join_fast(gps_ctx* c, const JoinStep& s, uint64_t P) {
 }
 
 void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint64_t P) {
+    if (join_bulk_enabled()) return run_join_bulk_write(c, s, P);
     switch (s.wout) {
         case 2: return launch_join_fast<2>(c, s, P);
         case 3: return launch_join_fast<3>(c, s, P);

@@ -177,6 +177,10 @@ void run_lower_bound(gps_ctx* c, const uint64_t* poff, uint64_t R, const uint64_
 void run_join_seg(gps_ctx* c, const JoinStep& s);      // s0 + poff (+ imask / aoff / woff / jobs[].total if fast)
 // fast steps: write pass over all P pairs (rows of count-only jobs are skipped)
 void run_join_fast_write(gps_ctx* c, const JoinStep& s, uint64_t P);
+// the same write pass with the per-row inputs staged by TMA bulk copies (join_bulk.cu);
+// GPS_JOIN_NO_BULK selects k_join_fast instead
+bool join_bulk_enabled();
+void run_join_bulk_write(gps_ctx* c, const JoinStep& s, uint64_t P);
 void run_join_count(gps_ctx* c, const JoinStep& s, uint32_t G);
 void run_join_write(gps_ctx* c, const JoinStep& s, uint32_t G);
 // Single pass (no count pass): P = pairs of the step's range [plo, phi); out holds cap rows

@@ -97,6 +97,23 @@ __global__ void k_label_hist(const uint16_t* __restrict__ vlab, uint32_t n, uint
             if (s_h[i]) atomicAdd(&hist[i], (unsigned long long)s_h[i]);
 }
 
+// Edge labels present in the stored arcs (f2 named variable edges bind only these):
+// one bit per label value, OR-reduced in shared memory per block.
+__global__ void k_elabel_set(const uint32_t* __restrict__ arcs, uint64_t m, uint32_t lmask,
+                             unsigned int* __restrict__ bits) {
+    __shared__ unsigned int s_b[2048];   // 2^16 labels at most
+    const uint32_t nw = (lmask >> 5) + 1;
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) s_b[i] = 0;
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t l = arcs[i] & lmask;
+        atomicOr(&s_b[l >> 5], 1u << (l & 31));
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x)
+        if (s_b[i]) atomicOr(&bits[i], s_b[i]);
+}
+
 // Sort + de-duplicate keys, emit one CSR direction.  Returns #unique arcs.
 static uint32_t build_direction(gps_ctx* c, uint64_t* keys, uint64_t* tmp, uint64_t m, uint32_t n, uint32_t pbits,
                                 int nbits, uint32_t* off, uint32_t** arc_out, uint64_t* ukeys_out) {
@@ -218,6 +235,14 @@ void load_graph(gps_ctx* c, const gps_csr_desc* d, gps_graph* g) {
     std::vector<unsigned long long> h(g->n_vlabels);
     GPS_CK(cudaMemcpyAsync(h.data(), dh.p, sizeof(unsigned long long) * g->n_vlabels, cudaMemcpyDeviceToHost,
                            c->stream));
+    const uint32_t elw = (g->d.lmask >> 5) + 1;
+    DevPtr del_bits(c, sizeof(unsigned int) * elw);
+    GPS_CK(cudaMemsetAsync(del_bits.p, 0, sizeof(unsigned int) * elw, c->stream));
+    if (mu)
+        launch(c, GPS_K_LOAD, dim3(std::min<uint32_t>((mu + 255) / 256, 1184)), dim3(256), 0, k_elabel_set,
+               (const uint32_t*)arc_out, (uint64_t)mu, g->d.lmask, del_bits.as<unsigned int>());
+    std::vector<unsigned int> elb(elw);
+    GPS_CK(cudaMemcpyAsync(elb.data(), del_bits.p, sizeof(unsigned int) * elw, cudaMemcpyDeviceToHost, c->stream));
     uint2* deg = nullptr;
     GPS_CK(cudaMalloc(&deg, sizeof(uint2) * (n + 1)));
     g->mem[5] = deg;
@@ -226,6 +251,9 @@ void load_graph(gps_ctx* c, const gps_csr_desc* d, gps_graph* g) {
                (const uint32_t*)off_out, (const uint32_t*)off_in, n, deg);
     ctx_sync(c);
     g->lab_hist.assign(h.begin(), h.end());
+    g->elabels.clear();
+    for (uint32_t l = 0; l <= g->d.lmask; l++)
+        if ((elb[l >> 5] >> (l & 31)) & 1u) g->elabels.push_back(l);
     g->d.off_out = off_out;
     g->d.arc_out = arc_out;
     g->d.off_in = off_in;

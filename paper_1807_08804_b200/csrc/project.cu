@@ -76,6 +76,31 @@ __global__ void k_compact(const uint32_t* __restrict__ P, const uint32_t* __rest
     for (uint32_t j = 0; j < kp; j++) o[j] = __ldg(a + j);
 }
 
+// f2 named variable edges: rows of instance j (k columns) copied to out rows [dst, dst + rows)
+// with the instance's V label bindings appended (k + V columns)
+constexpr uint32_t kNamedMax = 8;
+struct AppendJob {
+    const uint32_t* src;
+    uint64_t rows, dst;
+    uint32_t beta[kNamedMax];
+};
+
+__global__ void k_append(const AppendJob* __restrict__ jobs, uint32_t nj, uint32_t k, uint32_t V,
+                         uint32_t* __restrict__ out) {
+    const uint32_t K = k + V;
+    for (uint32_t j = blockIdx.y; j < nj; j += gridDim.y) {
+        const AppendJob& J = jobs[j];
+        const uint64_t words = J.rows * K;
+        uint32_t* o = out + J.dst * K;
+        for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < words;
+             x += (uint64_t)gridDim.x * blockDim.x) {
+            const uint64_t r = x / K;
+            const uint32_t col = (uint32_t)(x - r * K);
+            o[x] = col < k ? __ldg(J.src + r * k + col) : J.beta[col - k];
+        }
+    }
+}
+
 uint32_t bits_for(uint64_t x) {
     uint32_t b = 0;
     while (b < 64 && (x >> b)) b++;
@@ -137,6 +162,85 @@ uint64_t project_unique(gps_ctx* c, const uint32_t* rows, uint64_t R, uint32_t k
                static_cast<uint32_t*>((*out)->p));
     }
     return total;
+}
+
+// f2 named variable edges (DESIGN R32): edges sharing a name bind the same
+// edge label, reported as extra columns.  The query is instantiated once per assignment of
+// the labels present in the graph to the V names (every named edge of name v labelled
+// beta(v)); the instances run as ONE batch through the same device pipeline, their rows
+// get the assignment appended (k_append), and the projection + dedup above makes the set.
+uint64_t named_unique(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts& o,
+                      const int32_t* edge_var, uint32_t kp, const int32_t* cols, Block* out) {
+    const uint32_t k = q->n_vertices, E = q->n_edges;
+    if (E && (!edge_var || !q->edges)) fail(GPS_EINVAL, "null edge_var");
+    std::vector<int32_t> names;
+    for (uint32_t e = 0; e < E; e++)
+        if (edge_var[e] >= 0) {
+            if (q->edges[e].label != GPS_ANY) fail(GPS_EINVAL, "a named edge must be a variable (GPS_ANY) edge");
+            names.push_back(edge_var[e]);
+        }
+    std::sort(names.begin(), names.end());
+    names.erase(std::unique(names.begin(), names.end()), names.end());
+    const uint32_t V = (uint32_t)names.size();
+    if (V > kNamedMax) fail(GPS_EUNSUPPORTED, "more than 8 edge-variable names");
+    std::vector<int32_t> pc;
+    if (kp == 0) {
+        for (uint32_t u = 0; u < k; u++) pc.push_back((int32_t)u);
+    } else {
+        pc.assign(cols, cols + kp);
+    }
+    for (int32_t x : pc)
+        if (x < 0 || (uint32_t)x >= k) fail(GPS_EINVAL, "projected vertex out of range");
+    for (uint32_t v = 0; v < V; v++) pc.push_back((int32_t)(k + v));
+    if (pc.size() > kProjMax) fail(GPS_EINVAL, "projection plus bindings wider than 32 columns");
+    const std::vector<uint32_t>& L = g->elabels;
+    uint64_t ninst = 1;
+    for (uint32_t v = 0; v < V; v++) {
+        ninst *= L.size();
+        if (ninst > 65536) fail(GPS_EUNSUPPORTED, "more than 65536 label assignments of the edge variables");
+    }
+    if (ninst == 0) return 0;   // no arcs: nothing binds
+    std::vector<std::vector<gps_qedge>> edges(ninst, std::vector<gps_qedge>(q->edges, q->edges + E));
+    std::vector<std::vector<uint32_t>> beta(ninst, std::vector<uint32_t>(V));
+    std::vector<gps_query> qs(ninst, *q);
+    for (uint64_t i = 0; i < ninst; i++) {
+        uint64_t x = i;
+        for (int v = (int)V - 1; v >= 0; v--) {   // mixed radix: the last name varies fastest
+            beta[i][v] = L[x % L.size()];
+            x /= L.size();
+        }
+        for (uint32_t e = 0; e < E; e++)
+            if (edge_var[e] >= 0) {
+                const uint32_t v = (uint32_t)(std::lower_bound(names.begin(), names.end(), edge_var[e]) - names.begin());
+                edges[i][e].label = (int32_t)beta[i][v];
+            }
+        qs[i].edges = edges[i].data();
+    }
+    std::vector<QueryResult> qr;
+    run_queries(c, g, qs.data(), (uint32_t)ninst, o, false, qr);
+    uint64_t total = 0;
+    std::vector<AppendJob> jobs;
+    for (uint64_t i = 0; i < ninst; i++) {
+        if (qr[i].status != GPS_OK) fail(qr[i].status, qr[i].error);
+        if (qr[i].rows == 0) continue;
+        AppendJob J{};
+        J.src = qr[i].data;
+        J.rows = qr[i].rows;
+        J.dst = total;
+        for (uint32_t v = 0; v < V; v++) J.beta[v] = beta[i][v];
+        jobs.push_back(J);
+        total += qr[i].rows;
+    }
+    if (total == 0) return 0;
+    const uint32_t K = k + V;
+    DevPtr table(c, sizeof(uint32_t) * total * K);
+    std::vector<DevPtr> keep;
+    const AppendJob* dj = upload(c, jobs, keep);
+    launch(c, GPS_K_JOIN_WRITE, dim3(64, (uint32_t)std::min<size_t>(jobs.size(), 65535)), dim3(256), 0, k_append, dj,
+           (uint32_t)jobs.size(), k, V, table.as<uint32_t>());
+    uint32_t vmax = g->d.n ? g->d.n - 1 : 0;
+    if (!L.empty()) vmax = std::max(vmax, L.back());
+    return project_unique(c, table.as<uint32_t>(), total, K, pc.data(), (uint32_t)pc.size(), vmax, out);
 }
 
 }  // namespace gps

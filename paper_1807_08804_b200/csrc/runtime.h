@@ -51,6 +51,10 @@ void run_queries(gps_ctx* c, const gps_graph* g, const gps_query* qs, uint32_t n
 uint64_t project_unique(gps_ctx* c, const uint32_t* rows, uint64_t R, uint32_t k, const int32_t* cols, uint32_t kp,
                         uint32_t vmax, Block* out);
 
+// f2 named variable edges: the distinct (projection, label bindings) tuples (project.cu).
+uint64_t named_unique(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts& o,
+                      const int32_t* edge_var, uint32_t kp, const int32_t* cols, Block* out);
+
 // Filter only (debug entry point): candidate bitmaps after stage 0/1/2 to host.
 void run_filter_debug(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts& o, int stage,
                       uint32_t* host_bitmaps);

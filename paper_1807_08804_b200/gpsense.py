@@ -114,6 +114,8 @@ def _load_lib():
         "gps_load_triples": (S, [P, ctypes.c_uint32, ctypes.c_uint64, P, P, P, P, ctypes.c_uint32, P]),
         "gps_match_project": (S, [P, P, P, P, ctypes.c_uint32, P, P]),
         "gps_count_project": (S, [P, P, P, P, ctypes.c_uint32, P, P]),
+        "gps_match_named": (S, [P, P, P, P, P, ctypes.c_uint32, P, P]),
+        "gps_count_named": (S, [P, P, P, P, P, ctypes.c_uint32, P, P]),
         "gps_shard_recv": (S, [ctypes.c_int, ctypes.c_int, P, P, P]),
         "gps_local_comm_destroy": (S, [P]),
         "gps_create_local_rank": (S, [P, P, ctypes.c_int, P]),
@@ -132,7 +134,7 @@ EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_grap
             "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates", "gps_match_batch",
             "gps_count_batch", "gps_set_workers", "gps_set_slice", "gps_match_batch_host",
             "gps_result_global_rows", "gps_shard_plan", "gps_shard_recv", "gps_load_triples",
-            "gps_match_project", "gps_count_project", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
+            "gps_match_project", "gps_count_project", "gps_match_named", "gps_count_named", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
 
 
 def _check(st: int):
@@ -460,6 +462,34 @@ class Context:
         _check(lib.gps_count_project(self._h, graph.handle, ctypes.byref(qa.desc),
                                      ctypes.byref(opts) if opts is not None else None, pj.shape[0], _addr(pj),
                                      ctypes.byref(c)))
+        return int(c.value)
+
+    def match_named(self, graph: Graph, q, edge_var, project=None, opts: Optional[MatchOpts] = None) -> np.ndarray:
+        """Named variable edges (f2): distinct (projection, label bindings) tuples, as a
+        (rows, len(project or all k) + #names) uint32 numpy array in lexicographic order."""
+        qa = _QueryArrays(q)
+        ev = np.ascontiguousarray(edge_var, np.int32)
+        pj = np.ascontiguousarray([] if project is None else project, np.int32)
+        o = _with_device(opts if opts is not None else default_opts(), False)
+        res = ctypes.c_void_p()
+        _check(lib.gps_match_named(self._h, graph.handle, ctypes.byref(qa.desc), ctypes.byref(o), _addr(ev),
+                                   pj.shape[0], _addr(pj) if pj.shape[0] else None, ctypes.byref(res)))
+        rows, cols, ptr, ondev = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_void_p(), ctypes.c_int()
+        lib.gps_result_info(res, ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(ptr), ctypes.byref(ondev))
+        a = np.zeros((rows.value, cols.value), np.uint32)
+        if rows.value:
+            ctypes.memmove(a.ctypes.data, ptr.value, rows.value * cols.value * 4)
+        lib.gps_result_free(res)
+        return a
+
+    def count_named(self, graph: Graph, q, edge_var, project=None, opts: Optional[MatchOpts] = None) -> int:
+        qa = _QueryArrays(q)
+        ev = np.ascontiguousarray(edge_var, np.int32)
+        pj = np.ascontiguousarray([] if project is None else project, np.int32)
+        c = ctypes.c_uint64()
+        _check(lib.gps_count_named(self._h, graph.handle, ctypes.byref(qa.desc),
+                                   ctypes.byref(opts) if opts is not None else None, _addr(ev), pj.shape[0],
+                                   _addr(pj) if pj.shape[0] else None, ctypes.byref(c)))
         return int(c.value)
 
     # ---- queries ----

@@ -1,0 +1,20 @@
+# r02q: smem/TMA collect + pipelined bulk join + named edges: parity, then A/B bench lines.
+mkdir -p gpurun_out
+(timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_commonsense.py \
+    tests/test_gpu_large.py -m gpu -x -q > gpurun_out/q_tests.log 2>&1; echo exit $? >> gpurun_out/q_tests.log)
+tail -4 gpurun_out/q_tests.log; grep -E "Error|assert|FAIL" gpurun_out/q_tests.log | head -20
+for e in "" "GPS_COLLECT_TILED=1"; do
+  echo "== cfg2 $e"; env $e timeout 600 python bench.py --steps 20 --no-cpu-baseline 2>/dev/null | tail -1 | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline'].get('kernel'), d['roofline']['achieved'], d['roofline']['frac'])"
+done
+for e in "" "GPS_COLLECT_TILED=1"; do
+  echo "== cfg5 $e"; env $e timeout 600 python bench.py --config 5 --steps 5 --no-cpu-baseline 2>/dev/null | tail -1 | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline'].get('kernel'), d['roofline']['achieved'], d['roofline']['frac'])"
+done
+timeout 300 python scripts/classes.py 2 2>&1 | head -14
+for e in "" "GPS_JOIN_NO_BULK=1"; do
+  echo "== cfg4 classes $e"; env $e CLASSES=1 timeout 600 python scripts/ncu_cfg4.py 2>&1 | tail -9 | head -3
+done
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed \
+  --clock-control none -k regex:"k_join_bulk" --csv python scripts/ncu_cfg4.py 2>/dev/null | grep -E "k_join" | \
+  awk -F'","' '{print $5, $(NF-2), $(NF)}' | sed 's/"//g' | grep -E "pct|duration" | head -24

@@ -17,7 +17,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LOAD = ("k_rs_", "k_degrees", "k_make_keys", "k_build_rows", "k_dup_flags", "k_transpose_keys", "k_label_hist")
 CLASS = [("k_explore", "explore"), ("k_ec", "ec_write"), ("k_join<0>", "join_count"), ("k_join<1>", "join_write"),
-         ("k_join<2>", "join_write"), ("k_join_v", "join_write"), ("k_join_fast", "join_write"),
+         ("k_join<2>", "join_write"), ("k_join_v", "join_write"), ("k_join_fast", "join_write"), ("k_join_bulk", "join_write"),
          ("k_join_seg", "join_len"), ("k_join_job_totals", "join_len"), ("k_collect", "collect"),
          ("k_check", "check"), ("k_post", "bitand"), ("k_scan", "scan")]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",

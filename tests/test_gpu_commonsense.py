@@ -148,3 +148,85 @@ def test_load_triples(gps, ctx):
         assert np.array_equal(got, want)
     with pytest.raises(gps.GpsError):
         ctx.load_triples(10, [1, 2], [0, 0], [3, 10])
+
+
+# ------------------------------------------------------------ named variable edges
+def _named_instance(seed):
+    """A corpus instance with some variable edges named from a pool of 2 names (names repeat)."""
+    g, q = corpus.instance(seed)
+    rng = np.random.default_rng(77 + seed)
+    ev = [int(rng.integers(0, 2)) if (l == -1 and rng.random() < 0.6) else -1 for (_, _, l) in q.edges]
+    return g, q, ev
+
+
+@pytest.mark.parametrize("seed", range(0, 200, 4))
+def test_named_edges_corpus(gps, ctx, seed):
+    """gps_match_named / gps_count_named equal the oracle's plain definition (oracle.match_named:
+    embeddings x label assignments with each named edge carrying its name's label) as sorted
+    sets, for all vertices and for a projection."""
+    g, q, ev = _named_instance(seed)
+    og = oracle.OracleGraph(g)
+    try:
+        if oracle.count(og, q, limit=100_000) == oracle.ELIMIT:
+            pytest.skip("too many embeddings")
+    except ValueError:
+        pytest.skip("oracle rejects the instance")
+    G = ctx.load_graph(g)
+    rng = np.random.default_rng(seed)
+    for proj in (None, sorted(rng.permutation(q.k)[:max(1, q.k // 2)].tolist())):
+        want = oracle.match_named(g, og, q, ev, proj)
+        got = ctx.match_named(G, q, ev, proj)
+        assert np.array_equal(got, want), (proj, got.shape, want.shape)
+        assert ctx.count_named(G, q, ev, proj) == want.shape[0]
+
+
+def test_named_edges_worked_example(gps, ctx):
+    """The hand-worked example of tests/test_oracle_pins.py (values written out by hand)."""
+    person, bread, soup, cook = 0, 1, 2, 3
+    g = DataGraph(4, np.array([0, 0, 0, 3, 3], np.uint32), np.array([1, 2, 2, 2, 1], np.uint32),
+                  np.array([1, 1, 2, 3, 3], np.uint16), None, False)
+    q = Query(3, [-1, -1, -1], [person, -1, cook], [(0, 1, -1), (2, 1, -1)])
+    G = ctx.load_graph(g)
+    assert ctx.match_named(G, q, [0, 1]).tolist() == [[person, bread, cook, 1, 3], [person, soup, cook, 1, 3],
+                                                      [person, soup, cook, 2, 3]]
+    assert ctx.match_named(G, q, [0, 0]).shape == (0, 4)
+    assert ctx.match_named(G, q, [5, 9], [1]).tolist() == [[bread, 1, 3], [soup, 1, 3], [soup, 2, 3]]
+    assert ctx.match_named(G, q, [-1, 7], [1]).tolist() == [[bread, 3], [soup, 3]]
+    assert ctx.count_named(G, q, [-1, -1]) == 2   # no names: the distinct embeddings
+
+
+def test_named_edges_errors(gps, ctx):
+    g = DataGraph(3, np.array([0, 1], np.uint32), np.array([1, 2], np.uint32), np.array([0, 1], np.uint16), None, False)
+    G = ctx.load_graph(g)
+    q = Query(3, [-1] * 3, [-1] * 3, [(0, 1, 0), (1, 2, -1)])
+    with pytest.raises(gps.GpsError):   # a named edge must be a variable edge
+        ctx.match_named(G, q, [0, 1])
+    with pytest.raises(gps.GpsError):
+        ctx.match_named(G, q, [-1, 0], [3])
+
+
+def test_named_edges_cfg5_queries(gps, ctx):
+    """ConceptNet-shaped graph (34 edge labels): QA queries whose variable edges share one name
+    (the commonsense "same relation" question), against the oracle."""
+    path = os.path.join(ROOT, "synth", "data", "cfg5_queries.json")
+    if not os.path.exists(path):
+        pytest.skip("cfg5 queries not generated")
+    with open(path) as fh:
+        data = json.load(fh)
+    g = config_graph(5)
+    og = oracle.OracleGraph(g)
+    G = ctx.load_graph(g)
+    done = 0
+    for item in data["queries"][:400]:
+        q0 = Query.from_json(item["query"])
+        # the query with its relations replaced by variable edges: names 0, 1, 0, 1, ...
+        q = Query(q0.k, q0.vlabels, q0.bound, [(a, b, -1) for (a, b, _) in q0.edges])
+        ev = [i % 2 for i in range(len(q.edges))]
+        if oracle.count(og, q, limit=20_000) == oracle.ELIMIT:
+            continue
+        want = oracle.match_named(g, og, q, ev)
+        assert np.array_equal(ctx.match_named(G, q, ev), want), item["seed"]
+        done += 1
+        if done == 6:
+            break
+    assert done > 0
