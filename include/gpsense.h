@@ -276,6 +276,44 @@ GPS_API gps_status gps_count_named(gps_ctx* ctx, const gps_graph* g, const gps_q
                                    const int32_t* edge_var, uint32_t n_project, const int32_t* project,
                                    uint64_t* count);
 
+/* ---- f3: multi-level graph compression ------------
+ * gps_compress: levels 1..n_levels of the compression of g ("a sequence of smaller
+ *   graphs G_i ... similar nodes are combined to form a weighted node"; DESIGN readings
+ *   R33-R36): level i pairs SIMILAR nodes of level i-1 (same vertex label, identical set of
+ *   (direction, edge label, neighbour node) edge ends: R33 at delta = 1), greedily in id
+ *   order (R34); node ids of a level follow their smallest member.  Weights (P:846-850,
+ *   R35): w_out(U) = max over members x of the arcs x -> M(U) (w_in likewise), edge weights
+ *   start at #labelled arcs x -> y and combine as w(U, V) = sum over the parts V' of V of the
+ *   max over the parts U' of U of w(U', V').  deltas [n_levels] (host) must each be 1.0 on the
+ *   device: GPS_EUNSUPPORTED for delta < 1 (a similarity join, not built), GPS_EINVAL outside
+ *   (0, 1] or n_levels outside 1..16; GPS_EUNSUPPORTED when keys need more than 64 bits.
+ *   The compression owns device memory until gps_free_compressed; g must outlive it.
+ * gps_compressed_info: nodes and weighted out-/in-edges of level (1..n_levels).
+ * gps_compressed_fetch: copies level `level` to HOST arrays (each may be NULL):
+ *   group [n] (node of every data vertex: M(U) = {x : group[x] = U}), label / w_out / w_in
+ *   [nodes], edge_out [edges_out] (U << 32 | V, ascending) with weight_out, edge_in likewise
+ *   (U << 32 | V = in-weight of U from V).
+ * gps_compressed_candidates: the weighted candidate test of P:905 (R36: label, bound id in
+ *   M(X), distinct query out-/in-degree <= w(X) + sum over Z != X of w(X, Z)) through every
+ *   data vertex's node: bitmaps_out (host) k x ceil(n/32) words, bit v of row u = v lies in
+ *   the mapping list of a weighted candidate of u (a superset of Def. 3's candidates,
+ *   Theorem 1).
+ * gps_graph_attach_compressed: subsequent filters on g also apply that test at `level`
+ *   (cg = NULL or level 0 detaches); results are unchanged (Theorem 1).  GPS_EINVAL when cg
+ *   was built from another graph or level is out of range. */
+typedef struct gps_compressed gps_compressed;
+GPS_API gps_status gps_compress(gps_ctx* ctx, const gps_graph* g, uint32_t n_levels, const float* deltas,
+                                gps_compressed** out);
+GPS_API gps_status gps_free_compressed(gps_compressed* cg);
+GPS_API gps_status gps_compressed_info(const gps_compressed* cg, uint32_t level, uint32_t* n_nodes,
+                                       uint64_t* n_edges_out, uint64_t* n_edges_in);
+GPS_API gps_status gps_compressed_fetch(gps_ctx* ctx, const gps_compressed* cg, uint32_t level, uint32_t* group,
+                                        uint32_t* label, uint32_t* w_out, uint32_t* w_in, uint64_t* edge_out,
+                                        uint32_t* weight_out, uint64_t* edge_in, uint32_t* weight_in);
+GPS_API gps_status gps_compressed_candidates(gps_ctx* ctx, const gps_compressed* cg, uint32_t level,
+                                             const gps_query* q, uint32_t* bitmaps_out);
+GPS_API gps_status gps_graph_attach_compressed(gps_graph* g, const gps_compressed* cg, uint32_t level);
+
 /* rows, cols (= k), data (device or host pointer, owned by the result), on_device. */
 GPS_API gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols,
                            const uint32_t** data, int* on_device);

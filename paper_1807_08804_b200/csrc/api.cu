@@ -602,6 +602,94 @@ gps_status gps_count_named(gps_ctx* c, const gps_graph* g, const gps_query* q, c
     });
 }
 
+// ---- f3 multi-level graph compression --------------------------------------
+gps_status gps_compress(gps_ctx* c, const gps_graph* g, uint32_t n_levels, const float* deltas, gps_compressed** out) {
+    return guarded([&] {
+        check_args(c, g);
+        if (!out || (n_levels && !deltas)) fail(GPS_EINVAL, "null argument");
+        if (n_levels == 0 || n_levels > 16) fail(GPS_EINVAL, "1..16 compression levels");
+        DeviceGuard dg(c->device);
+        *out = compress_graph(c, g, n_levels, deltas);
+    });
+}
+
+gps_status gps_free_compressed(gps_compressed* cg) {
+    if (!cg) return GPS_OK;
+    free_compressed(cg);
+    return GPS_OK;
+}
+
+gps_status gps_compressed_info(const gps_compressed* cg, uint32_t level, uint32_t* n_nodes, uint64_t* n_edges_out,
+                               uint64_t* n_edges_in) {
+    return guarded([&] {
+        if (!cg) fail(GPS_EINVAL, "null compression");
+        compressed_level_info(cg, level, n_nodes, n_edges_out, n_edges_in);
+    });
+}
+
+gps_status gps_compressed_fetch(gps_ctx* c, const gps_compressed* cg, uint32_t level, uint32_t* group,
+                                uint32_t* label, uint32_t* w_out, uint32_t* w_in, uint64_t* edge_out,
+                                uint32_t* weight_out, uint64_t* edge_in, uint32_t* weight_in) {
+    return guarded([&] {
+        if (!c || !cg) fail(GPS_EINVAL, "null argument");
+        DeviceGuard dg(c->device);
+        compressed_fetch(c, cg, level, group, label, w_out, w_in, edge_out, weight_out, edge_in, weight_in);
+    });
+}
+
+gps_status gps_compressed_candidates(gps_ctx* c, const gps_compressed* cg, uint32_t level, const gps_query* q,
+                                     uint32_t* bitmaps_out) {
+    return guarded([&] {
+        if (!c || !cg || !q || !bitmaps_out) fail(GPS_EINVAL, "null argument");
+        const gps_graph* g = compressed_graph(cg);
+        DeviceGuard dg(c->device);
+        const uint32_t k = q->n_vertices;
+        if (k == 0 || k > GPS_MAX_QV) fail(GPS_EINVAL, "query size");
+        std::vector<std::vector<uint32_t>> outs(k), ins(k);
+        for (uint32_t e = 0; e < q->n_edges; e++) {
+            const gps_qedge& x = q->edges[e];
+            if (x.src < 0 || x.dst < 0 || (uint32_t)x.src >= k || (uint32_t)x.dst >= k) fail(GPS_EINVAL, "edge");
+            outs[x.src].push_back((uint32_t)x.dst);
+            ins[x.dst].push_back((uint32_t)x.src);
+        }
+        const uint32_t nws = g->d.nws;
+        DevPtr B(c, sizeof(uint32_t) * (size_t)k * nws);
+        std::vector<ChkQV> qv(k);
+        for (uint32_t u = 0; u < k; u++) {
+            auto uniq = [](std::vector<uint32_t> v) {
+                std::sort(v.begin(), v.end());
+                return (uint32_t)(std::unique(v.begin(), v.end()) - v.begin());
+            };
+            qv[u].lab = q->vertex_labels ? q->vertex_labels[u] : GPS_ANY;
+            qv[u].bound = q->bound ? q->bound[u] : GPS_FREE;
+            if (qv[u].bound >= (int64_t)g->d.n) fail(GPS_EINVAL, "bound id out of range");
+            qv[u].qout = uniq(outs[u]);
+            qv[u].qin = uniq(ins[u]);
+            qv[u].B = B.as<uint32_t>() + (size_t)u * nws;
+        }
+        std::vector<DevPtr> keep;
+        run_wcheck(c, cg, level, upload(c, qv, keep), k, true);
+        GPS_CK(cudaMemcpy2DAsync(bitmaps_out, sizeof(uint32_t) * g->d.nw, B.p, sizeof(uint32_t) * nws,
+                                 sizeof(uint32_t) * g->d.nw, k, cudaMemcpyDeviceToHost, c->stream));
+        ctx_sync(c);
+    });
+}
+
+gps_status gps_graph_attach_compressed(gps_graph* g, const gps_compressed* cg, uint32_t level) {
+    return guarded([&] {
+        if (!g) fail(GPS_EINVAL, "null graph");
+        if (!cg || level == 0) {
+            g->cg = nullptr;
+            g->cg_level = 0;
+            return;
+        }
+        if (compressed_graph(cg) != g) fail(GPS_EINVAL, "the compression was built from another graph");
+        if (level > compressed_levels(cg)) fail(GPS_EINVAL, "compression level out of range");
+        g->cg = cg;
+        g->cg_level = level;
+    });
+}
+
 gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols, const uint32_t** data,
                            int* on_device) {
     if (!r) return GPS_EINVAL;

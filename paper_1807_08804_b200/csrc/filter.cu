@@ -20,7 +20,6 @@
 //   k_post         word-parallel B &= (AND of the jobs' X bitmaps), scratch reset.
 #include <cstdlib>
 
-#include "bulk.cuh"
 #include "kernels.cuh"
 #include "lookback.cuh"
 #include "pairs.cuh"
@@ -113,7 +112,8 @@ constexpr int kColTile = kColThreads * kColWords;     // words per tile
 constexpr int kColBatch = 8;                          // candidates whose degrees are loaded together
 
 __global__ void __launch_bounds__(kColThreads, 5) k_collect(DevGraph g, const CollectJob* __restrict__ jobs,
-                                                         LbScratch lb, uint32_t ntiles, uint32_t epoch) {
+                                                         LbScratch lb, uint32_t ntiles, uint32_t epoch,
+                                                         unsigned long long* bytes_acc) {
     const uint32_t y = blockIdx.y;
     const CollectJob& J = jobs[y];
     const uint32_t tile = lb_ticket(lb.ctr + 3 * y, ntiles);
@@ -216,6 +216,8 @@ __global__ void __launch_bounds__(kColThreads, 5) k_collect(DevGraph g, const Co
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
         const uint32_t C = (uint32_t)s_pre[0] + tc;
+        // algorithmic bytes per candidate: its 8-byte degree word read + id and two prefixes written
+        atomicAdd(bytes_acc, 20ull * C);
         J.rp[g.nw] = C;
         *J.cnt = C;
         J.seg_out[C] = (uint32_t)s_pre[1] + tso;
@@ -227,180 +229,13 @@ __global__ void __launch_bounds__(kColThreads, 5) k_collect(DevGraph g, const Co
     }
 }
 
-// Small graphs (nw <= kCsMaxWords: configs 2/3/5 have 9,375 words): ONE block per job
-// and no look-back.  One elected thread stages the job's whole bitmap into shared memory
-// with a single TMA bulk copy (cp.async.bulk, mbarrier completion) while the block ANDs
-// in the folded posts' X bitmaps from global memory; thread t then owns the CONTIGUOUS
-// words [t*K, (t+1)*K) of the staged row (odd K: conflict-free), so the three prefixes
-// (rank, out- and in-degree sums) are one block scan.  Each thread emits its candidates,
-// overwrites its words with their rank prefixes, and the block stores the rank row with
-// coalesced 16-byte stores.  256 threads and <= 48 KB of shared memory per block keep
-// several jobs (and the other streams' kernels) resident per SM.
-constexpr int kCsThreads = 256;
-constexpr uint32_t kCsMaxWords = 12288;
-
-__global__ void __launch_bounds__(kCsThreads) k_collect_smem(DevGraph g, const CollectJob* __restrict__ jobs) {
-    extern __shared__ __align__(16) uint32_t s_B[];
-    __shared__ __align__(8) uint64_t s_bar;
-    const CollectJob& J = jobs[blockIdx.x];
-    const uint32_t nw = g.nw, tid = threadIdx.x;
-    const uint32_t nv = (nw + 3) / 4;   // 16-byte vectors of the row (the row is padded to 64 words)
-    if (tid == 0) {
-        mbar_init(&s_bar, 1);
-        mbar_fence_init();
-        bulk_g2s(s_B, J.B, nv * 16u, &s_bar);
-        mbar_arrive_expect_tx(&s_bar, nv * 16u);
-    }
-    __syncthreads();   // the barrier init is visible to every thread
-    mbar_wait(&s_bar, 0);
-    if (J.x1 > J.x0) {   // folded post: B &= AND of the X bitmaps, X cleared, B written back
-        constexpr int kV = 4;   // vectors per thread per round, loads issued together
-        for (uint32_t v0 = tid; v0 < nv; v0 += kCsThreads * kV) {
-            uint4 m[kV];
-#pragma unroll
-            for (int i = 0; i < kV; i++) m[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
-            for (uint32_t x = J.x0; x < J.x1; x++) {
-                uint4* xp = reinterpret_cast<uint4*>(J.xs[x]);
-#pragma unroll
-                for (int i = 0; i < kV; i++) {
-                    const uint32_t v = v0 + i * kCsThreads;
-                    if (v < nv) {
-                        const uint4 y = xp[v];
-                        m[i].x &= y.x;
-                        m[i].y &= y.y;
-                        m[i].z &= y.z;
-                        m[i].w &= y.w;
-                        xp[v] = make_uint4(0u, 0u, 0u, 0u);
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < kV; i++) {
-                const uint32_t v = v0 + i * kCsThreads;
-                if (v < nv) {
-                    uint4* sp = reinterpret_cast<uint4*>(s_B) + v;
-                    uint4 b = *sp;
-                    b.x &= m[i].x;
-                    b.y &= m[i].y;
-                    b.z &= m[i].z;
-                    b.w &= m[i].w;
-                    *sp = b;
-                    reinterpret_cast<uint4*>(J.B)[v] = b;
-                }
-            }
-        }
-    }
-    if (J.post_only) return;   // uniform per block
-    __syncthreads();           // every thread's AND is in s_B
-    const uint32_t K = (nw + kCsThreads - 1) / kCsThreads | 1u;   // odd: no bank conflicts
-    const uint32_t w0 = tid * K, w1 = min(w0 + K, nw);
-    // the thread's candidates in order, kColBatch at a time ACROSS its words: one round trip
-    // per kColBatch candidates, not per word
-    constexpr uint32_t kNone = 0xffffffffu;
-    uint32_t cw = w0, cbits = 0;
-    auto next = [&]() -> uint32_t {
-        while (cbits == 0) {
-            if (cw >= w1) return kNone;
-            cbits = s_B[cw++];
-        }
-        const uint32_t v = (cw - 1) * 32 + __ffs(cbits) - 1;
-        cbits &= cbits - 1;
-        return v;
-    };
-    uint32_t c = 0, so = 0, si = 0;
-    for (bool more = true; more;) {
-        uint32_t v[kColBatch];
-        uint2 d[kColBatch];
-#pragma unroll
-        for (int k = 0; k < kColBatch; k++) {
-            v[k] = next();
-            d[k] = v[k] != kNone ? __ldg(g.deg + v[k]) : make_uint2(0u, 0u);
-        }
-#pragma unroll
-        for (int k = 0; k < kColBatch; k++) {
-            c += v[k] != kNone;
-            so += d[k].x;
-            si += d[k].y;
-        }
-        more = v[kColBatch - 1] != kNone;
-    }
-    // the three exclusive prefixes in one pass of barriers
-    __shared__ uint32_t s_w[3][32];
-    const uint32_t lane = lane_id(), wid = warp_id();
-    const uint32_t xc = warp_incl_scan(c), xo = warp_incl_scan(so), xi = warp_incl_scan(si);
-    if (lane == 31) {
-        s_w[0][wid] = xc;
-        s_w[1][wid] = xo;
-        s_w[2][wid] = xi;
-    }
-    __syncthreads();
-    if (wid < 3) {
-        const uint32_t y = lane < kCsThreads / 32 ? s_w[wid][lane] : 0u;
-        s_w[wid][lane] = warp_incl_scan(y);
-    }
-    __syncthreads();
-    uint32_t rank = (wid ? s_w[0][wid - 1] : 0u) + xc - c;
-    uint32_t ro = (wid ? s_w[1][wid - 1] : 0u) + xo - so;
-    uint32_t ri = (wid ? s_w[2][wid - 1] : 0u) + xi - si;
-    const uint32_t rank0 = rank;
-    cw = w0;
-    cbits = 0;
-    for (bool more = true; more;) {
-        uint32_t v[kColBatch];
-        uint2 d[kColBatch];
-#pragma unroll
-        for (int k = 0; k < kColBatch; k++) {
-            v[k] = next();
-            d[k] = v[k] != kNone ? __ldg(g.deg + v[k]) : make_uint2(0u, 0u);
-        }
-#pragma unroll
-        for (int k = 0; k < kColBatch; k++) {
-            if (v[k] == kNone) break;
-            J.carr[rank] = v[k];
-            J.seg_out[rank] = ro;
-            J.seg_in[rank] = ri;
-            ro += d[k].x;
-            ri += d[k].y;
-            rank++;
-        }
-        more = v[kColBatch - 1] != kNone;
-    }
-    for (uint32_t w = w0, r = rank0; w < w1; w++) {   // each word's rank prefix replaces it (own words)
-        const uint32_t x = __popc(s_B[w]);
-        s_B[w] = r;
-        r += x;
-    }
-    __syncthreads();
-    // rank row: coalesced 16-byte stores of the staged prefixes (rp rows are 16-byte aligned)
-    for (uint32_t v = tid; v < nw / 4; v += kCsThreads) reinterpret_cast<uint4*>(J.rp)[v] = reinterpret_cast<uint4*>(s_B)[v];
-    for (uint32_t w = (nw / 4) * 4 + tid; w < nw; w += kCsThreads) J.rp[w] = s_B[w];
-    if (tid == kCsThreads - 1) {   // the last thread's running values are the totals
-        J.rp[nw] = rank;
-        *J.cnt = rank;
-        J.seg_out[rank] = ro;
-        J.seg_in[rank] = ri;
-        if (J.segtot) {
-            J.segtot[0] = ro;
-            J.segtot[1] = ri;
-        }
-    }
-}
-
 void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32_t nj) {
     if (nj == 0) return;
-    if (g.nw <= kCsMaxWords && std::getenv("GPS_COLLECT_TILED") == nullptr) {   // env: A/B switch for the tests
-        const size_t smem = (size_t)((g.nw + 3) / 4) * 16;
-        allow_smem((const void*)k_collect_smem, (int)(kCsMaxWords * 4));
-        launch(c, GPS_K_COLLECT, dim3(nj), dim3(kCsThreads), smem, k_collect_smem, g, d_jobs);
-        c->stats.k_bytes[GPS_K_COLLECT] += (double)nj * g.nw * 8.0;
-        return;
-    }
     const uint32_t ntiles = (g.nw + kColTile - 1) / kColTile;
     LbScratch lb = lb_scratch(c, 3 * nj, ntiles);
     launch(c, GPS_K_COLLECT, dim3(ntiles, nj), dim3(kColThreads), 0, k_collect, g, d_jobs, lb, ntiles,
-           lb_next_epoch(c));
-    // algorithmic: read the bitmap, write the rank prefix (ids / segments / offsets counted per candidate
-    // would need the candidate counts on the host)
+           lb_next_epoch(c), c->d_bytes + GPS_K_COLLECT);
+    // algorithmic: read the bitmap, write the rank prefix (+ 20 B per candidate, counted on the device)
     c->stats.k_bytes[GPS_K_COLLECT] += (double)nj * g.nw * 8.0;
 }
 

@@ -118,6 +118,7 @@ struct gps_ctx {
     size_t arena_cache_bytes = 0;
 };
 
+struct gps_compressed;   // f3 (compress.cu)
 struct gps_graph {
     int device = 0;
     gps::DevGraph d{};
@@ -126,6 +127,8 @@ struct gps_graph {
     uint32_t n_vlabels = 1;
     std::vector<uint64_t> lab_hist;   // freq(label)
     std::vector<uint32_t> elabels;    // edge labels carried by at least one stored arc, ascending
+    const gps_compressed* cg = nullptr;   // f3: attached compression (filters start from its level cg_level)
+    uint32_t cg_level = 0;
     void* mem[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 

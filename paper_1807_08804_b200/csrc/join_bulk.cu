@@ -54,8 +54,16 @@ struct BLay {
     // meta per row: WOUT template words (new value's column = 0xffffffff), then
     // (hole | in-segment mask of the output columns << 8)
     static constexpr size_t BUF = META + a16(4ull * (WOUT + 1) * kBW);
+    // output staging (two buffers, alternating per chunk): a chunk's rows, row-major, placed at the
+    // output's address offset mod 16 so the aligned interior goes out as one bulk store
+    // (wide rows, WOUT > kStagedMax: no staging -- it would halve the resident blocks -- but one
+    // (new value, window row) pair per output row and word-parallel 16-byte stores)
+    static constexpr bool STAGED = WOUT <= 4;
+    static constexpr uint32_t STG = STAGED ? kBCh * WOUT + 4 : kBCh;   // words
+    static constexpr size_t OUT = 2 * BUF;
     static __host__ __device__ size_t jobs_bytes(uint32_t nj) { return a16(8ull * (nj + 1) + 8ull * nj + 4ull * nj + nj); }
-    static __host__ __device__ size_t bytes(uint32_t nj) { return jobs_bytes(nj) + 2 * BUF + 16; }
+    static __host__ __device__ size_t bytes(uint32_t nj) { return jobs_bytes(nj) + OUT + 2 * a16(4ull * STG) + 16; }
+    // STAGED = false: the two staging buffers hold the kBCh uint2 (value, row) entries instead
 };
 
 template <uint32_t WOUT>
@@ -114,7 +122,8 @@ __global__ void __launch_bounds__(kBT, 3) k_join_bulk(const __grid_constant__ Jo
     __shared__ uint64_t s_bar[2];
     __shared__ uint64_t s_rng[2];
     __shared__ uint64_t s_base;
-    __shared__ uint2 s_ri[kBCh];   // (new value, window row) of each output row of a chunk
+    uint32_t* stage = reinterpret_cast<uint32_t*>(bufs + L::OUT);   // [2][STG] output staging
+    uint32_t ob = 0;   // staging buffer of the next chunk with output
 
     for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) {
         const JoinJob& J = a.jobs[j];
@@ -240,6 +249,9 @@ __global__ void __launch_bounds__(kBT, 3) k_join_bulk(const __grid_constant__ Jo
             bool nv_[kBI];
             uint32_t nwi[kBI], nj_[kBI], ncand[kBI];
             if (cp + kBCh < wp1) items(cp + kBCh, nv_, nwi, nj_, ncand);
+            // staging buffer ob was last read by the bulk store of the chunk before the previous one:
+            // the issuing thread waits for that read before the scan's barriers release the writers
+            if (L::STAGED && threadIdx.x == 0) bulk_wait_read_le1();
             uint32_t tot;
             uint32_t lpos = block_excl_scan(mine, &tot);
             auto rotate = [&]() {
@@ -255,7 +267,65 @@ __global__ void __launch_bounds__(kBT, 3) k_join_bulk(const __grid_constant__ Jo
                 rotate();
                 continue;
             }
-            if (mine && lpos == 0) {   // the chunk's first output fixes the chunk's output base
+            if constexpr (!L::STAGED) {
+                uint2* s_ri = reinterpret_cast<uint2*>(stage);   // (new value, window row) per output row
+                if (mine && lpos == 0) {   // the chunk's first output fixes the chunk's output base
+                    uint32_t fc = 0, fw = 0, fj = 0;
+#pragma unroll
+                    for (int it = kBI - 1; it >= 0; it--)
+                        if (ok[it]) {
+                            fc = cand[it];
+                            fw = wi[it];
+                            fj = j[it];
+                        }
+                    const uint32_t* m = meta + fw * (WOUT + 1);
+                    const uint32_t im = m[WOUT] >> 8;
+                    uint32_t before = 0;
+#pragma unroll
+                    for (uint32_t c = 0; c < WOUT; c++) before += ((im >> c) & 1u) && m[c] < fc;
+                    s_base = wwoff[fw] + fj - before;
+                }
+#pragma unroll
+                for (int it = 0; it < kBI; it++)
+                    if (ok[it]) s_ri[lpos++] = make_uint2(cand[it], wi[it]);
+                __syncthreads();
+                // word-parallel 16-byte stores of the chunk's consecutive output rows
+                uint32_t* g = a.out + s_base * WOUT;
+                const uint32_t words = tot * WOUT;
+                const uint32_t head = min(words, (uint32_t)((16u - ((uintptr_t)g & 15u)) & 15u) >> 2);
+                auto word_at = [&](uint32_t row, uint32_t col) -> uint32_t {
+                    const uint2 ri = s_ri[row];
+                    const uint32_t* m = meta + ri.y * (WOUT + 1);
+                    return col == (m[WOUT] & 0xffu) ? ri.x : m[col];
+                };
+                if (threadIdx.x < head) g[threadIdx.x] = word_at(threadIdx.x / WOUT, threadIdx.x % WOUT);
+                const uint32_t nvec = (words - head) >> 2;
+                uint4* g4 = reinterpret_cast<uint4*>(g + head);
+                for (uint32_t x = threadIdx.x; x < nvec; x += kBT) {
+                    const uint32_t o = head + 4 * x;
+                    uint32_t row = o / WOUT, col = o - row * WOUT, wv[4];
+                    uint2 ri = s_ri[row];
+                    const uint32_t* m = meta + ri.y * (WOUT + 1);
+                    uint32_t hole = m[WOUT] & 0xffu;
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        wv[k] = col == hole ? ri.x : m[col];
+                        if (++col == WOUT && k < 3) {
+                            col = 0;
+                            ri = s_ri[++row];
+                            m = meta + ri.y * (WOUT + 1);
+                            hole = m[WOUT] & 0xffu;
+                        }
+                    }
+                    g4[x] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+                for (uint32_t o = head + 4 * nvec + threadIdx.x; o < words; o += kBT) g[o] = word_at(o / WOUT, o % WOUT);
+                rotate();
+                continue;   // s_ri / s_base are rewritten only after the next chunk's scan barriers
+            }
+            uint32_t* stg = stage + ob * L::STG;
+            if (mine) {
+                // the global row of this thread's first output fixes the chunk's output base
                 uint32_t fc = 0, fw = 0, fj = 0;
 #pragma unroll
                 for (int it = kBI - 1; it >= 0; it--)
@@ -269,49 +339,48 @@ __global__ void __launch_bounds__(kBT, 3) k_join_bulk(const __grid_constant__ Jo
                 uint32_t before = 0;
 #pragma unroll
                 for (uint32_t c = 0; c < WOUT; c++) before += ((im >> c) & 1u) && m[c] < fc;
-                s_base = wwoff[fw] + fj - before;
-            }
+                const uint64_t base = wwoff[fw] + fj - before - lpos;
+                if (lpos == 0) s_base = base;
+                const uint32_t shift = (uint32_t)(((uintptr_t)(a.out + base * WOUT) >> 2) & 3u);
+                uint32_t* dst = stg + shift + lpos * WOUT;
 #pragma unroll
-            for (int it = 0; it < kBI; it++)
-                if (ok[it]) s_ri[lpos++] = make_uint2(cand[it], wi[it]);
-            __syncthreads();
-            // word-parallel 16-byte stores of the chunk's consecutive output rows
-            uint32_t* g = a.out + s_base * WOUT;
-            const uint32_t words = tot * WOUT;
-            const uint32_t head = min(words, (uint32_t)((16u - ((uintptr_t)g & 15u)) & 15u) >> 2);
-            auto word_at = [&](uint32_t row, uint32_t col) -> uint32_t {
-                const uint2 ri = s_ri[row];
-                const uint32_t* m = meta + ri.y * (WOUT + 1);
-                return col == (m[WOUT] & 0xffu) ? ri.x : m[col];
-            };
-            if (threadIdx.x < head) g[threadIdx.x] = word_at(threadIdx.x / WOUT, threadIdx.x % WOUT);
-            const uint32_t nvec = (words - head) >> 2;
-            uint4* g4 = reinterpret_cast<uint4*>(g + head);
-            for (uint32_t x = threadIdx.x; x < nvec; x += kBT) {
-                const uint32_t o = head + 4 * x;
-                uint32_t row = o / WOUT, col = o - row * WOUT, wv[4];
-                uint2 ri = s_ri[row];
-                const uint32_t* m = meta + ri.y * (WOUT + 1);
-                uint32_t hole = m[WOUT] & 0xffu;
+                for (int it = 0; it < kBI; it++) {
+                    if (!ok[it]) continue;
+                    const uint32_t* mm = meta + wi[it] * (WOUT + 1);
+                    const uint32_t hole = mm[WOUT] & 0xffu;
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    wv[k] = col == hole ? ri.x : m[col];
-                    if (++col == WOUT && k < 3) {
-                        col = 0;
-                        ri = s_ri[++row];
-                        m = meta + ri.y * (WOUT + 1);
-                        hole = m[WOUT] & 0xffu;
-                    }
+                    for (uint32_t c = 0; c < WOUT; c++) dst[c] = c == hole ? cand[it] : mm[c];
+                    dst += WOUT;
                 }
-                g4[x] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                fence_proxy_async_smem();   // the staged rows are read by the bulk store (async proxy)
             }
-            for (uint32_t o = head + 4 * nvec + threadIdx.x; o < words; o += kBT) g[o] = word_at(o / WOUT, o % WOUT);
-            // s_ri / s_base are rewritten only after the next chunk's scan barriers
+            __syncthreads();
+            {
+                const uint64_t base = s_base;
+                uint32_t* g = a.out + base * WOUT;
+                const uint32_t words = tot * WOUT;
+                const uint32_t shift = (uint32_t)(((uintptr_t)g >> 2) & 3u);
+                const uint32_t head = min(words, (4u - shift) & 3u);         // words before the first 16-byte boundary
+                const uint32_t body = ((words - head) >> 2) << 2;            // whole 16-byte vectors
+                if (threadIdx.x == 0 && body) {
+                    bulk_s2g(g + head, stg + shift + head, body * 4u);
+                    bulk_commit();
+                }
+                const uint32_t rest = words - head - body;                 // tail words after the last vector
+                if (threadIdx.x >= 32 && threadIdx.x < 32 + head) g[threadIdx.x - 32] = stg[shift + threadIdx.x - 32];
+                if (threadIdx.x >= 64 && threadIdx.x < 64 + rest) {
+                    const uint32_t o = head + body + threadIdx.x - 64;
+                    g[o] = stg[shift + o];
+                }
+            }
+            ob ^= 1u;
+            // s_base is rewritten only after the next chunk's scan barriers
             rotate();
         }
         __syncthreads();   // every thread is done with buffer b: it may be refilled
         r0 = rnext;
     }
+    if (threadIdx.x == 0) bulk_wait_all();   // the bulk stores have completed before the block exits
 }
 
 template <uint32_t WOUT>

@@ -216,7 +216,11 @@ void filter_phase(Chunk& ch, int stage, std::vector<CollectJob>* pending = nullp
                 x.B = q->B + (size_t)u * d.nws;
                 qv.push_back(x);
             }
-        run_check(c, d, upload(c, qv, ch.keep), (uint32_t)qv.size());
+        const ChkQV* d_qv = upload(c, qv, ch.keep);
+        run_check(c, d, d_qv, (uint32_t)qv.size());
+        // f3: a graph with an attached compression also applies the weighted candidate test of
+        // that level -- never removes a Def. 3 candidate (Theorem 1)
+        if (ch.g->cg) run_wcheck(c, ch.g->cg, ch.g->cg_level, d_qv, (uint32_t)qv.size(), false);
         if (stage < 1) return;
     }
     auto in_mask = [&](size_t qi) { return !mask || (*mask)[qi]; };

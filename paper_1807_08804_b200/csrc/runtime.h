@@ -55,6 +55,18 @@ uint64_t project_unique(gps_ctx* c, const uint32_t* rows, uint64_t R, uint32_t k
 uint64_t named_unique(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts& o,
                       const int32_t* edge_var, uint32_t kp, const int32_t* cols, Block* out);
 
+// f3 multi-level compression (compress.cu)
+struct ChkQV;
+gps_compressed* compress_graph(gps_ctx* c, const gps_graph* g, uint32_t nlev, const float* deltas);
+void free_compressed(gps_compressed* cg);
+uint32_t compressed_levels(const gps_compressed* cg);
+const gps_graph* compressed_graph(const gps_compressed* cg);
+void compressed_level_info(const gps_compressed* cg, uint32_t level, uint32_t* N, uint64_t* ne_out, uint64_t* ne_in);
+void compressed_fetch(gps_ctx* c, const gps_compressed* cg, uint32_t level, uint32_t* grp, uint32_t* label,
+                      uint32_t* wout, uint32_t* win, uint64_t* ekey_out, uint32_t* ew_out, uint64_t* ekey_in,
+                      uint32_t* ew_in);
+void run_wcheck(gps_ctx* c, const gps_compressed* cg, uint32_t level, const ChkQV* d_qv, uint32_t nf, bool fresh);
+
 // Filter only (debug entry point): candidate bitmaps after stage 0/1/2 to host.
 void run_filter_debug(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts& o, int stage,
                       uint32_t* host_bitmaps);
