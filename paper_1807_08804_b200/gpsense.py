@@ -115,6 +115,12 @@ def _load_lib():
         "gps_match_project": (S, [P, P, P, P, ctypes.c_uint32, P, P]),
         "gps_count_project": (S, [P, P, P, P, ctypes.c_uint32, P, P]),
         "gps_match_named": (S, [P, P, P, P, P, ctypes.c_uint32, P, P]),
+        "gps_compress": (S, [P, P, ctypes.c_uint32, P, P]),
+        "gps_free_compressed": (S, [P]),
+        "gps_compressed_info": (S, [P, ctypes.c_uint32, P, P, P]),
+        "gps_compressed_fetch": (S, [P, P, ctypes.c_uint32, P, P, P, P, P, P, P, P]),
+        "gps_compressed_candidates": (S, [P, P, ctypes.c_uint32, P, P]),
+        "gps_graph_attach_compressed": (S, [P, P, ctypes.c_uint32]),
         "gps_count_named": (S, [P, P, P, P, P, ctypes.c_uint32, P, P]),
         "gps_shard_recv": (S, [ctypes.c_int, ctypes.c_int, P, P, P]),
         "gps_local_comm_destroy": (S, [P]),
@@ -134,7 +140,8 @@ EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_grap
             "gps_set_profiling", "gps_debug_plan", "gps_debug_candidates", "gps_match_batch",
             "gps_count_batch", "gps_set_workers", "gps_set_slice", "gps_match_batch_host",
             "gps_result_global_rows", "gps_shard_plan", "gps_shard_recv", "gps_load_triples",
-            "gps_match_project", "gps_count_project", "gps_match_named", "gps_count_named", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
+            "gps_match_project", "gps_count_project", "gps_match_named", "gps_count_named", "gps_compress", "gps_free_compressed", "gps_compressed_info",
+            "gps_compressed_fetch", "gps_compressed_candidates", "gps_graph_attach_compressed", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
 
 
 def _check(st: int):
@@ -334,6 +341,68 @@ class Graph:
             pass
 
 
+class Compressed:
+    """f3 multi-level compression of a Graph (gps_compress); owns its device memory."""
+
+    def __init__(self, ctx: "Context", graph: Graph, handle, levels: int):
+        self.ctx, self.graph, self._h, self.levels = ctx, graph, handle, levels
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self, lv: int):
+        """(nodes, weighted out-edges, weighted in-edges) of level lv."""
+        N, eo, ei = ctypes.c_uint32(), ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib.gps_compressed_info(self._h, lv, ctypes.byref(N), ctypes.byref(eo), ctypes.byref(ei)))
+        return N.value, eo.value, ei.value
+
+    def level(self, lv: int) -> dict:
+        """Level lv (1..levels) as numpy arrays: group [n], label / w_out / w_in [nodes],
+        edges_out / edges_in as dict {(U, V): weight}."""
+        N, eo, ei = ctypes.c_uint32(), ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib.gps_compressed_info(self._h, lv, ctypes.byref(N), ctypes.byref(eo), ctypes.byref(ei)))
+        n = self.graph.n
+        grp = np.zeros(n, np.uint32)
+        lab, wo, wi = (np.zeros(N.value, np.uint32) for _ in range(3))
+        ko, wko = np.zeros(eo.value, np.uint64), np.zeros(eo.value, np.uint32)
+        ki, wki = np.zeros(ei.value, np.uint64), np.zeros(ei.value, np.uint32)
+        _check(lib.gps_compressed_fetch(self.ctx._h, self._h, lv, _addr(grp), _addr(lab), _addr(wo), _addr(wi),
+                                        _addr(ko), _addr(wko), _addr(ki), _addr(wki)))
+        def edges(k, w):
+            return {(int(x >> 32), int(x & 0xffffffff)): int(y) for x, y in zip(k.tolist(), w.tolist())}
+        return {"nodes": N.value, "group": grp, "label": lab, "w_out": wo, "w_in": wi,
+                "edges_out": edges(ko, wko), "edges_in": edges(ki, wki)}
+
+    def candidates(self, lv: int, q) -> np.ndarray:
+        """Expanded weighted candidates as a (k, n) bool array."""
+        qa = _QueryArrays(q)
+        nw = (self.graph.n + 31) // 32
+        bm = np.zeros((qa.k, nw), np.uint32)
+        _check(lib.gps_compressed_candidates(self.ctx._h, self._h, lv, ctypes.byref(qa.desc), _addr(bm)))
+        bits = np.unpackbits(bm.view(np.uint8).reshape(qa.k, -1), axis=1, bitorder="little")
+        return bits[:, :self.graph.n].astype(bool)
+
+    def attach(self, lv: int) -> None:
+        """Filters on the graph apply the weighted candidate test of level lv (0 detaches)."""
+        _check(lib.gps_graph_attach_compressed(self.graph.handle, self._h if lv else None, lv))
+
+    def free(self):
+        if self._h:
+            try:
+                lib.gps_graph_attach_compressed(self.graph.handle, None, 0)
+            except Exception:
+                pass
+            lib.gps_free_compressed(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 def shard_plan(world: int, rank: int, pairs_all, threshold: float = 1.10):
     """gps_shard_plan: (local_targets[world+1], rebalance, total)."""
     p = np.ascontiguousarray(pairs_all, np.uint64)
@@ -463,6 +532,13 @@ class Context:
                                      ctypes.byref(opts) if opts is not None else None, pj.shape[0], _addr(pj),
                                      ctypes.byref(c)))
         return int(c.value)
+
+    def compress(self, graph: Graph, deltas) -> "Compressed":
+        """gps_compress: levels 1..len(deltas) of the f3 multi-level compression (delta = 1 only)."""
+        d = np.ascontiguousarray(deltas, np.float32)
+        h = ctypes.c_void_p()
+        _check(lib.gps_compress(self._h, graph.handle, d.shape[0], _addr(d), ctypes.byref(h)))
+        return Compressed(self, graph, h, int(d.shape[0]))
 
     def match_named(self, graph: Graph, q, edge_var, project=None, opts: Optional[MatchOpts] = None) -> np.ndarray:
         """Named variable edges (f2): distinct (projection, label bindings) tuples, as a
