@@ -314,6 +314,29 @@ GPS_API gps_status gps_compressed_candidates(gps_ctx* ctx, const gps_compressed*
                                              const gps_query* q, uint32_t* bitmaps_out);
 GPS_API gps_status gps_graph_attach_compressed(gps_graph* g, const gps_compressed* cg, uint32_t level);
 
+/* ---- f4: gSparql primitives on binary relations --------
+ * A relation is a set of (a, b) pairs of u32 terms -- a property table's (subject, object)
+ * pairs.  Inputs are HOST column arrays of n pairs (duplicates allowed, any order;
+ * NULL columns only with n = 0).  Every result is a DEVICE gps_result of rows x 2 u32
+ * (a, b), lexicographically sorted and distinct (sort-based dedup); free with
+ * gps_result_free.
+ * gps_rel_join: subject/object join rule (sort-merge join): {(x, z) : (x, y) in
+ *   R, (y, z) in S}.  GPS_EUNSUPPORTED past 2^32 joined pairs.
+ * gps_rel_union / gps_rel_difference: A u B (the merge of a pattern node's rule results,
+ *   P:1232) and A \ B.
+ * gps_rel_closure: the recursive-rule loop of Algorithm P:1247-1262 (DESIGN R37) for the
+ *   transitive rule (x p y), (y p z) -> (x p z): NewT := T; while NewT: InferT := join(NewT, T)
+ *   u join(T, NewT); NewT := InferT \ T; T := T u NewT.  *rounds (may be NULL) = loop rounds;
+ *   max_rounds > 0 bounds them (GPS_EOVERFLOW past it), 0 = unbounded. */
+GPS_API gps_status gps_rel_join(gps_ctx* ctx, const uint32_t* r_src, const uint32_t* r_dst, uint64_t nr,
+                                const uint32_t* s_src, const uint32_t* s_dst, uint64_t ns, gps_result** out);
+GPS_API gps_status gps_rel_union(gps_ctx* ctx, const uint32_t* a_src, const uint32_t* a_dst, uint64_t na,
+                                 const uint32_t* b_src, const uint32_t* b_dst, uint64_t nb, gps_result** out);
+GPS_API gps_status gps_rel_difference(gps_ctx* ctx, const uint32_t* a_src, const uint32_t* a_dst, uint64_t na,
+                                      const uint32_t* b_src, const uint32_t* b_dst, uint64_t nb, gps_result** out);
+GPS_API gps_status gps_rel_closure(gps_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                                   uint32_t max_rounds, gps_result** out, uint32_t* rounds);
+
 /* rows, cols (= k), data (device or host pointer, owned by the result), on_device. */
 GPS_API gps_status gps_result_info(const gps_result* r, uint64_t* rows, uint32_t* cols,
                            const uint32_t** data, int* on_device);

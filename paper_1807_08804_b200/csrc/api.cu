@@ -130,13 +130,25 @@ static void run_sliced(gps_ctx* c, uint32_t nq, const std::function<void(gps_ctx
     }
     ensure_workers(c);
     const uint32_t W = (uint32_t)c->workers.size();
+    const uint32_t slice = std::max<uint32_t>(1, std::min<uint32_t>(c->slice ? c->slice : 64, (nq + W - 1) / W));
+    if (nq <= slice) {
+        // one slice: run it on the caller's ctx and stream.  Handing it to whichever worker is
+        // free put consecutive large single-query batches on different streams, and the memory
+        // pool then mapped fresh multi-GB blocks instead of reusing the freed ones (0.1-1 s stalls)
+        try {
+            body(c, 0, nq);
+        } catch (const Error& e) {
+            on_fail(0, nq, e.status);
+            set_last_error(e.msg);
+        }
+        return;
+    }
     cudaEvent_t start;
     GPS_CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     GPS_CK(cudaEventRecord(start, c->stream));
     std::vector<cudaEvent_t> fin(W, nullptr);
     std::vector<Error> errs;
     std::mutex emu;
-    const uint32_t slice = std::max<uint32_t>(1, std::min<uint32_t>(c->slice ? c->slice : 64, (nq + W - 1) / W));
     std::atomic<uint32_t> next{0};
     c->pool->run([&](int w) {
         gps_ctx* sc = c->workers[w];
@@ -687,6 +699,40 @@ gps_status gps_graph_attach_compressed(gps_graph* g, const gps_compressed* cg, u
         if (level > compressed_levels(cg)) fail(GPS_EINVAL, "compression level out of range");
         g->cg = cg;
         g->cg_level = level;
+    });
+}
+
+// ---- f4: gSparql relation primitives -------------------------------------
+static gps_status rel_call(gps_ctx* c, int op, const uint32_t* as, const uint32_t* ad, uint64_t na, const uint32_t* bs,
+                           const uint32_t* bd, uint64_t nb, gps_result** out) {
+    return guarded([&] {
+        if (!c || !out) fail(GPS_EINVAL, "null argument");
+        DeviceGuard dg(c->device);
+        QueryResult qr;
+        relation_op(c, op, as, ad, na, bs, bd, nb, qr);
+        *out = wrap_result(c, qr, true);
+    });
+}
+gps_status gps_rel_join(gps_ctx* c, const uint32_t* r_src, const uint32_t* r_dst, uint64_t nr, const uint32_t* s_src,
+                        const uint32_t* s_dst, uint64_t ns, gps_result** out) {
+    return rel_call(c, 0, r_src, r_dst, nr, s_src, s_dst, ns, out);
+}
+gps_status gps_rel_union(gps_ctx* c, const uint32_t* a_src, const uint32_t* a_dst, uint64_t na, const uint32_t* b_src,
+                         const uint32_t* b_dst, uint64_t nb, gps_result** out) {
+    return rel_call(c, 1, a_src, a_dst, na, b_src, b_dst, nb, out);
+}
+gps_status gps_rel_difference(gps_ctx* c, const uint32_t* a_src, const uint32_t* a_dst, uint64_t na,
+                              const uint32_t* b_src, const uint32_t* b_dst, uint64_t nb, gps_result** out) {
+    return rel_call(c, 2, a_src, a_dst, na, b_src, b_dst, nb, out);
+}
+gps_status gps_rel_closure(gps_ctx* c, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t max_rounds,
+                           gps_result** out, uint32_t* rounds) {
+    return guarded([&] {
+        if (!c || !out) fail(GPS_EINVAL, "null argument");
+        DeviceGuard dg(c->device);
+        QueryResult qr;
+        relation_closure(c, src, dst, n, max_rounds, qr, rounds);
+        *out = wrap_result(c, qr, true);
     });
 }
 

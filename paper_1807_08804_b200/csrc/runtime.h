@@ -67,6 +67,13 @@ void compressed_fetch(gps_ctx* c, const gps_compressed* cg, uint32_t level, uint
                       uint32_t* ew_in);
 void run_wcheck(gps_ctx* c, const gps_compressed* cg, uint32_t level, const ChkQV* d_qv, uint32_t nf, bool fresh);
 
+// f4 gSparql relation primitives (relate.cu): op 0 join, 1 union, 2 difference; the
+// recursive-rule loop (transitive closure).  Results: rows x 2 (a, b), sorted, distinct.
+void relation_op(gps_ctx* c, int op, const uint32_t* a_src, const uint32_t* a_dst, uint64_t na, const uint32_t* b_src,
+                 const uint32_t* b_dst, uint64_t nb, QueryResult& qr);
+void relation_closure(gps_ctx* c, const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t max_rounds,
+                      QueryResult& qr, uint32_t* rounds);
+
 // Filter only (debug entry point): candidate bitmaps after stage 0/1/2 to host.
 void run_filter_debug(gps_ctx* c, const gps_graph* g, const gps_query* q, const gps_match_opts& o, int stage,
                       uint32_t* host_bitmaps);

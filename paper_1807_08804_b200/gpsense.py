@@ -116,6 +116,10 @@ def _load_lib():
         "gps_count_project": (S, [P, P, P, P, ctypes.c_uint32, P, P]),
         "gps_match_named": (S, [P, P, P, P, P, ctypes.c_uint32, P, P]),
         "gps_compress": (S, [P, P, ctypes.c_uint32, P, P]),
+        "gps_rel_join": (S, [P, P, P, ctypes.c_uint64, P, P, ctypes.c_uint64, P]),
+        "gps_rel_union": (S, [P, P, P, ctypes.c_uint64, P, P, ctypes.c_uint64, P]),
+        "gps_rel_difference": (S, [P, P, P, ctypes.c_uint64, P, P, ctypes.c_uint64, P]),
+        "gps_rel_closure": (S, [P, P, P, ctypes.c_uint64, ctypes.c_uint32, P, P]),
         "gps_free_compressed": (S, [P]),
         "gps_compressed_info": (S, [P, ctypes.c_uint32, P, P, P]),
         "gps_compressed_fetch": (S, [P, P, ctypes.c_uint32, P, P, P, P, P, P, P, P]),
@@ -141,7 +145,8 @@ EXPORTED = ["gps_default_opts", "gps_create", "gps_destroy", "gps_load_data_grap
             "gps_count_batch", "gps_set_workers", "gps_set_slice", "gps_match_batch_host",
             "gps_result_global_rows", "gps_shard_plan", "gps_shard_recv", "gps_load_triples",
             "gps_match_project", "gps_count_project", "gps_match_named", "gps_count_named", "gps_compress", "gps_free_compressed", "gps_compressed_info",
-            "gps_compressed_fetch", "gps_compressed_candidates", "gps_graph_attach_compressed", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
+            "gps_compressed_fetch", "gps_compressed_candidates", "gps_graph_attach_compressed", "gps_rel_join",
+            "gps_rel_union", "gps_rel_difference", "gps_rel_closure", "gps_local_comm_create", "gps_local_comm_destroy", "gps_create_local_rank"]
 
 
 def _check(st: int):
@@ -532,6 +537,44 @@ class Context:
                                      ctypes.byref(opts) if opts is not None else None, pj.shape[0], _addr(pj),
                                      ctypes.byref(c)))
         return int(c.value)
+
+    # ---- f4: gSparql relation primitives ----
+    def _rel_rows(self, res) -> np.ndarray:
+        rows, cols, ptr, ondev = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_void_p(), ctypes.c_int()
+        lib.gps_result_info(res, ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(ptr), ctypes.byref(ondev))
+        a = np.zeros((rows.value, 2), np.uint32)
+        if rows.value:
+            import torch
+            t = torch.as_tensor(_DeviceRows(None, rows.value, 2, ptr.value), device=f"cuda:{self.device}")
+            a = t.cpu().numpy().copy()
+        lib.gps_result_free(res)
+        return a
+
+    def _rel2(self, fn, a_src, a_dst, b_src, b_dst) -> np.ndarray:
+        cols = [np.ascontiguousarray(x, np.uint32) for x in (a_src, a_dst, b_src, b_dst)]
+        res = ctypes.c_void_p()
+        _check(fn(self._h, _addr(cols[0]), _addr(cols[1]), cols[0].shape[0], _addr(cols[2]), _addr(cols[3]),
+                  cols[2].shape[0], ctypes.byref(res)))
+        return self._rel_rows(res)
+
+    def rel_join(self, r_src, r_dst, s_src, s_dst) -> np.ndarray:
+        """{(x, z) : (x, y) in R, (y, z) in S} as sorted distinct (rows, 2) uint32."""
+        return self._rel2(lib.gps_rel_join, r_src, r_dst, s_src, s_dst)
+
+    def rel_union(self, a_src, a_dst, b_src, b_dst) -> np.ndarray:
+        return self._rel2(lib.gps_rel_union, a_src, a_dst, b_src, b_dst)
+
+    def rel_difference(self, a_src, a_dst, b_src, b_dst) -> np.ndarray:
+        return self._rel2(lib.gps_rel_difference, a_src, a_dst, b_src, b_dst)
+
+    def rel_closure(self, src, dst, max_rounds: int = 0):
+        """Transitive closure by the recursive-rule loop: (rows, rounds)."""
+        s = np.ascontiguousarray(src, np.uint32)
+        d = np.ascontiguousarray(dst, np.uint32)
+        res, it = ctypes.c_void_p(), ctypes.c_uint32()
+        _check(lib.gps_rel_closure(self._h, _addr(s), _addr(d), s.shape[0], int(max_rounds), ctypes.byref(res),
+                                   ctypes.byref(it)))
+        return self._rel_rows(res), int(it.value)
 
     def compress(self, graph: Graph, deltas) -> "Compressed":
         """gps_compress: levels 1..len(deltas) of the f3 multi-level compression (delta = 1 only)."""

@@ -17,5 +17,5 @@ echo "cfg4 capture rc $?"
 TRAFFIC_PREFIX=cfg2: python scripts/summarize_profiles.py ${R}_cfg2 /tmp/launches_$R.csv /tmp/prof_${R}_cfg2.ncu-rep > /dev/null
 TRAFFIC_PREFIX=cfg4: python scripts/summarize_profiles.py ${R}_cfg4 /tmp/launches_$R.csv /tmp/prof_${R}_cfg4.ncu-rep > /dev/null
 cp profiles/${R}_* profiles/traffic.json gpurun_out/profiles/
-cp /tmp/prof_${R}_cfg4.ncu-rep /tmp/prof_${R}_cfg2.ncu-rep gpurun_out/ 2>/dev/null
+ls -la /tmp/prof_${R}_cfg4.ncu-rep /tmp/prof_${R}_cfg2.ncu-rep
 ls -la gpurun_out/profiles | tail; du -sh gpurun_out
