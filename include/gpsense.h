@@ -174,7 +174,8 @@ GPS_API gps_status gps_count(gps_ctx* ctx, const gps_graph* g, const gps_query* 
 /* Batched execution of nq independent queries (the QA-batch use, BASELINE
  * configs[4]): the library runs them concurrently on a pool of worker host
  * threads, each owning a CUDA stream and scratch (set its size with
- * gps_set_workers; default 2).  results[i] / counts[i] / statuses[i] (statuses
+ * gps_set_workers; default 2); a batch that fits one slice (gps_set_slice) runs on the
+ * ctx's own stream instead.  results[i] / counts[i] / statuses[i] (statuses
  * may be NULL) as for the single-query calls: every entry of statuses is written,
  * a query that failed has results[i] = NULL.  A query whose candidate-edge tables
  * alone exceed the 32-bit table limits fails with GPS_EOVERFLOW without affecting

@@ -68,4 +68,25 @@ th = [threading.Thread(target=body, args=(r,)) for r in range(2)]
 [t.join() for t in th]
 union = oracle.sort_rows(np.concatenate([res[0][0], res[1][0]]))
 assert np.array_equal(union, oracle.match(og1, q))
+# f2 named edges, f3 compression (attached), f4 relations
+from oracle import compress as ocomp, relate  # noqa: E402
+for s_ in seeds[:3]:
+    g, q = corpus.instance(s_)
+    og = oracle.OracleGraph(g)
+    if oracle.count(og, q, limit=20_000) == oracle.ELIMIT:
+        continue
+    G = ctx.load_graph(g)
+    ev = [i % 2 if l == -1 else -1 for i, (_, _, l) in enumerate(q.edges)]
+    assert np.array_equal(ctx.match_named(G, q, ev), oracle.match_named(g, og, q, ev))
+    cg = ctx.compress(G, [1.0, 1.0])
+    cg.attach(2)
+    check(G, og, q)
+    cg.free()
+rng = np.random.default_rng(1)
+a, b = rng.integers(0, 30, 80).astype(np.uint32), rng.integers(0, 30, 80).astype(np.uint32)
+assert np.array_equal(ctx.rel_join(a, b, b, a), relate.join(a, b, b, a))
+assert np.array_equal(ctx.rel_closure(a, b)[0], relate.closure(a, b)[0])
+os.environ["GPS_JOIN_NO_BULK"] = "1"
+check(G1, og1, triangle_tail((-1, -1, -1, -1)))
+del os.environ["GPS_JOIN_NO_BULK"]
 print(f"sanitize target ok: {nchk} checked match+count pairs")
