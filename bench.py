@@ -308,6 +308,10 @@ def main():
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.Stream(device=dev)
     sharded = CONFIG == 4 and world > 1   # row-sharded join of the same queries (strong scaling)
+    if CONFIG in (3, 4) and "GPS_POOL_RESERVE_BYTES" not in os.environ:
+        # multi-GB join tables: map the library's memory pool once up front (gps_create reads it)
+        # instead of growing it mid-step (0.1-1.3 s stalls in the first steps of a process)
+        os.environ["GPS_POOL_RESERVE_BYTES"] = str(96 << 30)
     if sharded:
         comm = dist.group.WORLD._get_backend(dev)._comm_ptr()
         ctx = gpsense.Context(local, stream=stream, nccl_comm=comm, rank=rank, world=world)

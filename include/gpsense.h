@@ -141,6 +141,11 @@ typedef struct {
 
 GPS_API gps_status gps_default_opts(gps_match_opts* opts);
 
+/* Creates a ctx on opts->device.  The library allocates stream-ordered from a private memory
+ * pool per device that keeps up to 3/4 of the device memory cached after frees
+ * (GPS_POOL_KEEP_BYTES overrides).  GPS_POOL_RESERVE_BYTES (environment, read when the first
+ * ctx of a device is created) maps that many bytes into the pool up front -- workloads with
+ * multi-GB join tables then sub-allocate instead of growing the pool mid-query. */
 GPS_API gps_status gps_create(const gps_ctx_opts* opts, gps_ctx** out);
 /* Frees the ctx and the device memory of any gps_result it still owns. */
 GPS_API gps_status gps_destroy(gps_ctx* ctx);

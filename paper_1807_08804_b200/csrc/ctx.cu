@@ -103,6 +103,25 @@ cudaMemPool_t device_pool(int dev) {
         if (prev >= 0 && prev != dev) cudaSetDevice(prev);
     }
     GPS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    // GPS_POOL_RESERVE_BYTES: map that much physical memory into the pool once, up front (one
+    // allocation, freed at once and kept below the release threshold), so large joins later
+    // sub-allocate instead of mapping fresh blocks mid-step (0.1-1 s stalls in a fresh process)
+    if (const char* r = std::getenv("GPS_POOL_RESERVE_BYTES")) {
+        const uint64_t want = std::min<uint64_t>(std::strtoull(r, nullptr, 10), keep);
+        if (want) {
+            int prev = -1;
+            cudaGetDevice(&prev);
+            if (prev != dev) cudaSetDevice(dev);
+            void* p = nullptr;
+            if (cudaMallocFromPoolAsync(&p, want, pool, 0) == cudaSuccess) {
+                (void)cudaFreeAsync(p, 0);
+                (void)cudaStreamSynchronize(0);
+            } else {
+                (void)cudaGetLastError();
+            }
+            if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+        }
+    }
     pools[dev] = pool;
     return pool;
 }
