@@ -77,6 +77,16 @@ typedef struct {
                                 join; NULL = single GPU.  world = 1 with a communicator
                                 runs the sharded path (and its collectives) on one rank */
     int rank, world;         /* this process's rank and the number of ranks of nccl_comm */
+    /* Optional caller allocator for the library's stream-ordered device memory (scratch, join
+     * tables, results), e.g. torch's caching allocator: dev_alloc(bytes, stream,
+     * user) returns a 16-byte-aligned device pointer usable in stream order on `stream` (NULL =
+     * out of memory -> GPS_ENOMEM); dev_free(ptr, stream, user) returns it, in stream order
+     * after the work enqueued on `stream` so far.  Both NULL = the library's private memory
+     * pool.  Called from the calling thread and from batch worker threads (with the worker's
+     * stream), possibly concurrently.  The graph arrays themselves are plain cudaMalloc. */
+    void* (*dev_alloc)(size_t bytes, void* stream, void* user);
+    void (*dev_free)(void* ptr, void* stream, void* user);
+    void* alloc_user;
 } gps_ctx_opts;
 
 /* Data graph as CSR ("nodes array ... edges array ... two additional

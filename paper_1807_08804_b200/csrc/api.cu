@@ -100,6 +100,9 @@ static void ensure_workers(gps_ctx* c) {
         gps_ctx* sc = new gps_ctx();
         ctx_init(sc, c->device, nullptr);
         sc->prof_mask = c->prof_mask;
+        sc->dev_alloc = c->dev_alloc;
+        sc->dev_free = c->dev_free;
+        sc->alloc_user = c->alloc_user;
         c->workers.push_back(sc);
     }
     c->pool = new WorkerPool((int)n);
@@ -222,6 +225,12 @@ gps_status gps_create(const gps_ctx_opts* opts, gps_ctx** out) {
         gps_ctx* c = new gps_ctx();
         try {
             ctx_init(c, dev, opts ? (cudaStream_t)opts->stream : nullptr);
+            if (opts && (!opts->dev_alloc) != (!opts->dev_free)) fail(GPS_EINVAL, "dev_alloc and dev_free go together");
+            if (opts) {
+                c->dev_alloc = opts->dev_alloc;
+                c->dev_free = opts->dev_free;
+                c->alloc_user = opts->alloc_user;
+            }
             if (opts && opts->nccl_comm) c->comm = make_nccl_comm(opts->nccl_comm, opts->rank, opts->world);
         } catch (...) {
             delete c;

@@ -144,7 +144,13 @@ void* dmalloc(gps_ctx* c, size_t bytes) {
     fault_injection();
     void* p = nullptr;
     // +16 bytes: bulk copies (bulk.cuh) round staged ranges out to 16-byte boundaries
-    cudaError_t e = cudaMallocFromPoolAsync(&p, ((bytes + 15) & ~size_t(15)) + 16, c->pool_mem, c->stream);
+    const size_t padded = ((bytes + 15) & ~size_t(15)) + 16;
+    if (c->dev_alloc) {
+        p = c->dev_alloc(padded, (void*)c->stream, c->alloc_user);
+        if (!p) fail(GPS_ENOMEM, "caller allocator: device allocation of " + std::to_string(bytes) + " bytes failed");
+        return p;
+    }
+    cudaError_t e = cudaMallocFromPoolAsync(&p, padded, c->pool_mem, c->stream);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
         fail(GPS_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed");
@@ -152,11 +158,13 @@ void* dmalloc(gps_ctx* c, size_t bytes) {
     return p;
 }
 void dfree(gps_ctx* c, void* p) {
-    if (p) (void)cudaFreeAsync(p, c->stream);
+    if (!p) return;
+    if (c->dev_free) c->dev_free(p, (void*)c->stream, c->alloc_user);
+    else (void)cudaFreeAsync(p, c->stream);
 }
 
 DevBlock::~DevBlock() {
-    if (p && c) (void)cudaFreeAsync(p, c->stream);
+    if (p && c) dfree(c, p);
 }
 Block make_block(gps_ctx* c, size_t bytes) {
     auto b = std::make_shared<DevBlock>();

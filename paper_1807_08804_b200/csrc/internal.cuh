@@ -79,6 +79,10 @@ struct gps_ctx {
     int nsm = 148;
     cudaStream_t stream = nullptr;
     cudaMemPool_t pool_mem = nullptr;        // the library's memory pool of this device (ctx.cu device_pool)
+    // optional caller allocator (gps_ctx_opts.dev_alloc / dev_free), inherited by batch workers
+    void* (*dev_alloc)(size_t, void*, void*) = nullptr;
+    void (*dev_free)(void*, void*, void*) = nullptr;
+    void* alloc_user = nullptr;
     bool own_stream = false;
     uint32_t prof_mask = 0;
     gps_stats stats{};

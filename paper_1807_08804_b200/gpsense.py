@@ -40,9 +40,14 @@ class GpsError(RuntimeError):
         self.status = status
 
 
+DEV_ALLOC = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+DEV_FREE = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class CtxOpts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p),
-                ("rank", ctypes.c_int), ("world", ctypes.c_int)]
+                ("rank", ctypes.c_int), ("world", ctypes.c_int), ("dev_alloc", DEV_ALLOC),
+                ("dev_free", DEV_FREE), ("alloc_user", ctypes.c_void_p)]
 
 
 class CsrDesc(ctypes.Structure):
@@ -449,8 +454,23 @@ class Context:
     local_comm/rank: in-process ranks sharing one device (tests)."""
 
     def __init__(self, device: int = 0, stream=None, workers: int = 0, nccl_comm=None, rank: int = 0,
-                 world: int = 1, local_comm: Optional[LocalComm] = None):
+                 world: int = 1, local_comm: Optional[LocalComm] = None, torch_allocator: bool = False):
         o = CtxOpts(device, None, None, int(rank), int(world))
+        if torch_allocator:
+            # the library's device memory comes from torch's caching allocator (gps_ctx_opts.dev_alloc)
+            import torch
+
+            def _alloc(nbytes, stream, user):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), device, int(stream or 0))
+                except Exception:   # out of memory: the library reports GPS_ENOMEM
+                    return None
+
+            def _free(ptr, stream, user):
+                torch.cuda.caching_allocator_delete(int(ptr))
+
+            self._alloc_cbs = (DEV_ALLOC(_alloc), DEV_FREE(_free))   # kept alive with the ctx
+            o.dev_alloc, o.dev_free = self._alloc_cbs
         if stream is not None:
             o.stream = int(getattr(stream, "cuda_stream", stream))
         if nccl_comm is not None:

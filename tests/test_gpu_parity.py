@@ -433,3 +433,37 @@ def test_recovers_after_allocation_failures(gps, ctx, cfg1, monkeypatch):
         assert np.array_equal(_rows(ctx.match(G, q)), want), n
         assert ctx.count(G, q2) == want2, n
     assert failed > 10   # the hook reached many allocation sites
+
+
+def test_torch_caching_allocator(gps, cfg2):
+    """gps_ctx_opts.dev_alloc / dev_free: with torch's caching allocator the
+    library's device memory (scratch, tables, results) is torch memory -- results equal the
+    oracle's, batch workers use it too, and a held result shows in torch.cuda.memory_allocated."""
+    import torch
+    c = gps.Context(0, torch_allocator=True)
+    try:
+        for seed in range(0, 200, 25):
+            g, q = _instance(seed)
+            og = oracle.OracleGraph(g)
+            try:
+                if oracle.count(og, q, limit=200_000) == oracle.ELIMIT:
+                    continue
+            except ValueError:
+                continue
+            _check(c, c.load_graph(g), og, q)
+        g, G, data = cfg2[0], c.load_graph(cfg2[0]), cfg2[2]
+        qs = [Query.from_json(d["query"]) for d in data["queries"][:12]]
+        c.set_workers(2)
+        c.set_slice(3)
+        counts = c.count_batch(G, qs)
+        assert counts.tolist() == [d["oracle_count"] for d in data["queries"][:12]]
+        torch.cuda.synchronize()
+        before = torch.cuda.memory_allocated(0)
+        big = max(data["queries"], key=lambda d: d["oracle_count"])
+        t = c.match(G, Query.from_json(big["query"]))
+        torch.cuda.synchronize()
+        assert t.shape[0] == big["oracle_count"]
+        assert torch.cuda.memory_allocated(0) >= before + t.shape[0] * t.shape[1] * 4
+        del t
+    finally:
+        c.close()
