@@ -330,8 +330,8 @@ void ctx_release(gps_ctx* c) {
         r->ctx = nullptr;
     }
     c->results.clear();
-    if (c->lb_status) cudaFreeAsync(c->lb_status, c->stream);
-    if (c->lb_ctr) cudaFreeAsync(c->lb_ctr, c->stream);
+    dfree(c, c->lb_status);   // dmalloc'd: the caller's allocator when one is set
+    dfree(c, c->lb_ctr);
     c->lb_status = nullptr;
     c->lb_ctr = nullptr;
     cudaStreamSynchronize(c->stream);

@@ -179,6 +179,7 @@ inline void launch(gps_ctx* c, int cls, dim3 grid, dim3 block, size_t smem, Kern
         e1 = ctx_event(c);
         GPS_CK(cudaEventRecord(e0, c->stream));
     }
+    (void)cudaGetLastError();   // a non-sticky error left by another caller's API call is not ours
     k<<<grid, block, smem, c->stream>>>(args...);
     GPS_CK(cudaGetLastError());
     if (timed) {
