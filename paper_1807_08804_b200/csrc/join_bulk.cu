@@ -40,7 +40,7 @@ struct BHdr {                // window descriptor, written by the producer befor
 };
 
 // Per-buffer layout (bytes): header, poff, woff, s0, imask, M, meta.
-template <uint32_t WOUT>
+template <uint32_t WOUT, bool ST = (WOUT <= 4)>
 struct BLay {
     static constexpr uint32_t w = WOUT - 1;
     static __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -58,11 +58,15 @@ struct BLay {
     // output's address offset mod 16 so the aligned interior goes out as one bulk store
     // (wide rows, WOUT > kStagedMax: no staging -- it would halve the resident blocks -- but one
     // (new value, window row) pair per output row and word-parallel 16-byte stores)
-    static constexpr bool STAGED = WOUT <= 4;
-    static constexpr uint32_t STG = STAGED ? kBCh * WOUT + 4 : kBCh;   // words
+    // (wide rows are staged in ONE buffer -- two would cost resident blocks -- whose previous
+    // bulk store must have finished reading before it is rewritten; ST = false: no staging, one
+    // (new value, window row) pair per output row and word-parallel 16-byte stores)
+    static constexpr bool STAGED = ST;
+    static constexpr uint32_t NSTG = (ST && WOUT <= 4) ? 2 : 1;
+    static constexpr uint32_t STG = STAGED ? kBCh * WOUT + 4 : 2 * kBCh;   // words
     static constexpr size_t OUT = 2 * BUF;
     static __host__ __device__ size_t jobs_bytes(uint32_t nj) { return a16(8ull * (nj + 1) + 8ull * nj + 4ull * nj + nj); }
-    static __host__ __device__ size_t bytes(uint32_t nj) { return jobs_bytes(nj) + OUT + 2 * a16(4ull * STG) + 16; }
+    static __host__ __device__ size_t bytes(uint32_t nj) { return jobs_bytes(nj) + OUT + NSTG * a16(4ull * STG) + 16; }
     // STAGED = false: the two staging buffers hold the kBCh uint2 (value, row) entries instead
 };
 
@@ -109,9 +113,9 @@ __device__ __forceinline__ void issue_window(const JoinStep& a, char* buf, uint6
     mbar_arrive_expect_tx(bar, tx);   // the header writes above are released by this arrive
 }
 
-template <uint32_t WOUT>
+template <uint32_t WOUT, bool ST>
 __global__ void __launch_bounds__(kBT, 3) k_join_bulk(const __grid_constant__ JoinStep a) {
-    using L = BLay<WOUT>;
+    using L = BLay<WOUT, ST>;
     constexpr uint32_t w = L::w;
     extern __shared__ __align__(16) char s_dyn[];
     uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);                     // [nj+1] first row of each job
@@ -251,7 +255,10 @@ __global__ void __launch_bounds__(kBT, 3) k_join_bulk(const __grid_constant__ Jo
             if (cp + kBCh < wp1) items(cp + kBCh, nv_, nwi, nj_, ncand);
             // staging buffer ob was last read by the bulk store of the chunk before the previous one:
             // the issuing thread waits for that read before the scan's barriers release the writers
-            if (L::STAGED && threadIdx.x == 0) bulk_wait_read_le1();
+            if (L::STAGED && threadIdx.x == 0) {
+                if (L::NSTG == 2) bulk_wait_read_le1();
+                else bulk_wait_read_all();
+            }
             uint32_t tot;
             uint32_t lpos = block_excl_scan(mine, &tot);
             auto rotate = [&]() {
@@ -373,7 +380,7 @@ __global__ void __launch_bounds__(kBT, 3) k_join_bulk(const __grid_constant__ Jo
                     g[o] = stg[shift + o];
                 }
             }
-            ob ^= 1u;
+            if (L::NSTG == 2) ob ^= 1u;
             // s_base is rewritten only after the next chunk's scan barriers
             rotate();
         }
@@ -383,27 +390,36 @@ __global__ void __launch_bounds__(kBT, 3) k_join_bulk(const __grid_constant__ Jo
     if (threadIdx.x == 0) bulk_wait_all();   // the bulk stores have completed before the block exits
 }
 
-template <uint32_t WOUT>
+template <uint32_t WOUT, bool ST>
 static void launch_bulk(gps_ctx* c, const JoinStep& s, uint64_t P) {
-    using L = BLay<WOUT>;
-    allow_smem((const void*)k_join_bulk<WOUT>, (int)L::bytes(kMaxJobsPerLaunch));
+    using L = BLay<WOUT, ST>;
+    allow_smem((const void*)k_join_bulk<WOUT, ST>, (int)L::bytes(kMaxJobsPerLaunch));
     const uint64_t chunks = (P + kBCh - 1) / kBCh;
-    const uint32_t wave = resident_grid(c, (const void*)k_join_bulk<WOUT>, kBT, L::bytes(64));
+    const uint32_t wave = resident_grid(c, (const void*)k_join_bulk<WOUT, ST>, kBT, L::bytes(64));
     const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)wave, chunks));
-    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kBT), L::bytes(s.nj), k_join_bulk<WOUT>, s);
+    launch(c, GPS_K_JOIN_WRITE, dim3(G), dim3(kBT), L::bytes(s.nj), k_join_bulk<WOUT, ST>, s);
+}
+
+template <uint32_t WOUT>
+static void launch_bulk_w(gps_ctx* c, const JoinStep& s, uint64_t P) {
+    // wide rows: word-parallel stores; GPS_JOIN_WIDE_STAGED=1 stages them in one buffer for bulk
+    // stores instead (measured 3 % slower on config 2: the staging costs a resident block)
+    const char* e = std::getenv("GPS_JOIN_WIDE_STAGED");
+    if (e && *e == '1') launch_bulk<WOUT, true>(c, s, P);
+    else launch_bulk<WOUT, false>(c, s, P);
 }
 
 bool join_bulk_enabled() { return std::getenv("GPS_JOIN_NO_BULK") == nullptr; }
 
 void run_join_bulk_write(gps_ctx* c, const JoinStep& s, uint64_t P) {
     switch (s.wout) {
-        case 2: return launch_bulk<2>(c, s, P);
-        case 3: return launch_bulk<3>(c, s, P);
-        case 4: return launch_bulk<4>(c, s, P);
-        case 5: return launch_bulk<5>(c, s, P);
-        case 6: return launch_bulk<6>(c, s, P);
-        case 7: return launch_bulk<7>(c, s, P);
-        case 8: return launch_bulk<8>(c, s, P);
+        case 2: return launch_bulk<2, true>(c, s, P);
+        case 3: return launch_bulk<3, true>(c, s, P);
+        case 4: return launch_bulk<4, true>(c, s, P);
+        case 5: return launch_bulk_w<5>(c, s, P);
+        case 6: return launch_bulk_w<6>(c, s, P);
+        case 7: return launch_bulk_w<7>(c, s, P);
+        case 8: return launch_bulk_w<8>(c, s, P);
         default: fail(GPS_EINVAL, "internal: bulk join row width out of range");
     }
 }

@@ -111,12 +111,12 @@ def test_random_corpus_other_join_paths(ctx, seed, env, monkeypatch):
     _check(ctx, ctx.load_graph(g), og, q)
 
 
-@pytest.mark.parametrize("env", ["GPS_JOIN_NO_BULK=1"])
+@pytest.mark.parametrize("env", ["GPS_JOIN_NO_BULK=1", "GPS_JOIN_WIDE_STAGED=1"])
 @pytest.mark.parametrize("seed", range(0, 200, 5))
 def test_random_corpus_kernel_variants(ctx, seed, env, monkeypatch):
-    """Same corpus through the kernel variant the default path replaced: the closing-free
+    """Same corpus through the kernel variants the default path replaced: the closing-free
     write loading its row inputs as it goes (k_join_fast instead of the bulk-staged
-    k_join_bulk)."""
+    k_join_bulk), and wide output rows staged + bulk-stored instead of stored word-parallel."""
     k, v = env.split("=")
     monkeypatch.setenv(k, v)
     g, q = _instance(seed)
