@@ -24,7 +24,8 @@ namespace gps {
 constexpr int kPT = 256;    // threads per block
 constexpr int kPI = 4;      // pairs per thread per chunk
 constexpr int kPW = 1024;   // EC: rows staged per chunk (keys are never empty: a chunk always fits)
-constexpr int kJW = 1024;   // join: rows staged (single buffer; fan-out can be 1)
+constexpr int kJW = 256;    // join: rows staged (single buffer; a chunk meeting more rows is cut at the window end).
+                             // 1024 rows (56 KB of row metadata) held k_join<2> to 2 blocks per SM
 constexpr uint32_t kStageW = kJoinStageCols;   // join: stage rows of width <= 8 in shared memory
 
 
