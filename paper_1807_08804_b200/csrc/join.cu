@@ -24,7 +24,7 @@ namespace gps {
 constexpr int kPT = 256;    // threads per block
 constexpr int kPI = 4;      // pairs per thread per chunk
 constexpr int kPW = 1024;   // EC: rows staged per chunk (keys are never empty: a chunk always fits)
-constexpr int kJW = 128;    // join: rows staged (single buffer; a chunk meeting more rows is cut at the window end).
+constexpr int kJW = 64;     // join: rows staged (single buffer; a chunk meeting more rows is cut at the window end).
                              // 1024 rows (56 KB of row metadata) held k_join<2> to 2 blocks per SM
 constexpr uint32_t kStageW = kJoinStageCols;   // join: stage rows of width <= 8 in shared memory
 
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(kPT) k_join(const __grid_constant__ JoinStep a
 // per input row, its values (with the output permutation of a final step packed
 // in nibbles), EC segment start and flags, so injectivity, closing checks and the
 // output row come from shared memory instead of per-pair global loads.
-constexpr int kJVW = 256;   // window rows
+constexpr int kJVW = 128;   // window rows
 struct JVMeta {
     uint32_t s0;            // EC segment start
     uint32_t job;
