@@ -114,7 +114,7 @@ __device__ __forceinline__ void issue_window(const JoinStep& a, char* buf, uint6
 }
 
 template <uint32_t WOUT, bool ST>
-__global__ void __launch_bounds__(kBT, 3) k_join_bulk(const __grid_constant__ JoinStep a) {
+__global__ void __launch_bounds__(kBT, (WOUT >= 5 ? 4 : 3)) k_join_bulk(const __grid_constant__ JoinStep a) {
     using L = BLay<WOUT, ST>;
     constexpr uint32_t w = L::w;
     extern __shared__ __align__(16) char s_dyn[];
