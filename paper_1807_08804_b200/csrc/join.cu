@@ -230,7 +230,7 @@ constexpr uint64_t kSegBigRows = 1u << 22;
 // searches advanced in lockstep), the per-job output totals, and the scan of the
 // rows' written outputs (woff) -- two look-backs in two warps.
 template <bool FAST, int kSegRows>
-__global__ void __launch_bounds__(256) k_join_seg(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
+__global__ void __launch_bounds__(256, (FAST && kSegRows == 4) ? 4 : 5) k_join_seg(const __grid_constant__ JoinStep a, LbScratch lb, uint32_t ntiles,
                                                   uint32_t epoch) {
     constexpr int kSegTile = 256 * kSegRows;
     extern __shared__ __align__(16) char s_dyn[];
