@@ -303,7 +303,8 @@ GPS_API gps_status gps_count_named(gps_ctx* ctx, const gps_graph* g, const gps_q
  *   max over the parts U' of U of w(U', V').  deltas [n_levels] (host) must each be 1.0 on the
  *   device: GPS_EUNSUPPORTED for delta < 1 (a similarity join, not built), GPS_EINVAL outside
  *   (0, 1] or n_levels outside 1..16; GPS_EUNSUPPORTED when keys need more than 64 bits.
- *   The compression owns device memory until gps_free_compressed; g must outlive it.
+ *   The compression owns device memory until gps_free_compressed (which also detaches it from
+ *   g if attached); g must outlive it.
  * gps_compressed_info: nodes and weighted out-/in-edges of level (1..n_levels).
  * gps_compressed_fetch: copies level `level` to HOST arrays (each may be NULL):
  *   group [n] (node of every data vertex: M(U) = {x : group[x] = U}), label / w_out / w_in

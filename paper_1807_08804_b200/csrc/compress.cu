@@ -518,6 +518,11 @@ gps_compressed* compress_graph(gps_ctx* c, const gps_graph* g, uint32_t nlev, co
 
 void free_compressed(gps_compressed* cg) {
     if (!cg) return;
+    if (cg->g && cg->g->cg == cg) {   // still attached: detach so the graph never points at freed levels
+        gps_graph* g = const_cast<gps_graph*>(cg->g);
+        g->cg = nullptr;
+        g->cg_level = 0;
+    }
     for (void* p : cg->mem) cudaFree(p);
     delete cg;
 }
