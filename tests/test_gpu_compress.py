@@ -173,3 +173,16 @@ def test_errors(gps, ctx):
     with pytest.raises(gps.GpsError):
         cg.attach(2)                    # only one level
     cg.free()
+
+
+def test_free_while_attached_detaches(gps, ctx):
+    """gps_free_compressed on an attached compression detaches it: later matches run without it."""
+    g, q = corpus.instance(10)
+    og = oracle.OracleGraph(g)
+    G = ctx.load_graph(g)
+    cg = ctx.compress(G, [1.0])
+    cg.attach(1)
+    gps._check(gps.lib.gps_free_compressed(cg.handle))   # the C call alone, no Python-side detach
+    cg._h = None
+    rows = oracle.sort_rows(ctx.match(G, q).cpu().numpy())
+    assert np.array_equal(rows, oracle.match(og, q))
