@@ -14,6 +14,11 @@ timeout 1500 ncu -f --set full --import-source on --clock-control none \
     -k regex:"k_check|k_collect|k_explore|k_ec|k_join" -c 40 -o /tmp/prof_${R}_cfg4 python scripts/ncu_cfg4.py \
     > gpurun_out/profiles/${R}_ncu_cfg4.log 2>&1
 echo "cfg4 capture rc $?"
+PASSES=1 timeout 1200 ncu -f --set full --import-source on --clock-control none \
+    -k regex:"k_join|k_explore|k_collect|k_ec" -c 40 -o /tmp/prof_${R}_cfg3 python scripts/ncu_cfg3.py \
+    > gpurun_out/profiles/${R}_ncu_cfg3.log 2>&1
+echo "cfg3 capture rc $?"
+TRAFFIC_PREFIX=cfg3: python scripts/summarize_profiles.py ${R}_cfg3 /tmp/launches_$R.csv /tmp/prof_${R}_cfg3.ncu-rep > /dev/null
 TRAFFIC_PREFIX=cfg2: python scripts/summarize_profiles.py ${R}_cfg2 /tmp/launches_$R.csv /tmp/prof_${R}_cfg2.ncu-rep > /dev/null
 TRAFFIC_PREFIX=cfg4: python scripts/summarize_profiles.py ${R}_cfg4 /tmp/launches_$R.csv /tmp/prof_${R}_cfg4.ncu-rep > /dev/null
 cp profiles/${R}_* profiles/traffic.json gpurun_out/profiles/
