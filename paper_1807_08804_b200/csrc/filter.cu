@@ -240,9 +240,9 @@ void run_collect(gps_ctx* c, const DevGraph& g, const CollectJob* d_jobs, uint32
 }
 
 // -------------------------------------------------------------- a4 explore
-constexpr int kET = 256;
+constexpr int kET = 128;
 constexpr int kEI = 4;   // pairs per thread per chunk (8 measured slower on configs 2 and 4)
-constexpr int kEW = 512;
+constexpr int kEW = 256;
 
 struct ExMeta {             // one row (key vertex) of an explore job, staged per chunk
     uint32_t key, base, skip, pad;
@@ -256,7 +256,7 @@ __device__ __forceinline__ uint64_t ex_pairs(const ExploreJob& J, bool* s_side) 
     return ps < pa ? ps : pa;
 }
 
-__global__ void __launch_bounds__(kET, 5) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
+__global__ void __launch_bounds__(kET, 10) k_explore(DevGraph g, const ExploreJob* __restrict__ jobs, uint32_t nj,
                                                 unsigned long long* bytes_acc, unsigned long long* dbg) {
     extern __shared__ __align__(16) char s_dyn[];
     uint64_t* s_jp = reinterpret_cast<uint64_t*>(s_dyn);          // [nj+1] job pair prefix
