@@ -467,3 +467,22 @@ def test_torch_caching_allocator(gps, cfg2):
         del t
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("k", [13, 16, 20, 24, 28, 32])
+@pytest.mark.parametrize("induced", [False, True])
+def test_large_queries_k13_to_32(gps, ctx, k, induced, monkeypatch):
+    """Queries of 13-32 vertices (BFS trees and induced cyclic queries on the config-1 graph):
+    rows of 13-32 columns exercise the wide-row join paths -- the k_join<2> single pass, the
+    count -> exact allocation -> write path (GPS_SINGLE_PASS_BYTES=0) and the depth-first path
+    under a 4 KB row budget -- each with full sorted-set equality with the oracle and the count."""
+    g = config_graph(1)
+    og = oracle.OracleGraph(g)
+    q = bfs_query(g, k, seed=(200 if induced else 100), induced=induced, max_children=3)
+    if oracle.count(og, q, limit=300_000) == oracle.ELIMIT:
+        pytest.skip("too many embeddings for the oracle")
+    G = ctx.load_graph(g)
+    _check(ctx, G, og, q)
+    _check(ctx, G, og, q, gps.default_opts(row_budget_bytes=4096))
+    monkeypatch.setenv("GPS_SINGLE_PASS_BYTES", "0")
+    _check(ctx, G, og, q)
