@@ -235,9 +235,13 @@ __global__ void __launch_bounds__(256, (FAST && kSegRows == 4) ? 4 : 5) k_join_s
     constexpr int kSegTile = 256 * kSegRows;
     extern __shared__ __align__(16) char s_dyn[];
     uint64_t* s_jr = reinterpret_cast<uint64_t*>(s_dyn);   // [nj+1] first row of every job
+    const uint32_t** s_jbn = reinterpret_cast<const uint32_t**>(s_jr + a.nj + 1);   // [nj] FAST: Bn of every job
     __shared__ uint64_t s_pre[3];
     const uint32_t tile = lb_ticket(lb.ctr, ntiles);
-    for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) s_jr[j] = a.jobs[j].row0;
+    for (uint32_t j = threadIdx.x; j < a.nj; j += blockDim.x) {
+        s_jr[j] = a.jobs[j].row0;
+        if (FAST) s_jbn[j] = a.jobs[j].Bn;
+    }
     if (threadIdx.x == 0) s_jr[a.nj] = a.R;
     __syncthreads();
     const uint64_t r0 = (uint64_t)tile * kSegTile + (uint64_t)threadIdx.x * kSegRows;
@@ -298,6 +302,20 @@ __global__ void __launch_bounds__(256, (FAST && kSegRows == 4) ? 4 : 5) k_join_s
                 t[x] = on ? __ldg(rp + qc) : 0u;
                 lo[x] = ss;
                 hi[x] = on ? ss + ll : ss;
+            }
+            // a row value that is not a candidate of the new vertex cannot be in the segment (every
+            // extension segment is a subset of that candidate set): one bitmap probe instead of a
+            // binary search for most values
+#pragma unroll
+            for (int x = 0; x < 8; x++) {
+                if (hi[x] - lo[x] <= 16) continue;   // a short search costs no more than the probe
+                const uint32_t qi = (q0 + x) / a.w;
+                uint32_t job = 0;
+#pragma unroll
+                for (int i = 0; i < kSegRows; i++)
+                    if (qi == (uint32_t)i) job = jrow[i];
+                const uint32_t* bn = s_jbn[job];
+                if (bn != nullptr && !bit_test(bn, t[x])) hi[x] = lo[x];
             }
             bool more = true;
             while (more) {
@@ -387,7 +405,7 @@ void run_join_seg(gps_ctx* c, const JoinStep& s) {
     const uint64_t nt = (s.R + tile - 1) / tile;
     if (nt > 0x7fffffffull) fail(GPS_EOVERFLOW, "join table too large");
     LbScratch lb = lb_scratch(c, 2, (uint32_t)nt);
-    const size_t smem = sizeof(uint64_t) * (s.nj + 1);
+    const size_t smem = sizeof(uint64_t) * (s.nj + 1) + sizeof(void*) * s.nj;
     const uint32_t ep = lb_next_epoch(c);
     if (!s.fast)
         launch(c, GPS_K_JOIN_LEN, dim3((uint32_t)nt), dim3(256), smem, k_join_seg<false, 4>, s, lb, (uint32_t)nt, ep);

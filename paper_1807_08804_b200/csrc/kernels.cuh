@@ -141,6 +141,7 @@ struct JoinJob {           // one query's share of a join step
     const uint32_t* Bx;    // key endpoint bitmap + rank prefix
     const uint32_t* rpx;
     const uint32_t* ec_off;  // EC key offsets of the extension arc
+    const uint32_t* Bn;    // candidate bitmap of the new vertex: every extension segment is a subset of it
     unsigned long long* total;  // per-query output count
     uint32_t x_col;
     uint32_t nclose, close0;

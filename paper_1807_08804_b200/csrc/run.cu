@@ -567,6 +567,7 @@ void join_deep(Chunk& ch, QS* q, size_t s, const uint32_t* M, uint64_t R, const 
     j.Bx = ch.Bp(*q, st.key);
     j.rpx = ch.rpp(*q, st.key);
     j.ec_off = ec_off_of(q->ecjob[st.arc][st.key_dir]);
+    j.Bn = ch.Bp(*q, st.nv);
     j.total = jt.as<unsigned long long>();
     j.x_col = (uint32_t)q->col_of[st.key];
     std::vector<CloseChk> cl;
@@ -910,6 +911,7 @@ void run_chunk(gps_ctx* c, const gps_graph* g, std::vector<QS*>& qsv, bool count
                 j.Bx = ch.Bp(*q, st.key);
                 j.rpx = ch.rpp(*q, st.key);
                 j.ec_off = ec_off_of(q->ecjob[st.arc][st.key_dir]);
+                j.Bn = ch.Bp(*q, st.nv);
                 j.total = jt.as<unsigned long long>() + i;
                 j.x_col = (uint32_t)q->col_of[st.key];
                 j.close0 = (uint32_t)cl.size();
